@@ -1,0 +1,327 @@
+"""Benchmark: batched 1-D complex FFT N=2^16 x 4096 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one forward transform of the whole batch (4096 signals of 65536
+complex64 = 2 GiB in, 2 GiB out), inputs resident in HBM; inputs are larger
+than L2 (126 MB) so no flush is needed.  Rank 0 prints ONE JSON line.
+
+* value: FFT GFLOP/s, 5*N*log2(N) per transform, whole job (all ranks).
+* roofline: HBM-bound; achieved = 16*N bytes per transform / kernel time.
+* e2e: same metric through the public API (apps.fft.fft_batch) with pinned
+  host buffers, H2D + transform + D2H inside the timed region.
+* cpu_baseline: the oracle restatement of the reference fft()
+  (oracle/fft_oracle.py) on the host, bounded sample, rank 0 only.
+* secondary.compression: C4 (8192^2 gray, block transform + quantise +
+  order, 256-entry codebook) MPixel/s on the same GPU.
+Multi-GPU (torchrun): every rank runs the full per-GPU batch (weak
+scaling, no collective on the data path); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N = 1 << 16
+BATCH = 4096
+FLOPS_PER_TRANSFORM = 5.0 * N * 16  # 5 N log2 N
+BYTES_PER_TRANSFORM = 16.0 * N      # complex64 read once + written once
+METRIC = "FFT GFLOP/s (5N·log2N)"
+WORKLOAD = "batched 1D complex fp32 FFT N=2^16, batch 4096, on 1 B200 (configs[1])"
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle restatement of the reference fft(); tests/bench only)
+
+def _cpu_chunk(args):
+    seed, count = args
+    from oracle import fft_oracle
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((count, N), dtype=np.float32)
+         + 1j * rng.standard_normal((count, N), dtype=np.float32)).astype(np.complex64)
+    t0 = time.perf_counter()
+    for row in x:
+        fft_oracle.fft(row)
+    return time.perf_counter() - t0, count
+
+
+def cpu_baseline(threads: int, seconds: float = 12.0) -> dict:
+    """Reference-algorithm FFT on host cores: per-signal fft() calls, bounded sample."""
+    import multiprocessing as mp
+    per_worker = 4
+    with mp.get_context("spawn").Pool(threads) as pool:
+        pool.map(_cpu_chunk, [(1, 1)] * threads)  # warm imports
+        t0 = time.perf_counter()
+        done = 0
+        seed = 100
+        while time.perf_counter() - t0 < seconds:
+            res = pool.map(_cpu_chunk, [(seed + i, per_worker) for i in range(threads)])
+            seed += threads
+            done += sum(c for _, c in res)
+        wall = time.perf_counter() - t0
+    value = done * FLOPS_PER_TRANSFORM / wall / 1e9
+    return {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"{done} of the 4096 signals (N=2^16), reference fft() algorithm "
+                      f"(oracle/fft_oracle.py: host bit-reversal, binary32 dft8 leaves, binary64 "
+                      f"butterflies), {threads} processes, {wall:.1f} s wall"}
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference_arm(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    steps = []
+    for _ in range(args.warmup + args.steps):
+        steps.append(cpu_baseline(threads, seconds=max(5.0, 60.0 / (args.warmup + args.steps))))
+    timed = steps[args.warmup:]
+    value = statistics.median(s["value"] for s in timed)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": BATCH * FLOPS_PER_TRANSFORM / (value * 1e9) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "n": N, "batch": BATCH},
+            "cpu_baseline": {**timed[-1], "value": value},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_1203_4938_b200 import ops
+    from paper_1203_4938_b200.apps import fft as afft
+    from paper_1203_4938_b200.apps import imgc as aimgc
+
+    gen = torch.Generator(device=dev).manual_seed(42 + rank)
+    x = torch.randn((BATCH, N), dtype=torch.complex64, device=dev, generator=gen)
+    y = torch.empty_like(x)
+    plan = ops.fft_plan(1, N, 1, BATCH, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(3, args.warmup)):
+        plan.execute(x, y, BATCH, stream)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all0.record(stream)
+        for i in range(args.steps):
+            starts[i].record(stream)
+            plan.execute(x, y, BATCH, stream)
+            stops[i].record(stream)
+        t_all1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    total_ms = t_all0.elapsed_time(t_all1)
+    kernel_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
+    total_ms = max_over_ranks(total_ms, world)
+    ms_per_step = total_ms / args.steps
+    value = world * BATCH * FLOPS_PER_TRANSFORM * args.steps / (total_ms / 1e3) / 1e9
+    avg_kernel_ms = sum(kernel_ms) / len(kernel_ms)
+    pk = peaks()
+    achieved = BATCH * BYTES_PER_TRANSFORM / (avg_kernel_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "fft_ncu_summary.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    # e2e through the public API with pinned host buffers (H2D + FFT + D2H)
+    e2e_steps = max(1, min(args.steps, 3))
+    host_in = torch.empty((BATCH, N), dtype=torch.complex64, pin_memory=True)
+    host_in.copy_(x.cpu())
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    afft.fft_batch(host_in, N, out=host_out)  # warm
+    torch.cuda.synchronize()
+    barrier(world)
+    e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        afft.fft_batch(host_in, N, out=host_out)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - e0, world)
+    e2e_value = world * BATCH * FLOPS_PER_TRANSFORM * e2e_steps / e2e_s / 1e9
+
+    # secondary: C4 compression throughput (fused encode kernel, 8192^2 gray)
+    h = w = 8192
+    img = torch.randint(0, 256, (h, w), dtype=torch.uint8, device=dev, generator=gen)
+    cb = torch.randn((256, 16), dtype=torch.float32, device=dev, generator=gen)
+    cb = (cb - cb.mean(1, keepdim=True)) / cb.std(1, unbiased=False, keepdim=True)
+    nb = (h // 4) * (w // 4)
+    rec = torch.empty(nb * 3, dtype=torch.uint8, device=dev)
+    cbp = torch.empty(nb, dtype=torch.uint8, device=dev)
+    crp = torch.empty(nb, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        ops.encode(img, 1, h, w, cb, rec, cbp, crp)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    csteps = max(3, min(args.steps, 10))
+    c0.record(stream)
+    for _ in range(csteps):
+        ops.encode(img, 1, h, w, cb, rec, cbp, crp)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    c_ms = max_over_ranks(c0.elapsed_time(c1) / csteps, world)
+    comp_bytes = h * w + nb * 5
+    compression = {"metric": "compression MPixel/s", "value": round(world * h * w / (c_ms / 1e3) / 1e6, 2),
+                   "unit": "MPixel/s", "ms_per_image": round(c_ms, 4),
+                   "config": "8192x8192 gray (R=G=B), 256-entry codebook, exact VQ, bit-exact with the "
+                             "reference (configs[3])",
+                   "roofline": {"bound": "fp32", "hbm_frac": round(comp_bytes / (c_ms / 1e3) / 1e9
+                                                                    / pk["hbm_gbs"], 5),
+                                "vq_flop_per_block": 12288}}
+
+    if rank == 0:
+        cpu = cpu_baseline(len(os.sched_getaffinity(0)), seconds=10.0) if world == 1 and not args.no_cpu \
+            else None
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": N, "batch": BATCH, "parallelism": f"batch-shard x{world}",
+                       "l2": "inputs 2 GiB > L2, no flush", "kernel": plan.description},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                         "traffic": traffic, "peak_source": pk["source"],
+                         "algorithmic_bytes_per_launch": BATCH * BYTES_PER_TRANSFORM,
+                         "avg_launch_ms": round(avg_kernel_ms, 4)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 2), "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": BATCH * N * 8, "d2h_bytes_per_step": BATCH * N * 8,
+                    "api": "apps.fft.fft_batch(pinned host tensor)"},
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+            "secondary": {"compression": compression},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

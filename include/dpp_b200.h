@@ -1,0 +1,143 @@
+/*
+ * dpp_b200.h — C ABI of the B200 (sm_100a) FFT and block-compression nodes.
+ *
+ * This is the drop-in boundary.  The reference (arXiv 1203.4938 platform,
+ * package `dpp`) has no FFI: its per-node execution point is the Python call
+ *   _run_instance(kernel, items, inputs, outputs, parallelism, budget, record)
+ *   (/root/reference/pkg/src/dpp/engine.py:218-235)
+ * which hands flat little-endian scalar buffers to the lockstep
+ * interpreter run_lanes (kernel/interp.py:471-485).  Every function below
+ * replaces that call for one node kind, taking the same flat buffers as
+ * device pointers plus the caller's cudaStream_t (passed as void*).  The host
+ * binding is ctypes (paper_1203_4938_b200/_lib.py); INTEGRATION.md shows the
+ * stub a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers owned by the caller (PyTorch
+ *    allocates).  No entry point allocates device memory except plan
+ *    creation (twiddle tables, freed by *_destroy).
+ *  - Every launch is asynchronous on `stream` (cudaStream_t; NULL = legacy).
+ *  - Return 0 (DPP_OK) or an error code; dpp_last_error() returns the
+ *    thread-local message of the last failure.  Host mapping:
+ *      DPP_EINVAL  -> PlanError / ValueError       (errors.py:62, fft.py:134-139)
+ *      DPP_ECUDA   -> EngineRuntimeError (DeviceError)   (errors.py:66-81)
+ *      DPP_ENCCL   -> EngineRuntimeError (DeviceError)
+ *  - Entry points are re-entrant; plans are immutable after creation and may
+ *    be shared by threads (engine.py:292-317 runs chunks on thread pools).
+ *  - Complex data is interleaved (re, im) binary32, exactly the reference's
+ *    complex64 view (fft.py:160-163).
+ */
+#ifndef DPP_B200_H
+#define DPP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPP_ABI_VERSION 1
+
+#define DPP_OK 0
+#define DPP_EINVAL 1
+#define DPP_ECUDA 2
+#define DPP_ENCCL 3
+#define DPP_ENOTSUP 4
+
+/* Library identity / diagnostics. */
+int dpp_abi_version(void);
+const char* dpp_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * FFT node
+ * ------------------------------------------------------------------------ */
+
+typedef struct dpp_fft_plan dpp_fft_plan;
+
+/* Create a forward, unnormalised complex-to-complex plan.
+ *   rank 1: `batch` contiguous transforms of n0 points (n1 ignored).
+ *   rank 2: `batch` contiguous n0 x n1 row-major 2-D transforms.
+ * Sizes must be powers of two >= 2 (same rule as FftPlan, fft.py:133-139).
+ * *workspace_bytes receives the scratch the execute call needs (may be 0).
+ * Replaces: apps/fft.py:150-174 `fft` (host bit-reversal fft.py:159, leaf
+ * DFT node fft.py:162, host binary64 butterflies fft.py:165-173). */
+int dpp_fft_plan_create(dpp_fft_plan** plan, int rank, int64_t n0, int64_t n1,
+                        int64_t batch, size_t* workspace_bytes);
+
+/* Human-readable kernel schedule of a plan (for logs and bench lines). */
+int dpp_fft_plan_describe(const dpp_fft_plan* plan, char* buf, size_t len);
+
+/* Execute: in/out hold batch * n0 (* n1) complex64; in == out is allowed. */
+int dpp_fft_c2c_forward(const dpp_fft_plan* plan, const float* in, float* out,
+                        void* workspace, void* stream);
+
+/* Same plan, different batch count (<= the planned batch). */
+int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* out,
+                              int64_t batch, void* workspace, void* stream);
+
+void dpp_fft_plan_destroy(dpp_fft_plan* plan);
+
+/* Leaf DFT node dft{2,4,8} (apps/fft.py:86-123): one dense 2^k-point DFT per
+ * work-item over float{2^(k+1)} vectors whose lanes sit at bit-reversed
+ * offsets.  Arithmetic is the generated body's exactly: binary32, terms in
+ * source order, left-to-right, no contraction -> bit-identical to the
+ * reference engine.  x, y: items * 2^(k+1) floats. */
+int dpp_fft_leaf(int k, const float* x, float* y, int64_t items, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Block-compression node (apps/imgc.py)
+ * ------------------------------------------------------------------------ */
+
+/* Drop-in replacements of the four reference nodes, same io, bit-exact.
+ *   ycbcr     imgc.py:128-140   rgba: pixels*4 u8 -> yl, cb, cr: pixels f32
+ *   boxdown   imgc.py:143-152   blk: blocks*16 f32 -> avg: blocks f32
+ *   gradient  imgc.py:155-166   lum: items f32 -> dx, dy: items f32
+ *             (width/height are the constants baked into the generated body;
+ *              items is the chunk's work-item count; a read past the chunk
+ *              is a fault exactly as the interpreter's bounds check,
+ *              kernel/interp.py:222-284: DPP_EINVAL + first faulting item)
+ *   vqnearest imgc.py:169-185   blk, cbk: items*16 f32 -> idx: items i32
+ *             (the chunk's cbk holds codebook_size centroids, as the
+ *              reference tiles it per chunk, imgc.py:406-423) */
+int dpp_imgc_ycbcr(const uint8_t* rgba, float* yl, float* cb, float* cr,
+                   int64_t pixels, void* stream);
+int dpp_imgc_boxdown(const float* blk, float* avg, int64_t blocks, void* stream);
+int dpp_imgc_gradient(const float* lum, float* dx, float* dy, int64_t width,
+                      int64_t height, int64_t items, int64_t* fault_item, void* stream);
+int dpp_imgc_vqnearest(const float* blk, const float* cbk, int32_t* idx, int64_t items,
+                       int64_t cbk_items, int codebook_size, void* stream);
+
+/* Fused encoder: forward block transform + quantisation + ordering in one
+ * kernel per tile (imgc.py:343-403 steps 1,2,5 and the quantisers, with the
+ * codebook as input).
+ *   px          batch images, each height x width pixels of `channels` u8
+ *               (1 = gray meaning R=G=B, 3 = RGB, 4 = RGBA with A ignored),
+ *               rows `row_stride` bytes apart, images `image_stride` apart.
+ *   codebook    per image n_cb x 16 f32 (codebook_stride floats apart; 0 =
+ *               one codebook shared by every image).
+ *   sigma_min   deviation floor of the normalisation (imgc.py:345, 387; 0.25).
+ *   records     per image 3 * blocks u8, interleaved (mean, sigma idx, index)
+ *               in raster block order (imgc.py:295-305).
+ *   cb_plane, cr_plane   per image (h/4) x (w/4) u8.
+ *   block_grad  nullable; per image blocks f32 mean gradient magnitude
+ *               (imgc.py:378-381), the k-means training filter.
+ *   norm32      nullable; per image blocks x 16 normalised f32 blocks
+ *               (imgc.py:396, the vq input).
+ * Output strides per image: 3*blocks, blocks, blocks, blocks*16. */
+int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t width,
+                    int64_t row_stride, int64_t image_stride, int64_t batch,
+                    const float* codebook, int n_cb, int64_t codebook_stride, double sigma_min,
+                    uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
+                    float* block_grad, float* norm32, void* stream);
+
+/* Inverse (imgc.py:426-439), for round-trip tests on device. */
+int dpp_imgc_decode(const uint8_t* records, const uint8_t* cb_plane, const uint8_t* cr_plane,
+                    const float* codebook, int n_cb, int64_t height, int64_t width,
+                    uint8_t* rgb, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DPP_B200_H */

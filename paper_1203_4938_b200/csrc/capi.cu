@@ -1,0 +1,117 @@
+// extern "C" surface of libdpp_b200.so (declared in include/dpp_b200.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "fft_plan.cuh"
+
+struct dpp_fft_plan {
+  dpp::FftPlan impl;
+};
+
+namespace dpp {
+
+static thread_local char g_last_error[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+void fft_plan_release(FftPlan* p) {
+  if (!p) return;
+  if (p->tw_a) cudaFree(p->tw_a);
+  if (p->tw_b) cudaFree(p->tw_b);
+  if (p->ctw_a) cudaFree(p->ctw_a);
+  if (p->ctw_b) cudaFree(p->ctw_b);
+  p->tw_a = p->tw_b = p->ctw_a = p->ctw_b = nullptr;
+  if (p->rows) {
+    fft_plan_release(p->rows);
+    delete p->rows;
+    p->rows = nullptr;
+  }
+}
+
+}  // namespace dpp
+
+extern "C" {
+
+int dpp_abi_version(void) { return DPP_ABI_VERSION; }
+
+const char* dpp_last_error(void) { return dpp::g_last_error; }
+
+int dpp_fft_plan_create(dpp_fft_plan** plan, int rank, int64_t n0, int64_t n1, int64_t batch,
+                        size_t* workspace_bytes) {
+  if (!plan) return dpp::fail(DPP_EINVAL, "plan pointer is NULL");
+  *plan = nullptr;
+  if (rank != 1 && rank != 2) return dpp::fail(DPP_EINVAL, "rank must be 1 or 2, got %d", rank);
+  if (batch < 0) return dpp::fail(DPP_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
+  auto* h = new (std::nothrow) dpp_fft_plan();
+  if (!h) return dpp::fail(DPP_EINVAL, "out of host memory");
+  h->impl.rank = rank;
+  h->impl.n0 = n0;
+  h->impl.n1 = rank == 2 ? n1 : 1;
+  h->impl.batch = batch;
+  cudaGetDevice(&h->impl.device);
+  const int rc = rank == 1 ? dpp::fft1d_plan_init(&h->impl) : dpp::fft2d_plan_init(&h->impl);
+  if (rc != DPP_OK) {
+    dpp::fft_plan_release(&h->impl);
+    delete h;
+    return rc;
+  }
+  if (workspace_bytes) *workspace_bytes = 0;
+  *plan = h;
+  return DPP_OK;
+}
+
+int dpp_fft_plan_describe(const dpp_fft_plan* plan, char* buf, size_t len) {
+  if (!plan || !buf || len == 0) return dpp::fail(DPP_EINVAL, "bad describe arguments");
+  snprintf(buf, len, "%s", plan->impl.desc);
+  return DPP_OK;
+}
+
+int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* out, int64_t batch,
+                              void* workspace, void* stream) {
+  (void)workspace;
+  if (!plan) return dpp::fail(DPP_EINVAL, "plan is NULL");
+  if (batch < 0 || batch > plan->impl.batch)
+    return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch,
+                     (long long)plan->impl.batch);
+  if (batch > 0 && (!in || !out)) return dpp::fail(DPP_EINVAL, "NULL data pointer");
+  auto s = static_cast<cudaStream_t>(stream);
+  const auto* src = reinterpret_cast<const float2*>(in);
+  auto* dst = reinterpret_cast<float2*>(out);
+  return plan->impl.rank == 1 ? dpp::fft1d_execute(&plan->impl, src, dst, batch, s)
+                              : dpp::fft2d_execute(&plan->impl, src, dst, batch, s);
+}
+
+int dpp_fft_c2c_forward(const dpp_fft_plan* plan, const float* in, float* out, void* workspace,
+                        void* stream) {
+  if (!plan) return dpp::fail(DPP_EINVAL, "plan is NULL");
+  return dpp_fft_c2c_forward_batch(plan, in, out, plan->impl.batch, workspace, stream);
+}
+
+void dpp_fft_plan_destroy(dpp_fft_plan* plan) {
+  if (!plan) return;
+  dpp::fft_plan_release(&plan->impl);
+  delete plan;
+}
+
+int dpp_fft_leaf(int k, const float* x, float* y, int64_t items, void* stream) {
+  if (items < 0) return dpp::fail(DPP_EINVAL, "items must be >= 0");
+  return dpp::leaf_execute(k, x, y, items, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// Shared helpers for the sm_100a library: error convention, complex math,
+// in-register DFTs.  Error convention follows include/dpp_b200.h: every entry
+// point returns DPP_OK or a code and records a message retrievable with
+// dpp_last_error() (thread-local), mapped on the host onto the reference's
+// PlanError / EngineRuntimeError (/root/reference/pkg/src/dpp/errors.py:62-81).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <string>
+
+#include "../../include/dpp_b200.h"
+
+namespace dpp {
+
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+#define DPP_CUDA_CHECK(expr)                                                         \
+  do {                                                                               \
+    cudaError_t err__ = (expr);                                                      \
+    if (err__ != cudaSuccess)                                                        \
+      return ::dpp::fail(DPP_ECUDA, "%s failed: %s (%s:%d)", #expr,                  \
+                         cudaGetErrorString(err__), __FILE__, __LINE__);             \
+  } while (0)
+
+#define DPP_LAUNCH_CHECK(what)                                                       \
+  do {                                                                               \
+    cudaError_t err__ = cudaGetLastError();                                          \
+    if (err__ != cudaSuccess)                                                        \
+      return ::dpp::fail(DPP_ECUDA, "launch of %s failed: %s", what,                 \
+                         cudaGetErrorString(err__));                                 \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// complex helpers (float2 = re, im).  FFT arithmetic is tolerance-checked, so
+// contraction to FFMA is allowed here; the bit-exact codec uses __f*_rn.
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// multiply by -i
+__device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a.x); }
+
+// W_8^1 = (1 - i)/sqrt2, W_8^3 = (-1 - i)/sqrt2
+__device__ __forceinline__ float2 cmul_w8_1(float2 a) {
+  const float h = 0.70710678118654752f;
+  return make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+}
+__device__ __forceinline__ float2 cmul_w8_3(float2 a) {
+  const float h = 0.70710678118654752f;
+  return make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
+}
+
+// ---------------------------------------------------------------------------
+// Natural-order in-register DFTs of size 2, 4, 8, 16 (forward, unnormalised).
+
+__device__ __forceinline__ void dft2(float2& a, float2& b) {
+  float2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+// in: x0..x3 natural, out: natural
+__device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
+  float2 s02 = cadd(x0, x2), d02 = csub(x0, x2);
+  float2 s13 = cadd(x1, x3), d13 = cmul_mi(csub(x1, x3));
+  x0 = cadd(s02, s13);
+  x2 = csub(s02, s13);
+  x1 = cadd(d02, d13);
+  x3 = csub(d02, d13);
+}
+
+__device__ __forceinline__ void dft8(float2 (&v)[8]) {
+  // even/odd split: E = DFT4(v0,v2,v4,v6), O = DFT4(v1,v3,v5,v7)
+  dft4(v[0], v[2], v[4], v[6]);
+  dft4(v[1], v[3], v[5], v[7]);
+  float2 o1 = cmul_w8_1(v[3]);
+  float2 o2 = cmul_mi(v[5]);
+  float2 o3 = cmul_w8_3(v[7]);
+  float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  float2 o0 = v[1];
+  v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
+  v[1] = cadd(e1, o1); v[5] = csub(e1, o1);
+  v[2] = cadd(e2, o2); v[6] = csub(e2, o2);
+  v[3] = cadd(e3, o3); v[7] = csub(e3, o3);
+}
+
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
+  // n = 4*n1 + n0 ; k = k1 + 4*k2
+  // step 1: A[n0][k1] = DFT4_{n1}(v[4 n1 + n0]) stored back in v[4 k1 + n0]
+  dft4(v[0], v[4], v[8], v[12]);
+  dft4(v[1], v[5], v[9], v[13]);
+  dft4(v[2], v[6], v[10], v[14]);
+  dft4(v[3], v[7], v[11], v[15]);
+  // step 2: twiddle W16^{n0 k1}; element (n0, k1) lives at v[4 k1 + n0]
+  const float c1 = 0.92387953251128676f, s1 = 0.38268343236508977f, h = 0.70710678118654752f;
+  v[5] = cmul(v[5], make_float2(c1, -s1));     // n0=1,k1=1 : W^1
+  v[9] = cmul_w8_1(v[9]);                       // n0=1,k1=2 : W^2
+  v[13] = cmul(v[13], make_float2(s1, -c1));   // n0=1,k1=3 : W^3
+  v[6] = cmul_w8_1(v[6]);                       // n0=2,k1=1 : W^2
+  v[10] = cmul_mi(v[10]);                       // n0=2,k1=2 : W^4
+  v[14] = cmul_w8_3(v[14]);                     // n0=2,k1=3 : W^6
+  v[7] = cmul(v[7], make_float2(s1, -c1));     // n0=3,k1=1 : W^3
+  v[11] = cmul_w8_3(v[11]);                     // n0=3,k1=2 : W^6
+  v[15] = cmul(v[15], make_float2(-c1, s1));   // n0=3,k1=3 : W^9
+  (void)h;
+  // step 3: X[k1 + 4 k2] = DFT4_{n0}(A[n0][k1]) ; inputs v[4k1 + n0], outputs to
+  // natural position k1 + 4 k2 — compute per k1 then scatter through temps.
+  float2 r[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    float2 a0 = v[4 * k1 + 0], a1 = v[4 * k1 + 1], a2 = v[4 * k1 + 2], a3 = v[4 * k1 + 3];
+    dft4(a0, a1, a2, a3);
+    r[k1 + 0] = a0; r[k1 + 4] = a1; r[k1 + 8] = a2; r[k1 + 12] = a3;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = r[i];
+}
+
+template <int R>
+__device__ __forceinline__ void dft_r(float2 (&v)[R]);
+template <> __device__ __forceinline__ void dft_r<1>(float2 (&)[1]) {}
+template <> __device__ __forceinline__ void dft_r<2>(float2 (&v)[2]) { dft2(v[0], v[1]); }
+template <> __device__ __forceinline__ void dft_r<4>(float2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
+template <> __device__ __forceinline__ void dft_r<8>(float2 (&v)[8]) { dft8(v); }
+template <> __device__ __forceinline__ void dft_r<16>(float2 (&v)[16]) { dft16(v); }
+
+__host__ __device__ constexpr int ilog2(long long n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+}  // namespace dpp

@@ -1,0 +1,77 @@
+// Block-level Stockham FFT building block shared by the 1-D and 2-D kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace dpp {
+
+// ---------------------------------------------------------------------------
+// Block-level Stockham FFT.
+//
+// Size-M transform computed by T = M/R threads.  On entry thread j holds
+// v[i] = x[j + T*i]; on exit v[i] = X[j + T*i] (natural order, strided).
+// Pass with current sub-transform size Ns (Govindaraju et al. 2008):
+//   twiddle v[i] *= W_{Ns*R}^{i*(j mod Ns)}; DFT_R; write to
+//   (j div Ns)*Ns*R + (j mod Ns) + i*Ns; read back v[i] = buf[j + T*i].
+// When log2 M is not a multiple of log2 R, one leading radix-2^(rem) pass is
+// done on the registers as it arrives from memory (no exchange before it).
+// `map` turns a logical element index into a shared-memory offset; `tw` is a
+// W_{M*tw_step} table so that W_M^e = tw[e*tw_step].
+
+struct MapIdentity {
+  __device__ __forceinline__ int operator()(int e) const { return e; }
+};
+struct MapPad16 {  // one float2 of padding per 16 elements: breaks stride-16 bank aliasing
+  __device__ __forceinline__ int operator()(int e) const { return e + (e >> 4); }
+};
+
+template <int M, int R, class Map>
+__device__ __forceinline__ void block_fft(float2 (&v)[R], int j, float2* buf, Map map,
+                                          const float2* tw, int tw_step) {
+  constexpr int T = M / R;
+  constexpr int LOGM = ilog2(M);
+  constexpr int LOGR = ilog2(R);
+  constexpr int REM = LOGM % LOGR;
+  constexpr int NPASS = LOGM / LOGR;
+  constexpr int NS0 = 1 << REM;
+  if constexpr (REM != 0) {
+    constexpr int r = 1 << REM;
+    constexpr int S = R / r;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      float2 u[r];
+#pragma unroll
+      for (int q = 0; q < r; ++q) u[q] = v[s + q * S];
+      dft_r<r>(u);
+      const int jp = j + T * s;
+#pragma unroll
+      for (int q = 0; q < r; ++q) buf[map(jp * r + q)] = u[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[map(j + T * i)];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int pass = 0; pass < NPASS; ++pass) {
+    const int ns = NS0 << (LOGR * pass);
+    const int jm = j & (ns - 1);
+    if (ns > 1) {
+      const int unit = jm * (M / (ns * R));
+#pragma unroll
+      for (int i = 1; i < R; ++i) v[i] = cmul(v[i], tw[(i * unit) * tw_step]);
+    }
+    dft_r<R>(v);
+    if (ns * R < M) {
+      const int base = (j - jm) * R + jm;
+#pragma unroll
+      for (int i = 0; i < R; ++i) buf[map(base + i * ns)] = v[i];
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = buf[map(j + T * i)];
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace dpp

@@ -1,0 +1,40 @@
+// Plan object behind the opaque dpp_fft_plan handle.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+struct dpp_fft_plan;  // public opaque name (include/dpp_b200.h)
+
+namespace dpp {
+
+struct FftPlan {
+  enum Kind { SMALL = 1, CLUSTER = 2 };
+  int rank = 1;
+  int64_t n0 = 0, n1 = 0, batch = 0;  // rank 1: n0 points; rank 2: n0 rows x n1 cols
+  int device = 0;
+  // 1-D schedule along a row (rank 1: the transform; rank 2: the row pass)
+  int kind = 0;
+  int64_t n1a = 0, n2a = 0;  // cluster split n = n1a * n2a
+  int cluster = 1;
+  float2* tw_a = nullptr;    // coarse twiddles (W_n for SMALL, W_max(n1a,n2a) for CLUSTER)
+  float2* tw_b = nullptr;    // fine twiddles W_n^lo
+  // rank 2: column pass schedule
+  FftPlan* rows = nullptr;   // 1-D plan along n1 (row pass)
+  int col_kind = 0;
+  int64_t col_split = 0;     // column length n0 = col_split * (n0 / col_split)
+  int col_cluster = 1;
+  int col_width = 0;         // columns per tile
+  float2* ctw_a = nullptr;
+  float2* ctw_b = nullptr;
+  char desc[256] = {0};
+};
+
+int fft1d_plan_init(FftPlan* p);
+int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
+int fft2d_plan_init(FftPlan* p);
+int fft2d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
+void fft_plan_release(FftPlan* p);
+int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
+
+}  // namespace dpp

@@ -1,0 +1,444 @@
+// Block-compression node for sm_100a (apps/imgc.py of the reference).
+//
+// Everything here is bit-exact with the reference on the same inputs: binary32
+// arithmetic is written with __f*_rn intrinsics (no FMA contraction, left to
+// right as the kernel-language bodies evaluate, kernel/interp.py:348-358), the
+// block statistics use binary64 with numpy's 8-accumulator pairwise order for
+// 16-wide reductions (r_m = a_m + a_{m+8}, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))),
+// and quantisers use round-half-even rint before clipping (imgc.py:375, 400-401).
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace dpp {
+
+// BT.601 constants as the kernel bodies spell them (imgc.py:131-134); each
+// literal parses to the same binary32 as the reference's float32(float(text)).
+#define K_YR 0.299f
+#define K_YG 0.587f
+#define K_YB 0.114f
+#define K_BR 0.168736f
+#define K_BG 0.331264f
+#define K_RG 0.418688f
+#define K_RB 0.081312f
+
+struct YCC {
+  float y, cb, cr;
+};
+
+// imgc.py:132-134: yl = 0.299f*r + 0.587f*g + 0.114f*b;
+// cb = 128 - 0.168736f*r - 0.331264f*g + 0.5f*b; cr = 128 + 0.5f*r - 0.418688f*g - 0.081312f*b
+__device__ __forceinline__ YCC ycc(float r, float g, float b) {
+  YCC o;
+  o.y = __fadd_rn(__fadd_rn(__fmul_rn(K_YR, r), __fmul_rn(K_YG, g)), __fmul_rn(K_YB, b));
+  o.cb = __fadd_rn(__fsub_rn(__fsub_rn(128.0f, __fmul_rn(K_BR, r)), __fmul_rn(K_BG, g)), __fmul_rn(0.5f, b));
+  o.cr = __fsub_rn(__fsub_rn(__fadd_rn(128.0f, __fmul_rn(0.5f, r)), __fmul_rn(K_RG, g)), __fmul_rn(K_RB, b));
+  return o;
+}
+__device__ __forceinline__ float luma(float r, float g, float b) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(K_YR, r), __fmul_rn(K_YG, g)), __fmul_rn(K_YB, b));
+}
+
+// numpy pairwise sum of 16 (binary32 / binary64)
+__device__ __forceinline__ float pw16f(const float (&a)[16]) {
+  float r[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) r[m] = __fadd_rn(a[m], a[m + 8]);
+  return __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                   __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+}
+__device__ __forceinline__ double pw16d(const double (&a)[16]) {
+  double r[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) r[m] = __dadd_rn(a[m], a[m + 8]);
+  return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+}
+
+// clip(rint(x), 0, 255) -> u8 (numpy rint is round-half-even)
+__device__ __forceinline__ uint8_t q8f(float x) { return (uint8_t)fminf(fmaxf(rintf(x), 0.f), 255.f); }
+__device__ __forceinline__ uint8_t q8d(double x) { return (uint8_t)fmin(fmax(rint(x), 0.0), 255.0); }
+
+// squared distance exactly as dot(d, d) of vq_program (imgc.py:176-177,
+// interp.py:417-419): d = b - c in binary32, products, pairwise-16 sum.
+__device__ __forceinline__ float vq_dist(const float (&b)[16], const float4* c) {
+  float p[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 cv = c[q];
+    float d0 = __fsub_rn(b[4 * q + 0], cv.x), d1 = __fsub_rn(b[4 * q + 1], cv.y);
+    float d2 = __fsub_rn(b[4 * q + 2], cv.z), d3 = __fsub_rn(b[4 * q + 3], cv.w);
+    p[4 * q + 0] = __fmul_rn(d0, d0);
+    p[4 * q + 1] = __fmul_rn(d1, d1);
+    p[4 * q + 2] = __fmul_rn(d2, d2);
+    p[4 * q + 3] = __fmul_rn(d3, d3);
+  }
+  return pw16f(p);
+}
+
+// "float best = 3.402823e38f" (imgc.py:173) parses to 0x7f7ffffd, not FLT_MAX
+#define VQ_BEST_INIT __int_as_float(0x7f7ffffd)
+
+// ---------------------------------------------------------------------------
+// drop-in nodes
+
+__global__ void ycbcr_kernel(const uchar4* __restrict__ rgba, float* __restrict__ yl,
+                             float* __restrict__ cb, float* __restrict__ cr, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uchar4 p = rgba[i];
+  const YCC o = ycc((float)p.x, (float)p.y, (float)p.z);
+  yl[i] = o.y;
+  cb[i] = o.cb;
+  cr[i] = o.cr;
+}
+
+// avg[i] = (b.s0 + b.s1 + ... + b.sf) * 0.0625f  (imgc.py:143-148), sequential sum
+__global__ void boxdown_kernel(const float4* __restrict__ blk, float* __restrict__ avg, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 v = blk[4 * i + q];
+    acc = q == 0 ? v.x : __fadd_rn(acc, v.x);
+    acc = __fadd_rn(acc, v.y);
+    acc = __fadd_rn(acc, v.z);
+    acc = __fadd_rn(acc, v.w);
+  }
+  avg[i] = __fmul_rn(acc, 0.0625f);
+}
+
+// gradient_program(width, height), imgc.py:155-166.  fault[0] collects the
+// first work-item whose dx read leaves the chunk, fault[1] the same for dy.
+__global__ void gradient_kernel(const float* __restrict__ lum, float* __restrict__ dx,
+                                float* __restrict__ dy, int64_t width, int64_t height,
+                                int64_t n, unsigned long long* fault) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t x = i % width, y = i / width;
+  const float li = lum[i];
+  float vx = 0.f, vy = 0.f;
+  if (x < width - 1) {
+    if (i + 1 < n) vx = __fsub_rn(lum[i + 1], li);
+    else if (fault) atomicMin(&fault[0], (unsigned long long)i);
+  }
+  if (y < height - 1) {
+    if (i + width < n) vy = __fsub_rn(lum[i + width], li);
+    else if (fault) atomicMin(&fault[1], (unsigned long long)i);
+  }
+  dx[i] = vx;
+  dy[i] = vy;
+}
+
+// vq_program(codebook_size), imgc.py:169-185: the chunk's cbk stream holds the
+// codebook (tiled per chunk by the reference host, imgc.py:419).
+__global__ void vqnearest_kernel(const float* __restrict__ blk, const float* __restrict__ cbk,
+                                 int32_t* __restrict__ idx, int64_t n, int ncb) {
+  extern __shared__ float4 scb[];
+  for (int e = threadIdx.x; e < ncb * 4; e += blockDim.x) scb[e] = reinterpret_cast<const float4*>(cbk)[e];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float b[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 v = reinterpret_cast<const float4*>(blk)[4 * i + q];
+    b[4 * q] = v.x; b[4 * q + 1] = v.y; b[4 * q + 2] = v.z; b[4 * q + 3] = v.w;
+  }
+  float best = VQ_BEST_INIT;
+  int bj = 0;
+  for (int j = 0; j < ncb; ++j) {
+    const float d = vq_dist(b, scb + 4 * j);
+    if (d < best) { best = d; bj = j; }
+  }
+  idx[i] = bj;
+}
+
+// ---------------------------------------------------------------------------
+// fused encoder: one thread per 4x4 block
+
+struct EncodeArgs {
+  const uint8_t* px;
+  int64_t height, width, row_stride, image_stride;
+  const float* codebook;
+  int ncb;
+  int64_t codebook_stride;
+  double sigma_min;
+  uint8_t* records;
+  uint8_t* cb_plane;
+  uint8_t* cr_plane;
+  float* block_grad;
+  float* norm32;
+};
+
+template <int CH>
+__device__ __forceinline__ void load_rgb(const uint8_t* row, int64_t x, float& r, float& g, float& b) {
+  if constexpr (CH == 1) {
+    r = g = b = (float)row[x];
+  } else {
+    const uint8_t* p = row + x * CH;
+    r = (float)p[0];
+    g = (float)p[1];
+    b = (float)p[2];
+  }
+}
+
+template <int CH>
+__global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
+  __shared__ float4 scb[256 * 4];
+  __shared__ uint8_t srec[256 * 3];
+  const int64_t img = blockIdx.y;
+  const float4* cbk = reinterpret_cast<const float4*>(a.codebook + img * a.codebook_stride);
+  for (int e = threadIdx.x; e < a.ncb * 4; e += blockDim.x) scb[e] = cbk[e];
+  __syncthreads();
+
+  const int64_t bw = a.width / 4, bh = a.height / 4, nblocks = bw * bh;
+  const int64_t k0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t k = k0 + threadIdx.x;
+  const bool active = k < nblocks;
+  if (active) {
+    const int64_t by = k / bw, bx = k - by * bw;
+    const uint8_t* base = a.px + img * a.image_stride;
+    float yv[16];
+    float cbs = 0.f, crs = 0.f;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint8_t* row = base + (4 * by + r) * a.row_stride;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float R, G, B;
+        load_rgb<CH>(row, 4 * bx + c, R, G, B);
+        const YCC o = ycc(R, G, B);
+        yv[4 * r + c] = o.y;
+        cbs = (r == 0 && c == 0) ? o.cb : __fadd_rn(cbs, o.cb);
+        crs = (r == 0 && c == 0) ? o.cr : __fadd_rn(crs, o.cr);
+      }
+    }
+    a.cb_plane[img * nblocks + k] = q8f(__fmul_rn(cbs, 0.0625f));
+    a.cr_plane[img * nblocks + k] = q8f(__fmul_rn(crs, 0.0625f));
+
+    if (a.block_grad) {
+      // forward differences with clamped borders (imgc.py:158-161), hypot
+      // in binary64 rounded once (numpy float32 hypot), pairwise-16 mean
+      float right[4], below[4];
+      const int64_t xr = 4 * bx + 4, yb = 4 * by + 4;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        right[r] = 0.f;
+        if (xr < a.width) {
+          float R, G, B;
+          load_rgb<CH>(base + (4 * by + r) * a.row_stride, xr, R, G, B);
+          right[r] = luma(R, G, B);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        below[c] = 0.f;
+        if (yb < a.height) {
+          float R, G, B;
+          load_rgb<CH>(base + yb * a.row_stride, 4 * bx + c, R, G, B);
+          below[c] = luma(R, G, B);
+        }
+      }
+      float mag[16];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float l = yv[4 * r + c];
+          float gx = 0.f, gy = 0.f;
+          if (4 * bx + c < a.width - 1) gx = __fsub_rn(c < 3 ? yv[4 * r + c + 1] : right[r], l);
+          if (4 * by + r < a.height - 1) gy = __fsub_rn(r < 3 ? yv[4 * (r + 1) + c] : below[c], l);
+          const double dxd = (double)gx, dyd = (double)gy;
+          mag[4 * r + c] = __double2float_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(dxd, dxd), __dmul_rn(dyd, dyd))));
+        }
+      }
+      a.block_grad[img * nblocks + k] = __fdiv_rn(pw16f(mag), 16.0f);
+    }
+
+    // block statistics in binary64 (imgc.py:384-388)
+    double bd[16], sq[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bd[i] = (double)yv[i];
+    const double mean = __ddiv_rn(pw16d(bd), 16.0);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      bd[i] = __dsub_rn(bd[i], mean);
+      sq[i] = __dmul_rn(bd[i], bd[i]);
+    }
+    const double sd = __dsqrt_rn(__ddiv_rn(pw16d(sq), 16.0));
+    const double safe = fmax(sd, a.sigma_min);  // np.maximum(sigmas, sigma_min)
+    float nb[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) nb[i] = __double2float_rn(__ddiv_rn(bd[i], safe));
+    if (a.norm32) {
+      float4* dst = reinterpret_cast<float4*>(a.norm32 + (img * nblocks + k) * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = make_float4(nb[4 * q], nb[4 * q + 1], nb[4 * q + 2], nb[4 * q + 3]);
+    }
+
+    // exact nearest centroid (vq_program semantics: strict <, first index wins)
+    float best = VQ_BEST_INIT;
+    int bj = 0;
+    for (int j = 0; j < a.ncb; ++j) {
+      const float d = vq_dist(nb, scb + 4 * j);
+      if (d < best) { best = d; bj = j; }
+    }
+    const int t = threadIdx.x;
+    srec[3 * t + 0] = q8d(mean);
+    srec[3 * t + 1] = q8d(__dmul_rn(sd, 4.0));  // sd / 0.25 is exact
+    srec[3 * t + 2] = (uint8_t)bj;
+  }
+  __syncthreads();
+  // records of this CTA are one contiguous run: write it with coalesced bytes
+  const int64_t nrec = (nblocks - k0 < (int64_t)blockDim.x ? nblocks - k0 : (int64_t)blockDim.x) * 3;
+  uint8_t* rec = a.records + (img * nblocks + k0) * 3;
+  for (int e = threadIdx.x; e < nrec; e += blockDim.x) rec[e] = srec[e];
+}
+
+// ---------------------------------------------------------------------------
+// decoder (imgc.py:426-439): one thread per pixel, binary64 like numpy
+
+__global__ void decode_kernel(const uint8_t* __restrict__ records, const uint8_t* __restrict__ cbp,
+                              const uint8_t* __restrict__ crp, const float* __restrict__ codebook,
+                              int64_t height, int64_t width, uint8_t* __restrict__ rgb) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= height * width) return;
+  const int64_t y = i / width, x = i - y * width;
+  const int64_t bw = width / 4;
+  const int64_t k = (y / 4) * bw + x / 4;
+  const int pos = (int)((y & 3) * 4 + (x & 3));
+  const double mean = (double)records[3 * k];
+  const double sigma = __dmul_rn((double)records[3 * k + 1], 0.25);
+  const double cval = (double)codebook[records[3 * k + 2] * 16 + pos];
+  const double l = __dadd_rn(mean, __dmul_rn(sigma, cval));
+  const double cb = __dsub_rn((double)cbp[k], 128.0);
+  const double cr = __dsub_rn((double)crp[k], 128.0);
+  const double r = __dadd_rn(l, __dmul_rn(1.402, cr));
+  const double g = __dsub_rn(__dsub_rn(l, __dmul_rn(0.344136, cb)), __dmul_rn(0.714136, cr));
+  const double b = __dadd_rn(l, __dmul_rn(1.772, cb));
+  rgb[3 * i + 0] = q8d(r);
+  rgb[3 * i + 1] = q8d(g);
+  rgb[3 * i + 2] = q8d(b);
+}
+
+static unsigned grid1(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+}  // namespace dpp
+
+extern "C" {
+
+int dpp_imgc_ycbcr(const uint8_t* rgba, float* yl, float* cb, float* cr, int64_t pixels, void* stream) {
+  if (pixels < 0) return dpp::fail(DPP_EINVAL, "pixels must be >= 0");
+  if (pixels == 0) return DPP_OK;
+  dpp::ycbcr_kernel<<<dpp::grid1(pixels, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const uchar4*>(rgba), yl, cb, cr, pixels);
+  DPP_LAUNCH_CHECK("ycbcr_kernel");
+  return DPP_OK;
+}
+
+int dpp_imgc_boxdown(const float* blk, float* avg, int64_t blocks, void* stream) {
+  if (blocks < 0) return dpp::fail(DPP_EINVAL, "blocks must be >= 0");
+  if (blocks == 0) return DPP_OK;
+  dpp::boxdown_kernel<<<dpp::grid1(blocks, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(blk), avg, blocks);
+  DPP_LAUNCH_CHECK("boxdown_kernel");
+  return DPP_OK;
+}
+
+int dpp_imgc_gradient(const float* lum, float* dx, float* dy, int64_t width, int64_t height,
+                      int64_t items, int64_t* fault_item, void* stream) {
+  if (width < 1 || height < 1 || items < 0) return dpp::fail(DPP_EINVAL, "bad gradient geometry");
+  if (fault_item) *fault_item = -1;
+  if (items == 0) return DPP_OK;
+  if (items >= width * height) {
+    // whole frames: every guarded read stays inside the chunk, nothing to report
+    dpp::gradient_kernel<<<dpp::grid1(items, 256), 256, 0, (cudaStream_t)stream>>>(lum, dx, dy, width, height,
+                                                                                    items, nullptr);
+    DPP_LAUNCH_CHECK("gradient_kernel");
+    return DPP_OK;
+  }
+  unsigned long long* fault = nullptr;
+  DPP_CUDA_CHECK(cudaMallocAsync(&fault, 2 * sizeof(unsigned long long), (cudaStream_t)stream));
+  DPP_CUDA_CHECK(cudaMemsetAsync(fault, 0xff, 2 * sizeof(unsigned long long), (cudaStream_t)stream));
+  dpp::gradient_kernel<<<dpp::grid1(items, 256), 256, 0, (cudaStream_t)stream>>>(lum, dx, dy, width, height,
+                                                                                  items, fault);
+  DPP_LAUNCH_CHECK("gradient_kernel");
+  unsigned long long h[2];
+  DPP_CUDA_CHECK(cudaMemcpyAsync(h, fault, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  DPP_CUDA_CHECK(cudaFreeAsync(fault, (cudaStream_t)stream));
+  DPP_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  // the interpreter evaluates the dx statement for every lane before dy
+  const unsigned long long none = ~0ULL;
+  const unsigned long long bad = h[0] != none ? h[0] : h[1];
+  if (bad != none) {
+    const int64_t i = (int64_t)bad;
+    const int64_t at = h[0] != none ? i + 1 : i + width;
+    if (fault_item) *fault_item = i;
+    return dpp::fail(DPP_EINVAL, "index %lld out of range for point 'lum' (0..%lld)", (long long)at,
+                     (long long)(items - 1));
+  }
+  return DPP_OK;
+}
+
+int dpp_imgc_vqnearest(const float* blk, const float* cbk, int32_t* idx, int64_t items, int64_t cbk_items,
+                       int codebook_size, void* stream) {
+  if (items < 0 || codebook_size < 0 || codebook_size > 4096)
+    return dpp::fail(DPP_EINVAL, "bad vqnearest arguments");
+  if (items == 0) return DPP_OK;
+  if (codebook_size > cbk_items)
+    return dpp::fail(DPP_EINVAL, "index %lld out of range for point 'cbk' (0..%lld)", (long long)cbk_items,
+                     (long long)(cbk_items - 1));
+  const size_t smem = (size_t)codebook_size * 16 * sizeof(float);
+  if (smem > 48 * 1024)
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(dpp::vqnearest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+  dpp::vqnearest_kernel<<<dpp::grid1(items, 256), 256, smem, (cudaStream_t)stream>>>(blk, cbk, idx, items,
+                                                                                     codebook_size);
+  DPP_LAUNCH_CHECK("vqnearest_kernel");
+  return DPP_OK;
+}
+
+int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
+                    int64_t image_stride, int64_t batch, const float* codebook, int n_cb,
+                    int64_t codebook_stride, double sigma_min, uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
+                    float* block_grad, float* norm32, void* stream) {
+  if (height % 4 || width % 4 || height < 4 || width < 4)
+    return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
+                     (long long)height);
+  if (n_cb < 1 || n_cb > 256) return dpp::fail(DPP_EINVAL, "codebook size must be in 1..256");
+  if (channels != 1 && channels != 3 && channels != 4)
+    return dpp::fail(DPP_EINVAL, "channels must be 1, 3 or 4, got %d", channels);
+  if (row_stride < width * channels) return dpp::fail(DPP_EINVAL, "row stride too small");
+  if (batch < 0 || batch > 65535) return dpp::fail(DPP_EINVAL, "batch must be in 0..65535");
+  if (batch == 0) return DPP_OK;
+  if (!(sigma_min > 0.0)) return dpp::fail(DPP_EINVAL, "sigma_min must be > 0");
+  dpp::EncodeArgs a{px, height, width, row_stride, image_stride, codebook, n_cb, codebook_stride, sigma_min,
+                    records, cb_plane, cr_plane, block_grad, norm32};
+  const int64_t nblocks = (height / 4) * (width / 4);
+  dim3 grid(dpp::grid1(nblocks, 256), (unsigned)batch);
+  auto s = (cudaStream_t)stream;
+  switch (channels) {
+    case 1: dpp::encode_kernel<1><<<grid, 256, 0, s>>>(a); break;
+    case 3: dpp::encode_kernel<3><<<grid, 256, 0, s>>>(a); break;
+    default: dpp::encode_kernel<4><<<grid, 256, 0, s>>>(a); break;
+  }
+  DPP_LAUNCH_CHECK("encode_kernel");
+  return DPP_OK;
+}
+
+int dpp_imgc_decode(const uint8_t* records, const uint8_t* cb_plane, const uint8_t* cr_plane,
+                    const float* codebook, int n_cb, int64_t height, int64_t width, uint8_t* rgb,
+                    void* stream) {
+  if (height % 4 || width % 4) return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4");
+  if (n_cb < 1 || n_cb > 256) return dpp::fail(DPP_EINVAL, "codebook size must be in 1..256");
+  const int64_t n = height * width;
+  if (n == 0) return DPP_OK;
+  dpp::decode_kernel<<<dpp::grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(records, cb_plane, cr_plane,
+                                                                           codebook, height, width, rgb);
+  DPP_LAUNCH_CHECK("decode_kernel");
+  return DPP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,301 @@
+"""Device executor: the reference engine's plan/chunk/run contract on CUDA streams.
+
+Mirrors /root/reference/pkg/src/dpp/engine.py with the same names and rules:
+
+* ``plan`` (engine.py:82-135): structural validation, topological order,
+  width-conversion multipliers as ``Fraction`` (engine.py:108-109), input
+  bindings ``("free", stream)`` / ``("arrow", iid, point)``; kernel bodies are
+  bound to native implementations (``nodes.resolve``) instead of compiled.
+  Plans are cached by (program id, chunk size, device) — the reference
+  recompiles on every call (~7 ms per ``fft()``).
+* ``chunk_arrays`` (engine.py:397-424): W-element chunks as tensor VIEWS.
+* ``run_chunk`` (engine.py:176-215): every instance in topological order;
+  outputs allocated on the device; producer buffers handed to consumers by
+  reference, so edges never leave HBM.
+* ``run_stream`` (engine.py:255-330): ordered emission; chunks are enqueued
+  back to back on one CUDA stream (stream order replaces the thread pool;
+  ``pool="process"`` is refused because CUDA contexts do not survive fork).
+
+Extension: a native node may declare *broadcast* inputs
+(side inputs such as a codebook) that are handed whole to every chunk and
+excluded from the equal-element-count rule.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Callable, Iterable, Iterator
+
+import torch
+
+from .errors import EngineRuntimeError, KernelRuntimeError, PlanError
+from .model import FreePoint, Program, as_program, free_points, program_id, topological_order, validate
+from .nodes import NativeNode, resolve
+from .types import Direction
+from ._torch import require_cuda, torch_dtype
+
+__all__ = ["DEFAULT_CHUNK_SIZE", "ExecutionPlan", "Chunk", "RunResult", "plan", "run_chunk",
+           "run_stream", "chunk_arrays"]
+
+DEFAULT_CHUNK_SIZE = None  # whole stream in one chunk (the reference default is 4096)
+
+
+@dataclass(frozen=True)
+class ExecutionPlan:
+    program: Program
+    order: tuple[int, ...]
+    multipliers: dict[int, Fraction]
+    kernels: dict[str, NativeNode]
+    bindings: dict[tuple[int, str], tuple]
+    free_inputs: tuple[FreePoint, ...]
+    free_outputs: tuple[FreePoint, ...]
+    chunk_size: int | None
+    device: torch.device
+    broadcast: frozenset = frozenset()  # free input stream names handed whole to every chunk
+
+    @property
+    def items_per_element(self) -> Fraction:
+        return sum(self.multipliers.values(), Fraction(0))
+
+    @property
+    def counted_inputs(self) -> tuple[FreePoint, ...]:
+        return tuple(fp for fp in self.free_inputs if fp.stream not in self.broadcast)
+
+
+@dataclass
+class Chunk:
+    """One block of stream data: flat device (or host) buffers keyed by stream name."""
+
+    index: int
+    buffers: dict[str, object]
+    counts: dict[str, int]
+
+
+@dataclass
+class RunResult:
+    chunks: list[Chunk] = field(default_factory=list)
+    total_work_items: int = 0
+    events: list = field(default_factory=list, repr=False)
+
+    @property
+    def timings(self) -> list[float]:
+        """Per-chunk device seconds (engine.py:65-69); waits for the stream on first use."""
+        if self.events:
+            self.events[-1][1].synchronize()
+        return [a.elapsed_time(b) / 1e3 for a, b in self.events]
+
+
+_cache: dict[tuple, ExecutionPlan] = {}
+_cache_lock = threading.Lock()
+
+
+def plan(program, chunk_size: int | None = DEFAULT_CHUNK_SIZE, *, device=None) -> ExecutionPlan:
+    """Validate, bind native nodes and fix the schedule (engine.py:82-135)."""
+    if chunk_size is not None and chunk_size < 1:
+        raise PlanError(f"chunk size must be >= 1, got {chunk_size}")
+    program = as_program(program)
+    dev = require_cuda(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (program_id(program), chunk_size, dev.index)
+    with _cache_lock:
+        hit = _cache.get(key)
+    if hit is not None:
+        return hit
+    report = validate(program)
+    if not report.ok:
+        raise PlanError(f"program is not executable:\n{report}")
+    kernels = {name: resolve(node) for name, node in program.kernels.items()}
+    order = tuple(topological_order(program))
+    producers = {a.input: a.output for a in program.arrows}
+    bindings: dict[tuple[int, str], tuple] = {}
+    multipliers: dict[int, Fraction] = {}
+    broadcast: set[str] = set()
+    for iid in order:
+        inst = program.instance(iid)
+        node = program.kernels[inst.kernel]
+        native = kernels[inst.kernel]
+        cands: list[tuple[str, Fraction]] = []
+        for p in node.io:
+            if not p.is_input:
+                continue
+            key_p = (iid, p.name)
+            if key_p in producers:
+                src = producers[key_p]
+                if p.name in native.broadcast:
+                    raise PlanError(f"broadcast input {iid}.{p.name} must be a free stream")
+                m = multipliers[src[0]] * program.point_of(*src).data.width / p.data.width
+                bindings[key_p] = ("arrow", src[0], src[1])
+            else:
+                m = Fraction(1)
+                bindings[key_p] = ("free", f"{iid}.{p.name}")
+                if p.name in native.broadcast:
+                    broadcast.add(f"{iid}.{p.name}")
+                    continue
+            cands.append((p.name, m))
+        first = cands[0][1]
+        for pname, m in cands[1:]:
+            if m != first:
+                raise PlanError(f"work-item count mismatch at instance {iid}: point {cands[0][0]!r} "
+                                f"implies x{first}, {pname!r} implies x{m}")
+        if chunk_size is not None and (first * chunk_size).denominator != 1:
+            raise PlanError(f"non-integral width conversion: instance {iid} runs {first} work-items per "
+                            f"element, not integral at chunk size {chunk_size}")
+        multipliers[iid] = first
+    free = free_points(program)
+    result = ExecutionPlan(
+        program=program, order=order, multipliers=multipliers, kernels=kernels, bindings=bindings,
+        free_inputs=tuple(p for p in free if p.direction is Direction.INPUT),
+        free_outputs=tuple(p for p in free if p.direction is Direction.OUTPUT),
+        chunk_size=chunk_size, device=dev, broadcast=frozenset(broadcast))
+    with _cache_lock:
+        _cache[key] = result
+    return result
+
+
+def _element_count(p: ExecutionPlan, chunk: Chunk) -> int:
+    counts = set()
+    for fp in p.free_inputs:
+        if fp.stream not in chunk.buffers:
+            raise EngineRuntimeError(f"missing input stream {fp.stream!r}", chunk=chunk.index)
+        if fp.stream in p.broadcast:
+            continue
+        buf = chunk.buffers[fp.stream]
+        n = buf.numel()
+        count = chunk.counts.get(fp.stream, n // fp.data.width)
+        if buf.dtype != torch_dtype(fp.data):
+            raise EngineRuntimeError(f"stream {fp.stream!r} carries {buf.dtype}, expected {fp.data}",
+                                     chunk=chunk.index)
+        if n != count * fp.data.width:
+            raise EngineRuntimeError(f"stream {fp.stream!r}: buffer holds {n} scalars, expected "
+                                     f"{count * fp.data.width}", chunk=chunk.index)
+        counts.add(count)
+    unknown = chunk.buffers.keys() - {fp.stream for fp in p.free_inputs}
+    if unknown:
+        raise EngineRuntimeError(f"unexpected input stream {sorted(unknown)[0]!r}", chunk=chunk.index)
+    if len(counts) > 1:
+        raise EngineRuntimeError(f"input streams disagree on element count: {sorted(counts)}",
+                                 chunk=chunk.index)
+    return counts.pop() if counts else 0
+
+
+def _items(p: ExecutionPlan, iid: int, elements: int, chunk_index: int) -> int:
+    items = p.multipliers[iid] * elements
+    if items.denominator != 1:
+        raise EngineRuntimeError(f"width conversion not integral for instance {iid} at {elements} "
+                                 f"elements", chunk=chunk_index)
+    return int(items)
+
+
+def run_chunk(p: ExecutionPlan, chunk: Chunk, stream: torch.cuda.Stream | None = None) -> Chunk:
+    """Run every instance over one chunk on ``stream`` (engine.py:176-215)."""
+    elements = _element_count(p, chunk)
+    produced: dict[tuple[int, str], torch.Tensor] = {}
+    for iid in p.order:
+        inst = p.program.instance(iid)
+        node = p.program.kernels[inst.kernel]
+        native = p.kernels[inst.kernel]
+        items = _items(p, iid, elements, chunk.index)
+        inputs = {}
+        for pt in node.io:
+            if not pt.is_input:
+                continue
+            kind = p.bindings[(iid, pt.name)]
+            inputs[pt.name] = chunk.buffers[kind[1]] if kind[0] == "free" else produced[(kind[1], kind[2])]
+        outputs = {pt.name: torch.empty(items * pt.data.width, dtype=torch_dtype(pt.data), device=p.device)
+                   for pt in node.io if not pt.is_input}
+        try:
+            if items:
+                native.check_items(items)
+                native.launch(items, inputs, outputs, stream)
+        except KernelRuntimeError as exc:
+            raise EngineRuntimeError(str(exc), instance=iid, work_item=exc.work_item,
+                                     chunk=chunk.index) from exc
+        for name, buf in outputs.items():
+            produced[(iid, name)] = buf
+    out_buf, out_cnt = {}, {}
+    for fp in p.free_outputs:
+        out_buf[fp.stream] = produced[(fp.instance, fp.point)]
+        out_cnt[fp.stream] = _items(p, fp.instance, elements, chunk.index)
+    return Chunk(chunk.index, out_buf, out_cnt)
+
+
+def _checked(p: ExecutionPlan, chunks: Iterable[Chunk]) -> Iterator[tuple[int, Chunk, int]]:
+    """Dense indices, short chunk only last (engine.py:339-361)."""
+    expected, short = 0, None
+    for chunk in chunks:
+        if chunk.index != expected:
+            raise EngineRuntimeError(f"chunk {chunk.index} arrived out of order (expected {expected})",
+                                     chunk=chunk.index)
+        if short is not None:
+            raise EngineRuntimeError(f"short chunk {short} was not the final chunk", chunk=chunk.index)
+        elements = _element_count(p, chunk)
+        if p.chunk_size is not None:
+            if elements > p.chunk_size:
+                raise EngineRuntimeError(f"chunk carries {elements} elements, plan chunk size is "
+                                         f"{p.chunk_size}", chunk=chunk.index)
+            if elements < p.chunk_size:
+                short = chunk.index
+        yield chunk.index, chunk, elements
+        expected += 1
+
+
+def run_stream(p: ExecutionPlan, chunks: Iterable[Chunk], writer: Callable[[Chunk], None] | None = None,
+               *, workers: int = 1, max_in_flight: int | None = None, pool: str = "thread",
+               stream: torch.cuda.Stream | None = None) -> RunResult:
+    """Whole stream, outputs emitted in input order (engine.py:255-330).
+
+    Chunks are enqueued back to back on ``stream`` without host syncs;
+    ``RunResult.timings`` reads the per-chunk CUDA events when asked."""
+    if pool not in ("thread", "process"):
+        raise ValueError(f"unknown pool kind {pool!r}")
+    if pool == "process" and workers > 1:
+        raise PlanError("pool='process' is not supported by the device engine (CUDA does not survive "
+                        "fork); chunks are pipelined on CUDA streams instead")
+    result = RunResult()
+    per_element = p.items_per_element
+    s = stream if stream is not None else torch.cuda.current_stream(p.device)
+    with torch.cuda.device(p.device):
+        for _, chunk, elements in _checked(p, chunks):
+            start = torch.cuda.Event(enable_timing=True)
+            stop = torch.cuda.Event(enable_timing=True)
+            start.record(s)
+            out = run_chunk(p, chunk, s)
+            stop.record(s)
+            result.events.append((start, stop))
+            result.total_work_items += int(per_element * elements)
+            if writer is not None:
+                writer(out)
+            else:
+                result.chunks.append(out)
+    return result
+
+
+def chunk_arrays(p: ExecutionPlan, streams: dict[str, object]) -> Iterator[Chunk]:
+    """Cut whole device streams into plan-sized chunks of views (engine.py:397-424)."""
+    counts = set()
+    for fp in p.free_inputs:
+        if fp.stream not in streams:
+            raise EngineRuntimeError(f"missing input stream {fp.stream!r}")
+        if fp.stream not in p.broadcast:
+            counts.add(streams[fp.stream].numel() // fp.data.width)
+    extra = streams.keys() - {fp.stream for fp in p.free_inputs}
+    if extra:
+        raise EngineRuntimeError(f"unexpected input stream {sorted(extra)[0]!r}")
+    if len(counts) > 1:
+        raise EngineRuntimeError(f"input streams disagree on element count: {sorted(counts)}")
+    total = counts.pop() if counts else 0
+    w = p.chunk_size or max(total, 1)
+    for index in range((total + w - 1) // w):
+        lo, hi = index * w, min((index + 1) * w, total)
+        bufs, cnts = {}, {}
+        for fp in p.free_inputs:
+            t = streams[fp.stream]
+            if fp.stream in p.broadcast:
+                bufs[fp.stream] = t
+                continue
+            bufs[fp.stream] = t[lo * fp.data.width:hi * fp.data.width]
+            cnts[fp.stream] = hi - lo
+        yield Chunk(index, bufs, cnts)

@@ -1,0 +1,165 @@
+"""FFT node parity on the B200 (through the C ABI), against the pinned oracle.
+
+Tolerance (north star): relative L2 error <= 1e-5 * log2(N) per signal in fp32,
+against the reference fft() (oracle.fft_oracle, bit-exact with the reference
+on the golden vectors).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import complex_signals, rel_l2
+from oracle import fft_oracle as fo
+
+pytestmark = pytest.mark.gpu
+
+
+def tol(n: int) -> float:
+    return 1e-5 * np.log2(n)
+
+
+def _fft(x: np.ndarray, n: int, cuda) -> np.ndarray:
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    t = torch.from_numpy(np.ascontiguousarray(x)).to(cuda)
+    return ops.fft_forward(t, n).cpu().numpy()
+
+
+@pytest.mark.parametrize("m", list(range(1, 18)))
+def test_batched_1d_every_size_vs_oracle(cuda, m):
+    n = 1 << m
+    batch = max(1, min(64, (1 << 19) // n))
+    x = complex_signals(100 + m, (batch, n))
+    got = _fft(x, n, cuda)
+    ref = fo.fft_rows(x)
+    errs = [rel_l2(g, r) for g, r in zip(got, ref)]
+    assert max(errs) <= tol(n), (n, max(errs))
+
+
+@pytest.mark.parametrize("n", [65536])
+def test_batch_not_multiple_of_cluster_grid(cuda, n):
+    x = complex_signals(7, (3, n))
+    got = _fft(x, n, cuda)
+    for g, r in zip(got, fo.fft_rows(x)):
+        assert rel_l2(g, r) <= tol(n)
+
+
+def test_reference_golden_ladder(cuda, fft_golden):
+    # acceptance ladder N=8..4096 (test_acceptance.py:170-205): max-rel < 1e-4 vs naive
+    for m in range(3, 13):
+        n = 1 << m
+        x = fft_golden[f"x_{n}"]
+        got = _fft(x, n, cuda)
+        ref = fft_golden[f"y_{n}_k3"]
+        assert rel_l2(got, ref) <= tol(n)
+        scale = np.abs(ref).max()
+        assert np.abs(got - ref).max() / scale < 1e-4
+
+
+def test_c1_through_the_graph_api(cuda, fft_golden):
+    """C1: N=1024 batch 1 through fft() -> run() -> fft1024 node -> C ABI."""
+    from paper_1203_4938_b200.apps.fft import FftPlan, fft
+    x = fft_golden["c1_x"]
+    got = fft(x, FftPlan(1024, 3))
+    assert got.dtype == np.complex64 and got.shape == (1024,)
+    ref = fft_golden["c1_y"]
+    assert rel_l2(got, ref) <= tol(1024)
+    assert np.abs(got - fo.naive_dft(x)).max() / np.abs(ref).max() < 1e-4  # test_fft.py:91-96
+
+
+def test_16k_golden(cuda, fft_golden):
+    got = _fft(fft_golden["x_16384"], 16384, cuda)
+    assert rel_l2(got, fft_golden["y_16384_k3"]) <= tol(16384)
+
+
+def test_impulse_constant_linearity_parseval(cuda):
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    for n in (8, 1024, 65536):
+        imp = np.zeros(n, np.complex64)
+        imp[0] = 1
+        assert np.allclose(_fft(imp, n, cuda), np.ones(n), atol=1e-6)
+        const = np.full(n, 2.5, np.complex64)
+        out = _fft(const, n, cuda)
+        assert abs(out[0] - 2.5 * n) / (2.5 * n) < 1e-6 and np.abs(out[1:]).max() < 1e-3 * n
+    n = 65536
+    x, y = complex_signals(11, n), complex_signals(12, n)
+    a, b = np.complex64(1.7 - 0.3j), np.complex64(-0.8 + 2.1j)
+    lhs = _fft((a * x + b * y).astype(np.complex64), n, cuda)
+    rhs = a * _fft(x, n, cuda) + b * _fft(y, n, cuda)
+    assert np.abs(lhs - rhs).max() / np.abs(rhs).max() < 1e-3
+    spec = _fft(x, n, cuda).astype(np.complex128)
+    et = float(np.sum(np.abs(x.astype(np.complex128)) ** 2))
+    assert abs(et - float(np.sum(np.abs(spec) ** 2)) / n) / et < 1e-5
+    # in place
+    t = torch.from_numpy(x).to(cuda)
+    ops.fft_forward(t, n, out=t)
+    assert rel_l2(t.cpu().numpy(), fo.fft(x)) <= tol(n)
+
+
+def test_large_batch_checksum_against_sampled_oracle(cuda):
+    """C2 shape (2^16 x 4096) at full size: sampled signals vs oracle + a
+    size-independent identity (sum over k of X[k] = N * x[0])."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    n, batch = 65536, 4096
+    gen = torch.Generator(device=cuda).manual_seed(42)
+    x = torch.randn((batch, n), dtype=torch.complex64, device=cuda, generator=gen)
+    y = ops.fft_forward(x, n)
+    lhs = y.to(torch.complex128).sum(dim=1)
+    rhs = n * x[:, 0].to(torch.complex128)
+    err = ((lhs - rhs).abs() / (n * torch.sqrt(torch.tensor(float(n), device=cuda)))).max().item()
+    assert err < 1e-4
+    for row in (0, 1, 1777, batch - 1):
+        xr = x[row].cpu().numpy()
+        assert rel_l2(y[row].cpu().numpy(), fo.fft(xr)) <= tol(n)
+
+
+@pytest.mark.parametrize("shape", [(256, 32), (512, 64), (1024, 256), (2048, 16), (4096, 64),
+                                   (8192, 8), (16384, 8)])
+def test_2d_vs_composed_oracle(cuda, shape):
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    rows, cols = shape
+    x = complex_signals(sum(shape), shape)
+    got = ops.fft2d_forward(torch.from_numpy(x).to(cuda), rows, cols).cpu().numpy()
+    ref = fo.fft2(x)
+    assert rel_l2(got, ref) <= 1e-5 * np.log2(rows * cols), shape
+
+
+def test_2d_through_fft2_api_batched(cuda):
+    from paper_1203_4938_b200.apps.fft import fft2
+    x = complex_signals(5, (3, 256, 64))
+    got = fft2(x)
+    for g, xi in zip(got, x):
+        assert rel_l2(g, fo.fft2(xi)) <= 1e-5 * 14
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_leaf_nodes_bit_exact_with_reference_engine(cuda, leaf_golden, k):
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    x = torch.from_numpy(leaf_golden[f"x_k{k}"]).to(cuda)
+    y = torch.empty_like(x)
+    ops.leaf_dft(k, x, y)
+    assert np.array_equal(y.cpu().numpy(), leaf_golden[f"y_k{k}"])
+
+
+def test_size_errors(cuda):
+    import torch
+
+    from paper_1203_4938_b200 import PlanError, ops
+    x = torch.zeros(24, dtype=torch.complex64, device=cuda)
+    with pytest.raises(PlanError, match="power of two"):
+        ops.fft_forward(x, 12)
+    with pytest.raises(PlanError, match="whole number"):
+        ops.fft_forward(x, 16)
+    with pytest.raises(PlanError):
+        ops.fft_forward(torch.zeros(1 << 19, dtype=torch.complex64, device=cuda), 1 << 19)

@@ -1,0 +1,153 @@
+"""Compression node parity on the B200: bit-exact bitstreams against the reference.
+
+Every bitstream in tests/golden/imgc_golden.npz was produced by the reference
+``compress()`` itself; the GPU encoder is fed the codebook stored in that
+bitstream (k-means is an input of the node) and must reproduce every byte.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import imgc_oracle as io
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(g):
+    return sorted(k[:-5] for k in g.files if k.endswith("_blob"))
+
+
+def test_bitstreams_bit_exact_vs_reference(cuda, imgc_golden):
+    from paper_1203_4938_b200.apps import imgc
+    for name in _cases(imgc_golden):
+        blob = imgc_golden[f"{name}_blob"].tobytes()
+        ref = imgc.CompressedImage.from_bytes(blob)
+        ci = imgc.compress(imgc_golden[f"{name}_image"], ref.codebook.size, codebook=ref.codebook)
+        got = ci.to_bytes()
+        if got != blob:
+            diff = [f for f in ("means", "sigma_idx", "indices", "cb", "cr")
+                    if not np.array_equal(getattr(ci, f), getattr(ref, f))]
+            pytest.fail(f"{name}: fields differ: {diff}")
+
+
+@pytest.mark.parametrize("layout", ["gray", "rgb", "rgba"])
+def test_channel_layouts_agree(cuda, imgc_golden, layout):
+    from paper_1203_4938_b200.apps import imgc
+    img3 = imgc_golden["gray256_cb256_s0_image"]
+    blob = imgc_golden["gray256_cb256_s0_blob"].tobytes()
+    ref = imgc.CompressedImage.from_bytes(blob)
+    if layout == "gray":
+        img = np.ascontiguousarray(img3[..., 0])
+    elif layout == "rgba":
+        img = np.concatenate([img3, np.full(img3.shape[:2] + (1,), 200, np.uint8)], axis=2)
+    else:
+        img = img3
+    assert imgc.compress(img, 256, codebook=ref.codebook).to_bytes() == blob
+
+
+def test_decompress_bit_exact(cuda, imgc_golden):
+    from paper_1203_4938_b200.apps import imgc
+    for name in _cases(imgc_golden):
+        ci = imgc.CompressedImage.from_bytes(imgc_golden[f"{name}_blob"].tobytes())
+        assert np.array_equal(imgc.decompress(ci), imgc_golden[f"{name}_decoded"]), name
+
+
+def test_drop_in_nodes_bit_exact(cuda, imgc_golden):
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)  # noqa: E731
+    rgba = t(imgc_golden["ycbcr_in"])
+    n = rgba.numel() // 4
+    yl, cb, cr = (torch.empty(n, dtype=torch.float32, device=cuda) for _ in range(3))
+    ops.ycbcr(rgba, yl, cb, cr)
+    assert np.array_equal(yl.cpu().numpy(), imgc_golden["ycbcr_yl"])
+    assert np.array_equal(cb.cpu().numpy(), imgc_golden["ycbcr_cb"])
+    assert np.array_equal(cr.cpu().numpy(), imgc_golden["ycbcr_cr"])
+    blk = t(imgc_golden["box_in"])
+    avg = torch.empty(len(imgc_golden["box_in"]), dtype=torch.float32, device=cuda)
+    ops.boxdown(blk, avg)
+    assert np.array_equal(avg.cpu().numpy(), imgc_golden["box_out"])
+    lum = t(imgc_golden["grad_in"])
+    dx, dy = torch.empty_like(lum), torch.empty_like(lum)
+    ops.gradient(lum, dx, dy, 24, 16)
+    assert np.array_equal(dx.cpu().numpy(), imgc_golden["grad_dx"])
+    assert np.array_equal(dy.cpu().numpy(), imgc_golden["grad_dy"])
+    blocks = t(imgc_golden["vq_blocks"])
+    cents = t(imgc_golden["vq_cents"])
+    idx = torch.empty(len(imgc_golden["vq_blocks"]), dtype=torch.int32, device=cuda)
+    ops.vqnearest(blocks, cents, idx, 64)
+    assert np.array_equal(idx.cpu().numpy(), imgc_golden["vq_idx"])
+
+
+def test_gradient_fault_matches_interpreter(cuda):
+    import torch
+
+    from paper_1203_4938_b200 import KernelRuntimeError, ops
+    lum = torch.zeros(24 * 15, dtype=torch.float32, device=cuda)  # one row short of 24x16
+    dx, dy = torch.empty_like(lum), torch.empty_like(lum)
+    with pytest.raises(KernelRuntimeError) as info:
+        ops.gradient(lum, dx, dy, 24, 16)
+    assert info.value.work_item == 24 * 14  # first lane whose lum[i+24] leaves the chunk
+    assert "out of range for point 'lum'" in str(info.value)
+
+
+def test_block_grad_and_norm32_outputs(cuda):
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    img = io.synthetic_image(96, 64, seed=21)
+    y, _, _ = io.ycbcr(img)
+    cents = io.train_codebook(y, 32, 1)
+    nb = (64 // 4) * (96 // 4)
+    dev = lambda n, dt: torch.empty(n, dtype=dt, device=cuda)  # noqa: E731
+    rec, cbp, crp = dev(3 * nb, torch.uint8), dev(nb, torch.uint8), dev(nb, torch.uint8)
+    grad, norm = dev(nb, torch.float32), dev(nb * 16, torch.float32)
+    ops.encode(torch.from_numpy(img).to(cuda), 3, 64, 96, torch.from_numpy(cents).to(cuda), rec, cbp,
+               crp, block_grad=grad, norm32=norm)
+    assert np.array_equal(grad.cpu().numpy(), io.gradient(y))
+    _, _, n64 = io.block_stats(y)
+    assert np.array_equal(norm.cpu().numpy().reshape(-1, 16), n64.astype(np.float32))
+
+
+def test_batched_encode_equals_single(cuda):
+    import torch
+
+    from paper_1203_4938_b200.apps import imgc
+    imgs = np.stack([io.synthetic_image(128, 64, seed=s)[..., 1] for s in (1, 2, 3)])
+    cbs = np.stack([io.train_codebook(io.ycbcr(np.repeat(g[..., None], 3, 2))[0], 64, 0) for g in imgs])
+    rec, cbp, crp = imgc.compress_batch(torch.from_numpy(imgs).cuda(), torch.from_numpy(cbs).cuda())
+    for b in range(3):
+        f = io.encode(np.repeat(imgs[b][..., None], 3, 2), cbs[b])
+        assert np.array_equal(rec[b].cpu().numpy()[:, 0], f["means"])
+        assert np.array_equal(rec[b].cpu().numpy()[:, 1], f["sigma_idx"])
+        assert np.array_equal(rec[b].cpu().numpy()[:, 2], f["indices"])
+        assert np.array_equal(cbp[b].cpu().numpy(), f["cb"].ravel())
+        assert np.array_equal(crp[b].cpu().numpy(), f["cr"].ravel())
+
+
+def test_c4_full_size_8192_gray(cuda):
+    """C4 at full size: 8192^2 gray (R=G=B).  The oracle (too slow for the whole
+    frame) checks the first 64 block rows exactly."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    rng = np.random.default_rng(7)
+    base = io.synthetic_image(1024, 1024, seed=7)[..., 1]
+    gray = np.tile(base, (8, 8)) ^ (rng.integers(0, 2, (8192, 8192), dtype=np.uint8))
+    band = np.repeat(gray[:256, :][..., None], 3, 2)
+    cents = io.train_codebook(io.ycbcr(band[:, :1024])[0], 256, 0)
+    px = torch.from_numpy(gray).to(cuda)
+    nb = 2048 * 2048
+    rec = torch.empty(nb * 3, dtype=torch.uint8, device=cuda)
+    cbp = torch.empty(nb, dtype=torch.uint8, device=cuda)
+    crp = torch.empty(nb, dtype=torch.uint8, device=cuda)
+    ops.encode(px, 1, 8192, 8192, torch.from_numpy(cents).to(cuda), rec, cbp, crp)
+    got = rec.view(-1, 3)[: 64 * 2048].cpu().numpy()
+    f = io.encode(band, cents)
+    assert np.array_equal(got[:, 0], f["means"])
+    assert np.array_equal(got[:, 1], f["sigma_idx"])
+    assert np.array_equal(got[:, 2], f["indices"])
+    assert np.array_equal(cbp[: 64 * 2048].cpu().numpy(), f["cb"].ravel())
