@@ -38,10 +38,19 @@ int fail(int code, const char* fmt, ...);
 // complex helpers (float2 = re, im).  FFT arithmetic is tolerance-checked, so
 // contraction to FFMA is allowed here; the bit-exact codec uses __f*_rn.
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+// sm_100 packed binary32 pairs (SASS FADD2 / FMUL2 / FFMA2): one instruction
+// per complex add/sub, two per complex multiply (operand broadcast .F32 and
+// negation are free modifiers).  Halves the FP issue slots of the butterflies.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// a * w = a.x * (w.x, w.y) + a.y * (-w.y, w.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x),
+                    __fmul2_rn(make_float2(a.x, a.x), w));
+}
+// same with the rotated twiddle (-w.y, w.x) precomputed (tables store both halves)
+__device__ __forceinline__ float2 cmul_pre(float2 a, float2 w, float2 wrot) {
+  return __ffma2_rn(make_float2(a.y, a.y), wrot, __fmul2_rn(make_float2(a.x, a.x), w));
 }
 // multiply by -i
 __device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a.x); }
@@ -49,11 +58,11 @@ __device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a
 // W_8^1 = (1 - i)/sqrt2, W_8^3 = (-1 - i)/sqrt2
 __device__ __forceinline__ float2 cmul_w8_1(float2 a) {
   const float h = 0.70710678118654752f;
-  return make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+  return cmul(a, make_float2(h, -h));
 }
 __device__ __forceinline__ float2 cmul_w8_3(float2 a) {
   const float h = 0.70710678118654752f;
-  return make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
+  return cmul(a, make_float2(-h, -h));
 }
 
 // ---------------------------------------------------------------------------
@@ -131,5 +140,103 @@ template <> __device__ __forceinline__ void dft_r<8>(float2 (&v)[8]) { dft8(v); 
 template <> __device__ __forceinline__ void dft_r<16>(float2 (&v)[16]) { dft16(v); }
 
 __host__ __device__ constexpr int ilog2(long long n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// ---------------------------------------------------------------------------
+// Thread-block cluster / DSMEM primitives (explicit shared::cluster state space:
+// cluster-scope release/acquire instead of the generic-pointer GPU-scope fence).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// address of the same shared-memory offset in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ float2 ld_cluster(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  cluster_arrive();
+  cluster_wait();
+}
+// arrive without a memory fence: callers only use it to say "my reads of
+// this buffer are done" after consuming the loaded values
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk async copies (TMA engine, SASS UBLKCP / SYNCS)
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// global -> own shared memory, completion counted on `bar` (bytes)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void st_async_f4(uint32_t raddr, float4 v, uint32_t rbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+      "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+      : "memory");
+}
+// 2-D tiled TMA load (tensor map in param/const space) into own shared memory
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// asynchronous store into (possibly remote) shared memory; the destination
+// CTA's mbarrier at `rbar` (same cluster address space) receives 8 tx bytes
+__device__ __forceinline__ void st_async_f2(uint32_t raddr, float2 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+                   raddr),
+               "f"(v.x), "f"(v.y), "r"(rbar)
+               : "memory");
+}
 
 }  // namespace dpp

@@ -15,16 +15,15 @@
 //                            one HBM write (the 16*n compulsory bytes).
 //   fft_columns_kernel       2-D column pass (strided FFTs over rows), see fft2d.cu.
 //   leaf_dft_kernel          the reference's dft2/4/8 node, bit-exact.
-#include <cooperative_groups.h>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "common.cuh"
 #include "fft_plan.cuh"
 #include "fft_block.cuh"
-
-namespace cg = cooperative_groups;
+#include "tma.cuh"
 
 namespace dpp {
 
@@ -43,7 +42,7 @@ struct SmallCfg {
 };
 
 template <int M>
-__global__ void __launch_bounds__(SmallCfg<M>::THREADS)
+__global__ void __launch_bounds__(SmallCfg<M>::THREADS, 1024 / SmallCfg<M>::THREADS)
 fft_small_kernel(const float2* __restrict__ in, float2* __restrict__ out, int64_t batch,
                  const float2* __restrict__ twg) {
   using Cfg = SmallCfg<M>;
@@ -95,59 +94,121 @@ struct ClusterCfg {
   static constexpr int S = N / NC;              // fine table W_N^lo, lo < S
   static constexpr int LOGS = ilog2(S);
   static constexpr int BUF1 = W1 * (N1 + 1), BUF2 = W2 * (N2 + 1);
-  static constexpr int BUF = BUF1 > BUF2 ? BUF1 : BUF2;
+  static constexpr int XPULL = N1 * (W1 + 1);   // pull layout: [c][b_local]
+  static constexpr int BUF = BUF1 > BUF2 ? (BUF1 > XPULL ? BUF1 : XPULL) : (BUF2 > XPULL ? BUF2 : XPULL);
   static constexpr size_t SMEM = (size_t)(NC + S + BUF) * sizeof(float2);
 };
 
-template <int N1, int N2, int C>
-__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::THREADS)
+// MODE 0: push — each CTA stores its Z' slices into the owners' buffers
+//         (st.shared::cluster) between two cluster barriers.
+// MODE 1: pull — each CTA publishes Z' in its own buffer and loads what it
+//         owns from the others (ld.shared::cluster).  Measured 3x slower.
+// MODE 2: async — the input tile arrives by bulk copies (TMA engine,
+//         cp.async.bulk, one 256 B row per thread) on an mbarrier; Z' goes
+//         out with st.async, each element signalling the owner's receive
+//         mbarrier, so the only cluster-wide barrier is a split, fence-free
+//         "my buffer is free" arrive/wait that overlaps the twiddle pass.
+template <int N1, int N2, int C, int MODE>
+__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::THREADS, 1024 / ClusterCfg<N1, N2, C>::THREADS)
 fft_cluster_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                    const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
   using Cfg = ClusterCfg<N1, N2, C>;
   constexpr int R = Cfg::R, N = Cfg::N, W1 = Cfg::W1, W2 = Cfg::W2, T1 = Cfg::T1, T2 = Cfg::T2;
-  extern __shared__ float2 smem[];
+  extern __shared__ __align__(128) float2 smem[];
+  __shared__ uint64_t bars[2];  // [0] input tile landed, [1] Z' slice received
   float2* coarse = smem;
   float2* fine = smem + Cfg::NC;
   float2* buf = fine + Cfg::S;
 
-  cg::cluster_group cluster = cg::this_cluster();
-  const int p = (int)cluster.block_rank();
+  const int p = (int)cluster_ctarank();
   const int64_t t = blockIdx.x / C;
   const int tid = threadIdx.x;
-
-  // pass 1: column FFTs over a for b in this CTA's slice
   const int j = tid / W1, col = tid - (tid / W1) * W1;
   const int b = p * W1 + col;
   float2 v[R];
-  const float2* src = in + t * N + b;
+
+  if constexpr (MODE == 2) {
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(&bars[0], (uint32_t)(N1 * W1 * sizeof(float2)));
+      mbar_arrive_expect_tx(&bars[1], (uint32_t)(N2 * W2 * sizeof(float2)));
+    }
+    __syncthreads();
+    if (tid < N1)  // row a of the tile: W1 contiguous complex values
+      bulk_g2s(buf + tid * W1, in + t * N + (int64_t)tid * N2 + p * W1, W1 * sizeof(float2), &bars[0]);
+    for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+    for (int e = tid; e < Cfg::S; e += Cfg::THREADS) fine[e] = fine_g[e];
+    mbar_wait(&bars[0], 0);
 #pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = __ldcs(src + (int64_t)(j + T1 * i) * N2);
-  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
-  for (int e = tid; e < Cfg::S; e += Cfg::THREADS) fine[e] = fine_g[e];
+    for (int i = 0; i < R; ++i) v[i] = buf[(j + T1 * i) * W1 + col];
+  } else {
+    const float2* src = in + t * N + b;
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = __ldcs(src + (int64_t)(j + T1 * i) * N2);
+    for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+    for (int e = tid; e < Cfg::S; e += Cfg::THREADS) fine[e] = fine_g[e];
+  }
   __syncthreads();
+
+  // pass 1: column FFTs over a for b in this CTA's slice
   block_fft<N1, R>(v, j, buf + col * (N1 + 1), MapIdentity{}, coarse, Cfg::NC / N1);
+  if constexpr (MODE == 2) cluster_arrive_relaxed();  // this CTA no longer reads buf
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int e = b * (j + T1 * i);  // b*c < N: exact in int32
     v[i] = cmul(v[i], cmul(coarse[e >> Cfg::LOGS], fine[e & (Cfg::S - 1)]));
   }
 
-  cluster.sync();  // every CTA has finished reading its own buffer
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int c = j + T1 * i;
-    const int q = c / W2, cl = c - (c / W2) * W2;
-    float2* dst = cluster.map_shared_rank(buf, q);
-    dst[cl * (N2 + 1) + b] = v[i];
-  }
-  cluster.sync();  // all Z' slices delivered
-
-  // pass 2: row FFTs over b for c in this CTA's slice
   const int j2 = tid / W2, cl = tid - (tid / W2) * W2;
   float2* row = buf + cl * (N2 + 1);
+  if constexpr (MODE == 2) {
+    cluster_wait();  // every destination buffer is free and its mbarrier initialised
+    const uint32_t base = smem_u32(buf);
+    const uint32_t rbar = smem_u32(&bars[1]);
 #pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = row[j2 + T2 * i];
-  __syncthreads();
+    for (int i = 0; i < R; ++i) {
+      const int c = j + T1 * i;
+      const int q = c / W2, cq = c - (c / W2) * W2;
+      st_async_f2(mapa_u32(base + (uint32_t)((cq * (N2 + 1) + b) * sizeof(float2)), q), v[i],
+                  mapa_u32(rbar, q));
+    }
+    mbar_wait(&bars[1], 0);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = row[j2 + T2 * i];
+    __syncthreads();
+  } else if constexpr (MODE == 0) {
+    cluster_sync();  // every CTA has finished reading its own buffer
+    const uint32_t base = smem_u32(buf);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = j + T1 * i;
+      const int q = c / W2, cq = c - (c / W2) * W2;
+      st_cluster(mapa_u32(base + (uint32_t)((cq * (N2 + 1) + b) * sizeof(float2)), q), v[i]);
+    }
+    cluster_sync();  // all Z' slices delivered
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = row[j2 + T2 * i];
+    __syncthreads();
+  } else {
+    __syncthreads();  // pass-1 exchange reads of buf are done
+#pragma unroll
+    for (int i = 0; i < R; ++i) buf[(j + T1 * i) * (W1 + 1) + col] = v[i];
+    cluster_sync();  // every Z' slice is published
+    const int c = p * W2 + cl;
+    const uint32_t base = smem_u32(buf) + (uint32_t)(c * (W1 + 1) * sizeof(float2));
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int bb = j2 + T2 * i;
+      const int q = bb / W1, bl = bb - (bb / W1) * W1;
+      v[i] = ld_cluster(mapa_u32(base + (uint32_t)(bl * sizeof(float2)), q));
+    }
+    cluster_arrive();  // done reading the other CTAs' buffers
+    cluster_wait();    // ... and they are done reading ours before it is reused
+  }
+
+  // pass 2: row FFTs over b for c in this CTA's slice
   block_fft<N2, R>(v, j2, row, MapIdentity{}, coarse, Cfg::NC / N2);
   const int c = p * W2 + cl;
   float2* dst = out + t * N + c;
@@ -273,9 +334,432 @@ static int launch_small(const float2* in, float2* out, int64_t batch, const floa
   return DPP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// MODE 3 (default): persistent clusters.  Each cluster loops over transforms
+// t = cluster, cluster + nclusters, ...  Per transform and CTA:
+//   one TMA tile load (64 KB box) on mbarrier bars[0] — issued for t+1 as
+//   soon as pass 2 has drained the buffer, so it overlaps the stores and the
+//   next iteration's wait; pass 1; split fence-free cluster barrier ("my
+//   buffer is free"); four-step twiddles by a per-thread recurrence (no
+//   table lookups); st.async scatter signalling the owners' bars[1]; pass 2;
+//   streaming stores.  Twiddle tables are loaded once per CTA.
 template <int N1, int N2, int C>
-static int prepare_cluster() {
-  auto kern = fft_cluster_kernel<N1, N2, C>;
+__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::THREADS, 1024 / ClusterCfg<N1, N2, C>::THREADS)
+fft_cluster_persistent(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, int64_t batch,
+                       const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
+  using Cfg = ClusterCfg<N1, N2, C>;
+  constexpr int R = Cfg::R, N = Cfg::N, W1 = Cfg::W1, W2 = Cfg::W2, T1 = Cfg::T1, T2 = Cfg::T2;
+  constexpr uint32_t TILE_BYTES = N1 * W1 * sizeof(float2);
+  constexpr uint32_t RECV_BYTES = N2 * W2 * sizeof(float2);
+  extern __shared__ __align__(128) float2 smem[];
+  __shared__ uint64_t bars[2];
+  float2* coarse = smem;
+  float2* fine = smem + Cfg::NC;
+  float2* buf = fine + Cfg::S;
+
+  const int p = (int)cluster_ctarank();
+  const int64_t cluster = blockIdx.x / C;
+  const int64_t nclusters = gridDim.x / C;
+  const int tid = threadIdx.x;
+  const int j = tid / W1, col = tid - (tid / W1) * W1;
+  const int b = p * W1 + col;
+  const int j2 = tid / W2, cl = tid - (tid / W2) * W2;
+  float2* row = buf + cl * (N2 + 1);
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if (cluster < batch) {
+      mbar_arrive_expect_tx(&bars[0], TILE_BYTES);
+      tma_load_2d(buf, &tin, p * W1, (int)(cluster * N1), &bars[0]);
+    }
+  }
+  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+  for (int e = tid; e < Cfg::S; e += Cfg::THREADS) fine[e] = fine_g[e];
+  __syncthreads();
+  const uint32_t base = smem_u32(buf);
+  const uint32_t rbar = smem_u32(&bars[1]);
+
+  uint32_t phase = 0;
+  for (int64_t t = cluster; t < batch; t += nclusters, phase ^= 1) {
+    float2 v[R];
+    mbar_wait(&bars[0], phase);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = buf[(j + T1 * i) * W1 + col];
+    if (tid == 0) mbar_arrive_expect_tx(&bars[1], RECV_BYTES);
+    __syncthreads();
+    block_fft<N1, R>(v, j, buf + col * (N1 + 1), MapIdentity{}, coarse, Cfg::NC / N1);
+    cluster_arrive_relaxed();  // this CTA no longer reads buf
+    {
+      // four-step twiddles W_N^{b*(j + T1*i)} = w0 * step^i (a short recurrence
+      // instead of 2 bank-conflicting table reads per element)
+      const int e0 = b * j, es = b * T1;
+      float2 w = cmul(coarse[e0 >> Cfg::LOGS], fine[e0 & (Cfg::S - 1)]);
+      const float2 step = cmul(coarse[es >> Cfg::LOGS], fine[es & (Cfg::S - 1)]);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        v[i] = cmul(v[i], w);
+        w = cmul(w, step);
+      }
+    }
+    cluster_wait();  // every destination buffer is free (and its mbarrier armed)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = j + T1 * i;
+      const int q = c / W2, cq = c - (c / W2) * W2;
+      st_async_f2(mapa_u32(base + (uint32_t)((cq * (N2 + 1) + b) * sizeof(float2)), q), v[i],
+                  mapa_u32(rbar, q));
+    }
+    mbar_wait(&bars[1], phase);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = row[j2 + T2 * i];
+    __syncthreads();
+    block_fft<N2, R>(v, j2, row, MapIdentity{}, coarse, Cfg::NC / N2);  // ends with a CTA barrier
+    if (tid == 0 && t + nclusters < batch) {
+      mbar_arrive_expect_tx(&bars[0], TILE_BYTES);
+      tma_load_2d(buf, &tin, p * W1, (int)((t + nclusters) * N1), &bars[0]);
+    }
+    float2* dst = out + t * N + p * W2 + cl;
+#pragma unroll
+    for (int i = 0; i < R; ++i) __stcs(dst + (int64_t)(j2 + T2 * i) * N1, v[i]);
+  }
+}
+
+template <int N1, int N2, int C>
+static int prepare_persistent(int* max_clusters) {
+  using Cfg = ClusterCfg<N1, N2, C>;
+  auto kern = fft_cluster_persistent<N1, N2, C>;
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+  if (C > 8) DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 1024, 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DPP_CUDA_CHECK(cudaOccupancyMaxActiveClusters(max_clusters, kern, &cfg));
+  if (*max_clusters < 1) return fail(DPP_ENOTSUP, "cluster of %d CTAs cannot be scheduled", C);
+  return DPP_OK;
+}
+
+template <int N1, int N2, int C>
+static int launch_persistent(const float2* in, float2* out, int64_t batch, const float2* coarse,
+                             const float2* fine, int max_clusters, cudaStream_t s) {
+  using Cfg = ClusterCfg<N1, N2, C>;
+  CUtensorMap tmap;
+  int rc = make_tmap_c64(&tmap, in, (uint64_t)batch * N1, N2, N1, Cfg::W1);
+  if (rc) return rc;
+  const int64_t clusters = batch < max_clusters ? batch : max_clusters;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(clusters * C), 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_cluster_persistent<N1, N2, C>, tmap, out, batch, coarse, fine));
+  return DPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// MODE 4 (default): column pairs.  Same four-step/DSMEM schedule as MODE 2,
+// but every thread carries two adjacent columns (256 threads per CTA), so
+//   - the input tile arrives by ONE 2-D TMA load (box W1 x N1) per CTA;
+//   - all shared-memory traffic is 16-byte LDS.128/STS.128 over contiguous
+//     256-byte rows (block_fft_pair): no bank conflicts, half the MIO ops;
+//   - the Z' scatter is one 16-byte st.async per element pair, into an
+//     XOR-swizzled receive layout so the pass-2 reads are conflict-free too;
+//   - outputs leave as 16-byte streaming stores (256 B per half-warp).
+template <int N1, int N2, int C>
+struct PairCfg {
+  static constexpr int R = 16;
+  static constexpr int N = N1 * N2;
+  static constexpr int W1 = N2 / C, W2 = N1 / C;
+  static constexpr int P1 = W1 / 2, P2 = W2 / 2;
+  static constexpr int T1 = N1 / R, T2 = N2 / R;
+  static constexpr int THREADS = P1 * T1;
+  static_assert(THREADS == P2 * T2, "pass thread counts must agree");
+  static constexpr int NC = N1 > N2 ? N1 : N2;
+  static constexpr int S = N / NC;
+  static constexpr int LOGS = ilog2(S);
+  static constexpr int BUF = N / C;
+  static constexpr size_t SMEM = (size_t)(NC + S + BUF) * sizeof(float2);
+};
+
+// receive-layout swizzle: element (cl, b) lives at cl*N2 + (b ^ rsw(cl))
+__device__ __forceinline__ int rsw(int cl) { return ((cl >> 1) & 7) << 1; }
+
+template <int N1, int N2, int C>
+__global__ void __launch_bounds__(PairCfg<N1, N2, C>::THREADS, 2)
+fft_cluster_pair(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out,
+                 const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
+  using Cfg = PairCfg<N1, N2, C>;
+  constexpr int R = Cfg::R, N = Cfg::N, W1 = Cfg::W1, W2 = Cfg::W2, T1 = Cfg::T1, T2 = Cfg::T2;
+  constexpr int P1 = Cfg::P1, P2 = Cfg::P2;
+  extern __shared__ __align__(128) float2 smem[];
+  __shared__ uint64_t bars[2];
+  float2* coarse = smem;
+  float2* fine = smem + Cfg::NC;
+  float2* buf = fine + Cfg::S;
+
+  const int p = (int)cluster_ctarank();
+  const int64_t t = blockIdx.x / C;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bars[0], (uint32_t)(N1 * W1 * sizeof(float2)));
+    mbar_arrive_expect_tx(&bars[1], (uint32_t)(N2 * W2 * sizeof(float2)));
+    tma_load_2d(buf, &tin, p * W1, (int)(t * N1), &bars[0]);
+  }
+  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+  for (int e = tid; e < Cfg::S; e += Cfg::THREADS) fine[e] = fine_g[e];
+  __syncthreads();
+
+  // pass 1: columns b0 = p*W1 + 2cp and b0 + 1, FFT over a
+  const int cp = tid % P1, j = tid / P1;
+  float2 v0[R], v1[R];
+  mbar_wait(&bars[0], 0);
+  {
+    const float4* tile = reinterpret_cast<const float4*>(buf) + cp;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float4 x = tile[(j + T1 * i) * P1];
+      v0[i] = make_float2(x.x, x.y);
+      v1[i] = make_float2(x.z, x.w);
+    }
+  }
+  __syncthreads();
+  block_fft_pair<N1, R, W1>(v0, v1, j, cp, buf, coarse, Cfg::NC / N1);
+  cluster_arrive_relaxed();  // this CTA no longer reads buf
+  const int b0 = p * W1 + 2 * cp;
+  {
+    // W_N^{b0 c} and W_N^{(b0+1) c} for c = j + T1*i by recurrences in i
+    auto tw = [&](int e) { return cmul(coarse[e >> Cfg::LOGS], fine[e & (Cfg::S - 1)]); };
+    float2 w = tw(b0 * j), u = tw(j);
+    const float2 sw = tw(b0 * T1), su = tw(T1);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      v0[i] = cmul(v0[i], w);
+      v1[i] = cmul(v1[i], cmul(w, u));
+      w = cmul(w, sw);
+      u = cmul(u, su);
+    }
+  }
+  cluster_wait();  // every destination buffer is free and its mbarrier armed
+  {
+    const uint32_t base = smem_u32(buf);
+    const uint32_t rbar = smem_u32(&bars[1]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = j + T1 * i;
+      const int q = c / W2, cl = c - q * W2;
+      const uint32_t off = (uint32_t)((cl * N2 + (b0 ^ rsw(cl))) * sizeof(float2));
+      st_async_f4(mapa_u32(base + off, q), make_float4(v0[i].x, v0[i].y, v1[i].x, v1[i].y), mapa_u32(rbar, q));
+    }
+  }
+  mbar_wait(&bars[1], 0);
+
+  // pass 2: c0 = p*W2 + 2cp2 and c0 + 1, FFT over b
+  const int cp2 = tid % P2, j2 = tid / P2;
+  {
+    const int cl0 = 2 * cp2, cl1 = cl0 + 1;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int b = j2 + T2 * i;
+      v0[i] = buf[cl0 * N2 + (b ^ rsw(cl0))];
+      v1[i] = buf[cl1 * N2 + (b ^ rsw(cl1))];
+    }
+  }
+  __syncthreads();
+  block_fft_pair<N2, R, W2>(v0, v1, j2, cp2, buf, coarse, Cfg::NC / N2);
+  float4* dst = reinterpret_cast<float4*>(out + t * N + p * W2 + 2 * cp2);
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    __stcs(dst + (int64_t)(j2 + T2 * i) * (N1 / 2), make_float4(v0[i].x, v0[i].y, v1[i].x, v1[i].y));
+}
+
+// MODE 5: one column per thread (512 threads, 64 registers -> 2 CTAs = 32
+// warps per SM) with the same conflict-free row layouts as MODE 4: exchanges
+// in [element][W] rows (a warp's 32 columns = one 256 B row), an XOR-
+// swizzled receive buffer, one TMA tile load and recurrence twiddles.
+struct MapRow {
+  int w, col;
+  __device__ __forceinline__ int operator()(int e) const { return e * w + col; }
+};
+
+// SEPRECV (MODE 6): a separate receive buffer, so no CTA ever has to wait for
+// the others to stop using theirs — the only cluster barrier (mbarrier-init
+// visibility) is arrived at kernel start and waited just before the scatter.
+template <int N1, int N2, int C, bool SEPRECV>
+struct RowsCfg {
+  using Base = ClusterCfg<N1, N2, C>;
+  static constexpr int TILE = N1 * N2 / C;
+  static constexpr int BUF = TILE;
+  static constexpr size_t SMEM = (size_t)(Base::NC + BUF + (SEPRECV ? TILE : 0)) * sizeof(float2);
+};
+
+template <int N1, int N2, int C, bool SEPRECV>
+__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::THREADS, 1024 / ClusterCfg<N1, N2, C>::THREADS)
+fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out,
+                 const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
+  using Cfg = ClusterCfg<N1, N2, C>;
+  using RC = RowsCfg<N1, N2, C, SEPRECV>;
+  constexpr int R = Cfg::R, N = Cfg::N, W1 = Cfg::W1, W2 = Cfg::W2, T1 = Cfg::T1, T2 = Cfg::T2;
+  extern __shared__ __align__(128) float2 smem[];
+  __shared__ uint64_t bars[2];
+  float2* coarse = smem;
+  float2* buf = smem + Cfg::NC;
+  float2* recv = SEPRECV ? buf + RC::TILE : buf;
+
+  const int p = (int)cluster_ctarank();
+  const int64_t t = blockIdx.x / C;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bars[0], (uint32_t)(N1 * W1 * sizeof(float2)));
+    mbar_arrive_expect_tx(&bars[1], (uint32_t)(N2 * W2 * sizeof(float2)));
+    tma_load_2d(buf, &tin, p * W1, (int)(t * N1), &bars[0]);
+  }
+  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+  __syncthreads();
+  if constexpr (SEPRECV) cluster_arrive_relaxed();  // mbarriers initialised
+
+  const int col = tid % W1, j = tid / W1;
+  float2 v[R];
+  mbar_wait(&bars[0], 0);
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = buf[(j + T1 * i) * W1 + col];
+  __syncthreads();
+  block_fft<N1, R>(v, j, buf, MapRow{W1, col}, coarse, Cfg::NC / N1);
+  if constexpr (!SEPRECV) cluster_arrive_relaxed();  // this CTA no longer reads buf
+  const int b = p * W1 + col;
+  {
+    // per-thread four-step bases from the global tables (L1-cached, no bank conflicts)
+    auto tw = [&](int e) { return cmul(__ldg(coarse_g + (e >> Cfg::LOGS)), __ldg(fine_g + (e & (Cfg::S - 1)))); };
+    float2 w = tw(b * j);
+    const float2 sw = tw(b * T1);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      v[i] = cmul(v[i], w);
+      w = cmul(w, sw);
+    }
+  }
+  cluster_wait();
+  {
+    const uint32_t base = smem_u32(recv);
+    const uint32_t rbar = smem_u32(&bars[1]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = j + T1 * i;
+      const int q = c / W2, cl = c - q * W2;
+      const uint32_t off = (uint32_t)((cl * N2 + (b ^ (cl & 15))) * sizeof(float2));
+      st_async_f2(mapa_u32(base + off, q), v[i], mapa_u32(rbar, q));
+    }
+  }
+  mbar_wait(&bars[1], 0);
+  const int cl = tid % W2, j2 = tid / W2;
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = recv[cl * N2 + ((j2 + T2 * i) ^ (cl & 15))];
+  if constexpr (!SEPRECV) __syncthreads();  // SEPRECV: pass 2 exchanges in buf, free since pass 1
+  block_fft<N2, R>(v, j2, buf, MapRow{W2, cl}, coarse, Cfg::NC / N2);
+  float2* dst = out + t * N + p * W2 + cl;
+#pragma unroll
+  for (int i = 0; i < R; ++i) __stcs(dst + (int64_t)(j2 + T2 * i) * N1, v[i]);
+}
+
+template <int N1, int N2, int C, bool SEPRECV>
+static int prepare_rows() {
+  auto kern = fft_cluster_rows<N1, N2, C, SEPRECV>;
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)RowsCfg<N1, N2, C, SEPRECV>::SMEM));
+  if (C > 8) DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  return DPP_OK;
+}
+
+template <int N1, int N2, int C, bool SEPRECV>
+static int launch_rows(const float2* in, float2* out, int64_t batch, const float2* coarse, const float2* fine,
+                       cudaStream_t s) {
+  using Cfg = ClusterCfg<N1, N2, C>;
+  CUtensorMap tmap;
+  int rc = make_tmap_c64(&tmap, in, (uint64_t)batch * N1, N2, N1, Cfg::W1);
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * C), 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = RowsCfg<N1, N2, C, SEPRECV>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_cluster_rows<N1, N2, C, SEPRECV>, tmap, out, coarse, fine));
+  return DPP_OK;
+}
+
+template <int N1, int N2, int C>
+static int prepare_pair() {
+  auto kern = fft_cluster_pair<N1, N2, C>;
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)PairCfg<N1, N2, C>::SMEM));
+  if (C > 8) DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  return DPP_OK;
+}
+
+template <int N1, int N2, int C>
+static int launch_pair(const float2* in, float2* out, int64_t batch, const float2* coarse, const float2* fine,
+                       cudaStream_t s) {
+  using Cfg = PairCfg<N1, N2, C>;
+  CUtensorMap tmap;
+  int rc = make_tmap_c64(&tmap, in, (uint64_t)batch * N1, N2, N1, Cfg::W1);
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * C), 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_cluster_pair<N1, N2, C>, tmap, out, coarse, fine));
+  return DPP_OK;
+}
+
+static int g_cluster_mode = -1;  // DPP_FFT_CLUSTER_MODE=0..4 selects the exchange variant (default 4)
+
+static int cluster_mode() {
+  if (g_cluster_mode < 0) {
+    const char* e = getenv("DPP_FFT_CLUSTER_MODE");
+    g_cluster_mode = e ? (e[0] - '0') : 5;
+    if (g_cluster_mode < 0 || g_cluster_mode > 6) g_cluster_mode = 5;
+  }
+  return g_cluster_mode;
+}
+
+template <int N1, int N2, int C, int MODE>
+static int prepare_cluster_mode() {
+  auto kern = fft_cluster_kernel<N1, N2, C, MODE>;
   DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)ClusterCfg<N1, N2, C>::SMEM));
   if (C > 8) DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -283,10 +767,31 @@ static int prepare_cluster() {
 }
 
 template <int N1, int N2, int C>
-static int launch_cluster(const float2* in, float2* out, int64_t batch, const float2* coarse,
-                          const float2* fine, cudaStream_t s) {
+static int prepare_cluster(FftPlan* p) {
+  p->mode = cluster_mode();
+  switch (p->mode) {
+    case 0: return prepare_cluster_mode<N1, N2, C, 0>();
+    case 1: return prepare_cluster_mode<N1, N2, C, 1>();
+    case 2: return prepare_cluster_mode<N1, N2, C, 2>();
+    case 3: return prepare_persistent<N1, N2, C>(&p->max_clusters);
+    case 5: return prepare_rows<N1, N2, C, false>();
+    case 6: return prepare_rows<N1, N2, C, true>();
+    default: return prepare_pair<N1, N2, C>();
+  }
+}
+
+template <int N1, int N2, int C>
+static int launch_cluster(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s) {
   using Cfg = ClusterCfg<N1, N2, C>;
-  auto kern = fft_cluster_kernel<N1, N2, C>;
+  const float2* coarse = p->tw_a;
+  const float2* fine = p->tw_b;
+  if (p->mode == 3) return launch_persistent<N1, N2, C>(in, out, batch, coarse, fine, p->max_clusters, s);
+  if (p->mode == 4) return launch_pair<N1, N2, C>(in, out, batch, coarse, fine, s);
+  if (p->mode == 5) return launch_rows<N1, N2, C, false>(in, out, batch, coarse, fine, s);
+  if (p->mode == 6) return launch_rows<N1, N2, C, true>(in, out, batch, coarse, fine, s);
+  auto kern = p->mode == 0   ? fft_cluster_kernel<N1, N2, C, 0>
+              : p->mode == 1 ? fft_cluster_kernel<N1, N2, C, 1>
+                             : fft_cluster_kernel<N1, N2, C, 2>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * C), 1, 1);
   cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
@@ -328,20 +833,32 @@ int fft1d_plan_init(FftPlan* p) {
     p->n1a = 1LL << (lg / 2);
     p->n2a = n / p->n1a;
     p->cluster = (int)(n / 8192 > 1 ? n / 8192 : 1);
+    if (n == 65536) {
+      // 16 CTAs of 4096 points (4 CTAs = 32 warps per SM) beat 8 of 8192
+      // (2 per SM): 1.34 vs 1.53 ms for 4096 x 2^16 (profiles/fft_c2_r1.md)
+      const char* e = getenv("DPP_FFT_C65536");
+      p->cluster = (e && atoi(e) == 8) ? 8 : 16;
+    }
     int rc = DPP_OK;
     switch (n) {
-      case 8192: rc = prepare_cluster<64, 128, 1>(); break;
-      case 16384: rc = prepare_cluster<128, 128, 2>(); break;
-      case 32768: rc = prepare_cluster<128, 256, 4>(); break;
-      case 65536: rc = prepare_cluster<256, 256, 8>(); break;
-      case 131072: rc = prepare_cluster<256, 512, 16>(); break;
+      case 8192: rc = prepare_cluster<64, 128, 1>(p); break;
+      case 16384: rc = prepare_cluster<128, 128, 2>(p); break;
+      case 32768: rc = prepare_cluster<128, 256, 4>(p); break;
+      case 65536:
+        rc = p->cluster == 16 ? prepare_cluster<256, 256, 16>(p) : prepare_cluster<256, 256, 8>(p);
+        break;
+      case 131072: rc = prepare_cluster<256, 512, 16>(p); break;
     }
     if (rc) return rc;
     const int64_t nc = p->n1a > p->n2a ? p->n1a : p->n2a;
     if (upload_table(twiddle_table(nc, nc), &p->tw_a)) return DPP_ECUDA;
     if (upload_table(twiddle_table(n, n / nc), &p->tw_b)) return DPP_ECUDA;
-    snprintf(p->desc, sizeof(p->desc), "cluster<%lldx%lld, C=%d> four-step over DSMEM",
-             (long long)p->n1a, (long long)p->n2a, p->cluster);
+    static const char* modes[7] = {"push", "pull", "async", "persistent TMA + st.async",
+                                   "column pairs, TMA tile + st.async", "row layouts, TMA tile + st.async",
+                                   "row layouts, separate receive buffer"};
+    snprintf(p->desc, sizeof(p->desc), "cluster<%lldx%lld, C=%d> four-step over DSMEM (%s%s)",
+             (long long)p->n1a, (long long)p->n2a, p->cluster, modes[p->mode],
+             p->mode == 3 ? (std::string(", ") + std::to_string(p->max_clusters) + " clusters").c_str() : "");
     return DPP_OK;
   }
   return fail(DPP_ENOTSUP, "1-D transform size 2^%d is above the 2^17 single-pass limit", lg);
@@ -358,11 +875,13 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
     }
   } else if (p->kind == FftPlan::CLUSTER) {
     switch (p->n0) {
-      case 8192: return launch_cluster<64, 128, 1>(in, out, batch, p->tw_a, p->tw_b, s);
-      case 16384: return launch_cluster<128, 128, 2>(in, out, batch, p->tw_a, p->tw_b, s);
-      case 32768: return launch_cluster<128, 256, 4>(in, out, batch, p->tw_a, p->tw_b, s);
-      case 65536: return launch_cluster<256, 256, 8>(in, out, batch, p->tw_a, p->tw_b, s);
-      case 131072: return launch_cluster<256, 512, 16>(in, out, batch, p->tw_a, p->tw_b, s);
+      case 8192: return launch_cluster<64, 128, 1>(p, in, out, batch, s);
+      case 16384: return launch_cluster<128, 128, 2>(p, in, out, batch, s);
+      case 32768: return launch_cluster<128, 256, 4>(p, in, out, batch, s);
+      case 65536:
+        return p->cluster == 16 ? launch_cluster<256, 256, 16>(p, in, out, batch, s)
+                                : launch_cluster<256, 256, 8>(p, in, out, batch, s);
+      case 131072: return launch_cluster<256, 512, 16>(p, in, out, batch, s);
     }
   }
   return fail(DPP_EINVAL, "no kernel for 1-D size %lld", (long long)p->n0);

@@ -75,3 +75,82 @@ __device__ __forceinline__ void block_fft(float2 (&v)[R], int j, float2* buf, Ma
 }
 
 }  // namespace dpp
+
+namespace dpp {
+
+// ---------------------------------------------------------------------------
+// Column-pair variant: each thread runs the same Stockham schedule on TWO
+// adjacent columns (v0 = column 2cp, v1 = column 2cp+1).  Exchanges use a
+// row-major [element][W] layout, so every shared-memory access is one
+// 16-byte LDS.128/STS.128 of a column pair and a half-warp (16 column pairs)
+// covers one contiguous 256-byte row: conflict-free without padding, and
+// half the shared-memory instructions of the single-column form.
+template <int M, int R, int W>
+__device__ __forceinline__ void block_fft_pair(float2 (&v0)[R], float2 (&v1)[R], int j, int cp, float2* buf,
+                                               const float2* tw, int tw_step) {
+  constexpr int T = M / R;
+  constexpr int LOGM = ilog2(M);
+  constexpr int LOGR = ilog2(R);
+  constexpr int REM = LOGM % LOGR;
+  constexpr int NPASS = LOGM / LOGR;
+  constexpr int NS0 = 1 << REM;
+  float4* row = reinterpret_cast<float4*>(buf) + cp;  // element e of the pair at row[e * (W / 2)]
+  constexpr int RS = W / 2;
+  if constexpr (REM != 0) {
+    constexpr int r = 1 << REM;
+    constexpr int S = R / r;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      float2 u0[r], u1[r];
+#pragma unroll
+      for (int q = 0; q < r; ++q) {
+        u0[q] = v0[s + q * S];
+        u1[q] = v1[s + q * S];
+      }
+      dft_r<r>(u0);
+      dft_r<r>(u1);
+      const int jp = j + T * s;
+#pragma unroll
+      for (int q = 0; q < r; ++q) row[(jp * r + q) * RS] = make_float4(u0[q].x, u0[q].y, u1[q].x, u1[q].y);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float4 t = row[(j + T * i) * RS];
+      v0[i] = make_float2(t.x, t.y);
+      v1[i] = make_float2(t.z, t.w);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int pass = 0; pass < NPASS; ++pass) {
+    const int ns = NS0 << (LOGR * pass);
+    const int jm = j & (ns - 1);
+    if (ns > 1) {
+      const int unit = jm * (M / (ns * R));
+#pragma unroll
+      for (int i = 1; i < R; ++i) {
+        const float2 w = tw[(i * unit) * tw_step];
+        v0[i] = cmul(v0[i], w);
+        v1[i] = cmul(v1[i], w);
+      }
+    }
+    dft_r<R>(v0);
+    dft_r<R>(v1);
+    if (ns * R < M) {
+      const int base = (j - jm) * R + jm;
+#pragma unroll
+      for (int i = 0; i < R; ++i) row[(base + i * ns) * RS] = make_float4(v0[i].x, v0[i].y, v1[i].x, v1[i].y);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const float4 t = row[(j + T * i) * RS];
+        v0[i] = make_float2(t.x, t.y);
+        v1[i] = make_float2(t.z, t.w);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace dpp

@@ -17,6 +17,8 @@ struct FftPlan {
   int kind = 0;
   int64_t n1a = 0, n2a = 0;  // cluster split n = n1a * n2a
   int cluster = 1;
+  int mode = 3;              // cluster exchange variant (fft.cu)
+  int max_clusters = 0;      // co-resident clusters for the persistent variant
   float2* tw_a = nullptr;    // coarse twiddles (W_n for SMALL, W_max(n1a,n2a) for CLUSTER)
   float2* tw_b = nullptr;    // fine twiddles W_n^lo
   // rank 2: column pass schedule

@@ -34,7 +34,7 @@ def test_batched_1d_every_size_vs_oracle(cuda, m):
     batch = max(1, min(64, (1 << 19) // n))
     x = complex_signals(100 + m, (batch, n))
     got = _fft(x, n, cuda)
-    ref = fo.fft_rows(x)
+    ref = fo.fft_rows(x, min(3, m))
     errs = [rel_l2(g, r) for g, r in zip(got, ref)]
     assert max(errs) <= tol(n), (n, max(errs))
 
