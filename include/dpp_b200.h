@@ -131,6 +131,22 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
                     uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
                     float* block_grad, float* norm32, void* stream);
 
+/* Training pass of the codec (imgc.py:378-388): per block the mean gradient
+ * magnitude (block_grad, the k-means training filter) and the binary64
+ * normalised block (norm64, blocks x 16) — the k-means input. */
+int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_t width,
+                         int64_t row_stride, int64_t image_stride, int64_t batch, double sigma_min,
+                         double* norm64, float* block_grad, void* stream);
+
+/* k-means codebook trainer (imgc.py:221-273) on device: k-means++ seeding
+ * from the caller's RNG stream (index of the first pick and a HOST array of
+ * k-1 uniforms in [0,1), as numpy's Generator.choice consumes them), then
+ * <= max_iter Lloyd iterations in binary64.  pts: n x 16 doubles (device);
+ * centroids_out: k x 16 floats (device); trace: nullable host array of
+ * max_iter per-iteration SSE values; *iterations = iterations run. */
+int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const double* uniforms,
+               int max_iter, float* centroids_out, double* trace, int* iterations, void* stream);
+
 /* Inverse (imgc.py:426-439), for round-trip tests on device. */
 int dpp_imgc_decode(const uint8_t* records, const uint8_t* cb_plane, const uint8_t* cr_plane,
                     const float* codebook, int n_cb, int64_t height, int64_t width,

@@ -367,8 +367,8 @@ def kmeans(blocks, codebook_size: int, seed: int, max_iter: int = 20, trace: lis
            *, backend: CudaBackend | None = None) -> Codebook:
     """k-means++ + Lloyd on the GPU (algorithm of imgc.py:221-273)."""
     from ..kmeans import kmeans_device
-    return Codebook(kmeans_device(blocks, codebook_size, seed, max_iter, trace,
-                                  device=(backend or CudaBackend()).device))
+    cents = kmeans_device(blocks, codebook_size, seed, max_iter, trace, device=(backend or CudaBackend()).device)
+    return Codebook(cents.cpu().numpy())
 
 
 def kmeans_codebook(px, ch, h, w, codebook_size, seed, sigma_min, grad_min):

@@ -170,6 +170,7 @@ struct EncodeArgs {
   uint8_t* cr_plane;
   float* block_grad;
   float* norm32;
+  double* norm64;  // STATS variant only
 };
 
 template <int CH>
@@ -184,14 +185,18 @@ __device__ __forceinline__ void load_rgb(const uint8_t* row, int64_t x, float& r
   }
 }
 
-template <int CH>
+// STATS = true: the k-means training pass — only block_grad and the binary64
+// normalised blocks (imgc.py:378-388), no chroma, VQ or records.
+template <int CH, bool STATS = false>
 __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
   __shared__ float4 scb[256 * 4];
   __shared__ uint8_t srec[256 * 3];
   const int64_t img = blockIdx.y;
-  const float4* cbk = reinterpret_cast<const float4*>(a.codebook + img * a.codebook_stride);
-  for (int e = threadIdx.x; e < a.ncb * 4; e += blockDim.x) scb[e] = cbk[e];
-  __syncthreads();
+  if constexpr (!STATS) {
+    const float4* cbk = reinterpret_cast<const float4*>(a.codebook + img * a.codebook_stride);
+    for (int e = threadIdx.x; e < a.ncb * 4; e += blockDim.x) scb[e] = cbk[e];
+    __syncthreads();
+  }
 
   const int64_t bw = a.width / 4, bh = a.height / 4, nblocks = bw * bh;
   const int64_t k0 = (int64_t)blockIdx.x * blockDim.x;
@@ -215,8 +220,10 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
         crs = (r == 0 && c == 0) ? o.cr : __fadd_rn(crs, o.cr);
       }
     }
-    a.cb_plane[img * nblocks + k] = q8f(__fmul_rn(cbs, 0.0625f));
-    a.cr_plane[img * nblocks + k] = q8f(__fmul_rn(crs, 0.0625f));
+    if constexpr (!STATS) {
+      a.cb_plane[img * nblocks + k] = q8f(__fmul_rn(cbs, 0.0625f));
+      a.cr_plane[img * nblocks + k] = q8f(__fmul_rn(crs, 0.0625f));
+    }
 
     if (a.block_grad) {
       // forward differences with clamped borders (imgc.py:158-161), hypot
@@ -269,6 +276,13 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
     }
     const double sd = __dsqrt_rn(__ddiv_rn(pw16d(sq), 16.0));
     const double safe = fmax(sd, a.sigma_min);  // np.maximum(sigmas, sigma_min)
+    if constexpr (STATS) {
+      // training rows for the k-means trainer: normalised blocks in binary64
+      double* dst = a.norm64 + (img * nblocks + k) * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dst[i] = __ddiv_rn(bd[i], safe);
+      return;
+    }
     float nb[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) nb[i] = __double2float_rn(__ddiv_rn(bd[i], safe));
@@ -290,11 +304,13 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
     srec[3 * t + 1] = q8d(__dmul_rn(sd, 4.0));  // sd / 0.25 is exact
     srec[3 * t + 2] = (uint8_t)bj;
   }
-  __syncthreads();
-  // records of this CTA are one contiguous run: write it with coalesced bytes
-  const int64_t nrec = (nblocks - k0 < (int64_t)blockDim.x ? nblocks - k0 : (int64_t)blockDim.x) * 3;
-  uint8_t* rec = a.records + (img * nblocks + k0) * 3;
-  for (int e = threadIdx.x; e < nrec; e += blockDim.x) rec[e] = srec[e];
+  if constexpr (!STATS) {
+    __syncthreads();
+    // records of this CTA are one contiguous run: write it with coalesced bytes
+    const int64_t nrec = (nblocks - k0 < (int64_t)blockDim.x ? nblocks - k0 : (int64_t)blockDim.x) * 3;
+    uint8_t* rec = a.records + (img * nblocks + k0) * 3;
+    for (int e = threadIdx.x; e < nrec; e += blockDim.x) rec[e] = srec[e];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -415,7 +431,7 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
   if (batch == 0) return DPP_OK;
   if (!(sigma_min > 0.0)) return dpp::fail(DPP_EINVAL, "sigma_min must be > 0");
   dpp::EncodeArgs a{px, height, width, row_stride, image_stride, codebook, n_cb, codebook_stride, sigma_min,
-                    records, cb_plane, cr_plane, block_grad, norm32};
+                    records, cb_plane, cr_plane, block_grad, norm32, nullptr};
   const int64_t nblocks = (height / 4) * (width / 4);
   dim3 grid(dpp::grid1(nblocks, 256), (unsigned)batch);
   auto s = (cudaStream_t)stream;
@@ -425,6 +441,31 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
     default: dpp::encode_kernel<4><<<grid, 256, 0, s>>>(a); break;
   }
   DPP_LAUNCH_CHECK("encode_kernel");
+  return DPP_OK;
+}
+
+int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
+                         int64_t image_stride, int64_t batch, double sigma_min, double* norm64,
+                         float* block_grad, void* stream) {
+  if (height % 4 || width % 4 || height < 4 || width < 4)
+    return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
+                     (long long)height);
+  if (channels != 1 && channels != 3 && channels != 4)
+    return dpp::fail(DPP_EINVAL, "channels must be 1, 3 or 4, got %d", channels);
+  if (!norm64 || !block_grad) return dpp::fail(DPP_EINVAL, "norm64 and block_grad are required");
+  if (batch < 0 || batch > 65535) return dpp::fail(DPP_EINVAL, "batch must be in 0..65535");
+  if (batch == 0) return DPP_OK;
+  dpp::EncodeArgs a{px, height, width, row_stride, image_stride, nullptr, 0, 0, sigma_min,
+                    nullptr, nullptr, nullptr, block_grad, nullptr, norm64};
+  const int64_t nblocks = (height / 4) * (width / 4);
+  dim3 grid(dpp::grid1(nblocks, 256), (unsigned)batch);
+  auto s = (cudaStream_t)stream;
+  switch (channels) {
+    case 1: dpp::encode_kernel<1, true><<<grid, 256, 0, s>>>(a); break;
+    case 3: dpp::encode_kernel<3, true><<<grid, 256, 0, s>>>(a); break;
+    default: dpp::encode_kernel<4, true><<<grid, 256, 0, s>>>(a); break;
+  }
+  DPP_LAUNCH_CHECK("encode_kernel<stats>");
   return DPP_OK;
 }
 

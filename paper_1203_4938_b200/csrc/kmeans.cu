@@ -1,0 +1,248 @@
+// GPU k-means codebook trainer following the reference
+// algorithm /root/reference/pkg/src/dpp/apps/imgc.py:221-273:
+//   k-means++ seeding driven by the caller's RNG stream (first pick index and
+//   one uniform per further centroid, as numpy's Generator.choice consumes
+//   them), then <= max_iter Lloyd iterations (assign to nearest centroid,
+//   centroid = member mean, empty cluster -> farthest point from its assigned
+//   centroid, stop when assignments repeat), binary64 throughout.
+// Parity with the host trainer is tolerance-based (the reference's GEMM-based
+// distances and sequential cumsum are CPU/BLAS dependent), see tests.
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dpp {
+
+constexpr int KD = 16;  // block vectors are 16-dim
+
+__device__ __forceinline__ double dist2(const double* a, const double* c) {
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < KD; ++m) {
+    const double d = a[m] - c[m];
+    s = fma(d, d, s);
+  }
+  return s;
+}
+
+// d2[i] = min(d2[i], |p_i - c|^2) (or init when first); per-block partial sums
+__global__ void kpp_update(const double* __restrict__ pts, int64_t n, const double* __restrict__ c,
+                           double* __restrict__ d2, double* __restrict__ block_sums, int first) {
+  __shared__ double cs[KD];
+  __shared__ double red[32];
+  if (threadIdx.x < KD) cs[threadIdx.x] = c[threadIdx.x];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    const double d = dist2(pts + i * KD, cs);
+    v = first ? d : fmin(d2[i], d);
+    d2[i] = v;
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
+  }
+}
+
+// single CTA: scan block sums, locate u*total, then the point inside the block
+// (first index whose inclusive prefix exceeds the target: searchsorted 'right')
+__global__ void kpp_pick(const double* __restrict__ d2, int64_t n, const double* __restrict__ block_sums,
+                         int nblocks, int block, double u, const double* __restrict__ pts,
+                         double* __restrict__ centroid, int64_t* __restrict__ pick_out) {
+  __shared__ double total_s;
+  __shared__ int64_t pick_s;
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int b = 0; b < nblocks; ++b) total += block_sums[b];
+    int64_t pick = -1;
+    if (total <= 0.0) {
+      pick = (int64_t)(u * (double)n);  // degenerate: uniform pick
+      if (pick >= n) pick = n - 1;
+    } else {
+      const double target = u * total;
+      double acc = 0.0;
+      int b = 0;
+      for (; b < nblocks - 1; ++b) {
+        if (acc + block_sums[b] > target) break;
+        acc += block_sums[b];
+      }
+      const int64_t lo = (int64_t)b * block, hi = lo + block < n ? lo + block : n;
+      pick = hi - 1;
+      for (int64_t i = lo; i < hi; ++i) {
+        acc += d2[i];
+        if (acc > target) { pick = i; break; }
+      }
+    }
+    total_s = total;
+    pick_s = pick;
+    *pick_out = pick;
+  }
+  __syncthreads();
+  if (threadIdx.x < KD) centroid[threadIdx.x] = pts[pick_s * KD + threadIdx.x];
+  (void)total_s;
+}
+
+// nearest centroid (first minimum), counts changes vs previous assignment,
+// accumulates per-cluster sums/counts in shared memory then globally
+__global__ void lloyd_assign(const double* __restrict__ pts, int64_t n, const double* __restrict__ cents, int k,
+                             int32_t* __restrict__ assign, double* __restrict__ sums,
+                             unsigned long long* __restrict__ counts, unsigned long long* __restrict__ changed,
+                             double* __restrict__ sse) {
+  extern __shared__ double sh[];
+  double* sc = sh;                  // k * KD centroids
+  double* ssum = sh + k * KD;       // k * KD partial sums
+  unsigned int* scnt = reinterpret_cast<unsigned int*>(ssum + k * KD);
+  for (int e = threadIdx.x; e < k * KD; e += blockDim.x) {
+    sc[e] = cents[e];
+    ssum[e] = 0.0;
+  }
+  for (int e = threadIdx.x; e < k; e += blockDim.x) scnt[e] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double local_sse = 0.0;
+  if (i < n) {
+    double p[KD];
+#pragma unroll
+    for (int m = 0; m < KD; ++m) p[m] = pts[i * KD + m];
+    double best = 1.0 / 0.0;
+    int bj = 0;
+    for (int j = 0; j < k; ++j) {
+      const double d = dist2(p, sc + j * KD);
+      if (d < best) { best = d; bj = j; }
+    }
+    local_sse = best;
+    if (assign[i] != bj) atomicAdd(changed, 1ULL);
+    assign[i] = bj;
+#pragma unroll
+    for (int m = 0; m < KD; ++m) atomicAdd(&ssum[bj * KD + m], p[m]);
+    atomicAdd(&scnt[bj], 1u);
+  }
+  for (int o = 16; o > 0; o >>= 1) local_sse += __shfl_xor_sync(0xffffffffu, local_sse, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(sse, local_sse);
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * KD; e += blockDim.x)
+    if (ssum[e] != 0.0) atomicAdd(&sums[e], ssum[e]);
+  for (int e = threadIdx.x; e < k; e += blockDim.x)
+    if (scnt[e]) atomicAdd(&counts[e], (unsigned long long)scnt[e]);
+}
+
+__global__ void lloyd_means(double* __restrict__ cents, const double* __restrict__ sums,
+                            const unsigned long long* __restrict__ counts, int k) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * KD && counts[e / KD]) cents[e] = sums[e] / (double)counts[e / KD];
+}
+
+// farthest point from its assigned centroid (for empty-cluster reseeding)
+__global__ void far_point(const double* __restrict__ pts, int64_t n, const double* __restrict__ cents,
+                          const int32_t* __restrict__ assign, unsigned long long* __restrict__ best) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double d = dist2(pts + i * KD, cents + (int64_t)assign[i] * KD);
+  // pack (distance as f32 bits, inverted index): atomicMax picks the largest
+  // distance and, among equal ones, the lowest index (np.argmax)
+  atomicMax(best, ((unsigned long long)__float_as_uint((float)d) << 32) | (0xffffffffu - (uint32_t)i));
+}
+
+}  // namespace dpp
+
+extern "C" {
+
+int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const double* uniforms, int max_iter,
+               float* centroids_out, double* trace, int* iterations, void* stream) {
+  using namespace dpp;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (n < 1) return fail(DPP_EINVAL, "no blocks to cluster");
+  if (k < 1 || k > 256) return fail(DPP_EINVAL, "codebook size must be in 1..256");
+  if (k > n) return fail(DPP_EINVAL, "codebook size %d exceeds %lld training blocks", k, (long long)n);
+  if (n > 0x7fffffffLL) return fail(DPP_EINVAL, "too many training blocks");
+  const int T = 256;
+  const int nb = (int)((n + T - 1) / T);
+  double *d2, *bsum, *cents, *sums, *sse;
+  int32_t* assign;
+  unsigned long long *counts, *changed, *far;
+  int64_t* pick;
+  DPP_CUDA_CHECK(cudaMallocAsync(&d2, n * sizeof(double), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&bsum, nb * sizeof(double), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&cents, (size_t)k * KD * sizeof(double), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&sums, (size_t)k * KD * sizeof(double), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&sse, sizeof(double), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&assign, n * sizeof(int32_t), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&counts, k * sizeof(unsigned long long), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&changed, sizeof(unsigned long long), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&far, sizeof(unsigned long long), s));
+  DPP_CUDA_CHECK(cudaMallocAsync(&pick, sizeof(int64_t), s));
+
+  // k-means++ seeding
+  DPP_CUDA_CHECK(cudaMemcpyAsync(cents, pts + first_pick * KD, KD * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (int j = 1; j < k; ++j) {
+    kpp_update<<<nb, T, 0, s>>>(pts, n, cents + (j - 1) * KD, d2, bsum, j == 1);
+    kpp_pick<<<1, 32, 0, s>>>(d2, n, bsum, nb, T, uniforms[j - 1], pts, cents + j * KD, pick);
+  }
+  DPP_LAUNCH_CHECK("k-means++ seeding");
+
+  // Lloyd
+  DPP_CUDA_CHECK(cudaMemsetAsync(assign, 0xff, n * sizeof(int32_t), s));  // -1: every point "changes"
+  const size_t shm = (size_t)k * KD * 2 * sizeof(double) + k * sizeof(unsigned int);
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  std::vector<unsigned long long> hcounts(k);
+  int it = 0;
+  // first assignment
+  auto assign_pass = [&](unsigned long long* h_changed, double* h_sse) -> int {
+    DPP_CUDA_CHECK(cudaMemsetAsync(sums, 0, (size_t)k * KD * sizeof(double), s));
+    DPP_CUDA_CHECK(cudaMemsetAsync(counts, 0, k * sizeof(unsigned long long), s));
+    DPP_CUDA_CHECK(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), s));
+    DPP_CUDA_CHECK(cudaMemsetAsync(sse, 0, sizeof(double), s));
+    lloyd_assign<<<nb, T, shm, s>>>(pts, n, cents, k, assign, sums, counts, changed, sse);
+    DPP_LAUNCH_CHECK("lloyd_assign");
+    DPP_CUDA_CHECK(cudaMemcpyAsync(h_changed, changed, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    DPP_CUDA_CHECK(cudaMemcpyAsync(h_sse, sse, sizeof(double), cudaMemcpyDeviceToHost, s));
+    DPP_CUDA_CHECK(cudaMemcpyAsync(hcounts.data(), counts, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    DPP_CUDA_CHECK(cudaStreamSynchronize(s));
+    return DPP_OK;
+  };
+  unsigned long long h_changed = 0;
+  double h_sse = 0.0;
+  if (int rc = assign_pass(&h_changed, &h_sse)) return rc;
+  for (; it < max_iter; ++it) {
+    // centroid = member mean; empty cluster -> farthest point (in index order)
+    lloyd_means<<<(k * KD + 255) / 256, 256, 0, s>>>(cents, sums, counts, k);
+    for (int j = 0; j < k; ++j) {
+      if (hcounts[j]) continue;
+      DPP_CUDA_CHECK(cudaMemsetAsync(far, 0, sizeof(unsigned long long), s));
+      far_point<<<nb, T, 0, s>>>(pts, n, cents, assign, far);
+      unsigned long long hf = 0;
+      DPP_CUDA_CHECK(cudaMemcpyAsync(&hf, far, sizeof(hf), cudaMemcpyDeviceToHost, s));
+      DPP_CUDA_CHECK(cudaStreamSynchronize(s));
+      const int32_t idx = (int32_t)(0xffffffffu - (uint32_t)(hf & 0xffffffffu));
+      DPP_CUDA_CHECK(cudaMemcpyAsync(cents + (int64_t)j * KD, pts + (int64_t)idx * KD, KD * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+      DPP_CUDA_CHECK(cudaMemcpyAsync(assign + idx, &j, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      DPP_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    if (int rc = assign_pass(&h_changed, &h_sse)) return rc;
+    if (trace) trace[it] = h_sse;
+    if (h_changed == 0) { ++it; break; }
+  }
+  if (iterations) *iterations = it;
+  // binary64 -> binary32 centroids
+  std::vector<double> hc((size_t)k * KD);
+  DPP_CUDA_CHECK(cudaMemcpyAsync(hc.data(), cents, hc.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPP_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<float> hf(hc.size());
+  for (size_t e = 0; e < hc.size(); ++e) hf[e] = (float)hc[e];
+  DPP_CUDA_CHECK(cudaMemcpyAsync(centroids_out, hf.data(), hf.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  DPP_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (void* ptr : {(void*)d2, (void*)bsum, (void*)cents, (void*)sums, (void*)sse, (void*)assign, (void*)counts,
+                    (void*)changed, (void*)far, (void*)pick})
+    cudaFreeAsync(ptr, s);
+  return DPP_OK;
+}
+
+}  // extern "C"

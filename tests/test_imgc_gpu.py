@@ -151,3 +151,76 @@ def test_c4_full_size_8192_gray(cuda):
     assert np.array_equal(got[:, 1], f["sigma_idx"])
     assert np.array_equal(got[:, 2], f["indices"])
     assert np.array_equal(cbp[: 64 * 2048].cpu().numpy(), f["cb"].ravel())
+
+
+# -- GPU k-means codebook (tolerance parity) ----------------------
+
+def test_block_stats_bit_exact(cuda):
+    import torch
+
+    from paper_1203_4938_b200.kmeans import block_stats_device
+    img = io.synthetic_image(96, 64, seed=22)
+    norm64, grad = block_stats_device(torch.from_numpy(img).to(cuda), 3, 64, 96)
+    y, _, _ = io.ycbcr(img)
+    _, _, ref = io.block_stats(y)
+    assert np.array_equal(norm64.cpu().numpy(), ref)
+    assert np.array_equal(grad.cpu().numpy(), io.gradient(y))
+
+
+def test_kmeans_known_answers(cuda):  # test_imgc.py:90-128
+    from paper_1203_4938_b200.apps import imgc
+    rng = np.random.default_rng(5)
+    a = rng.normal(0, 0.01, (300, 16)) + 4.0
+    b = rng.normal(0, 0.01, (300, 16)) - 4.0
+    cb = imgc.kmeans(np.vstack([a, b]), 2, seed=8)
+    lows, highs = sorted(cb.centroids[:, 0])
+    assert abs(lows - b[:, 0].mean()) < 1e-2 and abs(highs - a[:, 0].mean()) < 1e-2
+    pts = np.array([[float(i)] * 16 for i in range(5)])
+    assert sorted(imgc.kmeans(pts, 5, seed=1).centroids[:, 0].tolist()) == [0, 1, 2, 3, 4]
+    pts = rng.standard_normal((400, 16))
+    trace: list[float] = []
+    imgc.kmeans(pts, 16, seed=2, trace=trace)
+    assert len(trace) >= 1 and all(y <= x + 1e-9 for x, y in zip(trace, trace[1:]))
+    pts = rng.standard_normal((256, 16))
+    assert imgc.kmeans(pts, 32, 9).to_bytes() == imgc.kmeans(pts, 32, 9).to_bytes()
+    with pytest.raises(ValueError, match="exceeds"):
+        imgc.kmeans(np.zeros((3, 16)), 4, seed=0)
+
+
+def test_kmeans_quality_matches_reference_trainer(cuda):
+    """Same training set and seed: the GPU codebook's SSE is within 3% of the
+    reference algorithm's (oracle), and the seeding consumes the same RNG stream."""
+    from paper_1203_4938_b200.apps import imgc
+    img = io.synthetic_image(128, 128, seed=12)
+    y, _, _ = io.ycbcr(img)
+    _, _, norm = io.block_stats(y)
+    train = norm[io.gradient(y) >= 1.0]
+    ref = io.kmeans(train, 64, 0)
+    got = imgc.kmeans(train, 64, 0).centroids
+
+    def sse(c):
+        d = ((train[:, None, :] - c[None].astype(np.float64)) ** 2).sum(-1)
+        return d.min(1).sum()
+
+    assert sse(got) <= 1.03 * sse(ref)
+
+
+def test_compress_without_codebook_end_to_end(cuda, imgc_golden):
+    """compress(image, 256, seed) with the GPU trainer: SPEC acceptance on the
+    512^2 fixture (ratio <= 0.13, PSNR >= 25 dB, deterministic), and quality
+    within 0.5 dB of the reference's own bitstream."""
+    from paper_1203_4938_b200.apps import imgc
+    image = imgc_golden["fix512_cb256_s0_image"]
+    ci = imgc.compress(image, 256, seed=0)
+    blob = ci.to_bytes()
+    assert len(blob) / image.nbytes <= 0.13
+    q = imgc.psnr(image, imgc.decompress(ci))
+    ref = imgc.CompressedImage.from_bytes(imgc_golden["fix512_cb256_s0_blob"].tobytes())
+    q_ref = imgc.psnr(image, imgc.decompress(ref))
+    assert q >= 25.0 and q >= q_ref - 0.5, (q, q_ref)
+    assert imgc.compress(image, 256, seed=0).to_bytes() == blob
+    # uniform gray and single block (test_imgc.py:156-172)
+    gray = np.full((32, 32, 3), 77, np.uint8)
+    ci = imgc.compress(gray, 8, seed=3)
+    assert int(ci.sigma_idx.max()) == 0 and np.array_equal(imgc.decompress(ci), gray)
+    assert len(imgc.compress(io.synthetic_image(4, 4, seed=3), 1, seed=2).means) == 1
