@@ -76,6 +76,12 @@ int dpp_fft_c2c_forward(const dpp_fft_plan* plan, const float* in, float* out,
 int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* out,
                               int64_t batch, void* workspace, void* stream);
 
+/* Column pass only of a rank-2 plan, in place: for each of `batch` n0 x n1
+ * row-major arrays, the n0-point FFT of every column.  The row-sharded 2-D
+ * transform runs it on the column slab each rank holds after the all-to-all
+ * (SURVEY §8(e) C3). */
+int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, void* stream);
+
 void dpp_fft_plan_destroy(dpp_fft_plan* plan);
 
 /* Leaf DFT node dft{2,4,8} (apps/fft.py:86-123): one dense 2^k-point DFT per

@@ -103,6 +103,16 @@ int dpp_fft_c2c_forward(const dpp_fft_plan* plan, const float* in, float* out, v
   return dpp_fft_c2c_forward_batch(plan, in, out, plan->impl.batch, workspace, stream);
 }
 
+int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, void* stream) {
+  if (!plan) return dpp::fail(DPP_EINVAL, "plan is NULL");
+  if (plan->impl.rank != 2) return dpp::fail(DPP_EINVAL, "column pass needs a rank-2 plan");
+  if (batch < 0 || batch > plan->impl.batch)
+    return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch,
+                     (long long)plan->impl.batch);
+  return dpp::fft2d_columns_execute(&plan->impl, reinterpret_cast<float2*>(data), batch,
+                                    static_cast<cudaStream_t>(stream));
+}
+
 void dpp_fft_plan_destroy(dpp_fft_plan* plan) {
   if (!plan) return;
   dpp::fft_plan_release(&plan->impl);

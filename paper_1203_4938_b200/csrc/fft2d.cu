@@ -179,6 +179,17 @@ int fft2d_plan_init(FftPlan* p) {
   return DPP_OK;
 }
 
+int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s) {
+  if (batch == 0) return DPP_OK;
+  switch (p->n0) {
+#define RUN(L, A, B, C, W) \
+  case L: return launch_columns<A, B, C, W>(data, p->n1, p->n0 * p->n1, batch, p->ctw_a, p->ctw_b, s);
+    DPP_COLUMN_TABLE(RUN)
+#undef RUN
+  }
+  return fail(DPP_EINVAL, "no column kernel for %lld", (long long)p->n0);
+}
+
 int fft2d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s) {
   if (batch == 0) return DPP_OK;
   int rc = fft1d_execute(p->rows, in, out, batch * p->n0, s);

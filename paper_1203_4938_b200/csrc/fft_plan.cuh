@@ -36,6 +36,7 @@ int fft1d_plan_init(FftPlan* p);
 int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_plan_init(FftPlan* p);
 int fft2d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
+int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s);
 void fft_plan_release(FftPlan* p);
 int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
 

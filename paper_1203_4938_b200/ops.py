@@ -129,6 +129,19 @@ def fft2d_forward(x: torch.Tensor, n0: int, n1: int, out: torch.Tensor | None = 
     return out
 
 
+def fft_columns(x: torch.Tensor, n0: int, n1: int, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """In place: n0-point FFT of every column of batched n0 x n1 row-major arrays."""
+    _check_cuda(x, "x", torch.complex64)
+    if x.numel() % (n0 * n1):
+        raise PlanError(f"{x.numel()} samples is not a whole number of {n0}x{n1} arrays")
+    batch = x.numel() // (n0 * n1)
+    if batch:
+        plan = fft_plan(2, n0, n1, batch, x.device)
+        _lib.check(_lib.load().dpp_fft_c2c_columns(plan._h, x.data_ptr(), batch, stream_handle(stream)),
+                   "fft columns")
+    return x
+
+
 def leaf_dft(k: int, x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     """dft{2^k} leaf node over float{2^(k+1)} work-items (bit-exact with the reference)."""
     _check_cuda(x, "x", torch.float32)

@@ -141,6 +141,23 @@ def test_2d_through_fft2_api_batched(cuda):
         assert rel_l2(g, fo.fft2(xi)) <= 1e-5 * 14
 
 
+def test_column_pass_and_single_rank_sharded_driver(cuda):
+    """The column-only pass used on each rank's slab, and the C3 driver at P=1."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    from paper_1203_4938_b200.distributed import fft2d_row_sharded
+    x = complex_signals(77, (2, 1024, 64))
+    t = torch.from_numpy(x).to(cuda)
+    ops.fft_columns(t, 1024, 64)
+    for g, xi in zip(t.cpu().numpy(), x):
+        ref = np.ascontiguousarray(fo.fft_rows(np.ascontiguousarray(xi.T)).T)
+        assert rel_l2(g, ref) <= tol(1024)
+    y = complex_signals(78, (512, 256))
+    got = fft2d_row_sharded(torch.from_numpy(y).to(cuda), 512).cpu().numpy()
+    assert rel_l2(got, fo.fft2(y)) <= 1e-5 * 17
+
+
 @pytest.mark.parametrize("k", [1, 2, 3])
 def test_leaf_nodes_bit_exact_with_reference_engine(cuda, leaf_golden, k):
     import torch
