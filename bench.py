@@ -280,6 +280,50 @@ def run_ours(args) -> None:
                                                                     / pk["hbm_gbs"], 5),
                                 "vq_flop_per_block": 12288}}
 
+    # secondary: C3 single-GPU 2-D FFT 16384^2 (row pass + DSMEM column pass)
+    del x, y
+    n2d = 16384
+    x2 = torch.randn((n2d, n2d), dtype=torch.complex64, device=dev, generator=gen)
+    for _ in range(2):
+        ops.fft2d_forward(x2, n2d, n2d, out=x2)
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for _ in range(3):
+        ops.fft2d_forward(x2, n2d, n2d, out=x2)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    ms2d = max_over_ranks(d0.elapsed_time(d1) / 3, world)
+    flops2d = 5.0 * n2d * n2d * 28
+    fft2d = {"metric": "2-D FFT GFLOP/s (5N^2 log2 N^2)", "config": "16384x16384 complex64, 1 GPU (configs[2] at P=1)",
+             "value": round(world * flops2d / (ms2d / 1e3) / 1e9, 1), "ms": round(ms2d, 3),
+             "roofline": {"bound": "hbm", "two_pass_bytes": 32 * n2d * n2d,
+                          "frac_of_two_pass": round(32 * n2d * n2d / (ms2d / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                          "frac_of_compulsory": round(16 * n2d * n2d / (ms2d / 1e3) / 1e9 / pk["hbm_gbs"], 4)}}
+    del x2
+
+    # secondary: C5 chain on 64 x 4096^2 gray images (device-resident edges)
+    from paper_1203_4938_b200.apps import chain as achain
+    from paper_1203_4938_b200 import CudaBackend
+    nimg, side = 64, 4096
+    imgs = torch.randint(0, 256, (nimg, side, side), dtype=torch.uint8, device=dev, generator=gen)
+    cbs = torch.randn((nimg, 256, 16), dtype=torch.float32, device=dev, generator=gen)
+    be = CudaBackend(outputs="device")
+    achain.run_chain(imgs, cbs, backend=be)
+    torch.cuda.synchronize()
+    e0c, e1c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0c.record(stream)
+    for _ in range(2):
+        achain.run_chain(imgs, cbs, backend=be)
+    e1c.record(stream)
+    torch.cuda.synchronize()
+    ms_chain = max_over_ranks(e0c.elapsed_time(e1c) / 2, world)
+    chain5 = {"metric": "chain images/s", "config": "64 x 4096^2 gray: to_complex -> fft2d -> spectrum_u8 -> "
+                                                     "imgc_encode (256 centroids/image), one graph, device edges",
+              "value": round(world * nimg / (ms_chain / 1e3), 2), "ms_per_step": round(ms_chain, 2),
+              "mpixel_s": round(world * nimg * side * side / (ms_chain / 1e3) / 1e6, 1)}
+    del imgs, cbs
+
     if rank == 0:
         cpu = cpu_baseline(len(os.sched_getaffinity(0)), seconds=10.0) if world == 1 and not args.no_cpu \
             else None
@@ -301,7 +345,7 @@ def run_ours(args) -> None:
                     "api": "apps.fft.fft_batch(pinned host tensor)"},
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
-            "secondary": {"compression": compression},
+            "secondary": {"compression_c4": compression, "fft2d_c3": fft2d, "chain_c5": chain5},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

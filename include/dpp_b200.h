@@ -153,6 +153,12 @@ int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_
 int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const double* uniforms,
                int max_iter, float* centroids_out, double* trace, int* iterations, void* stream);
 
+/* C5 chain adapters (node bodies in apps/chain.py):
+ *   to_complex:  y[i] = ((float)x[i], 0)          n u8 -> n complex64 (n % 4 == 0)
+ *   spectrum_u8: y[i] = (u8)clamp(floor(alpha*log(1+|z[i]|)), 0, 255)   (n even) */
+int dpp_u8_to_complex(const uint8_t* x, float* y, int64_t n, void* stream);
+int dpp_spectrum_u8(const float* z, uint8_t* y, int64_t n, float alpha, void* stream);
+
 /* Inverse (imgc.py:426-439), for round-trip tests on device. */
 int dpp_imgc_decode(const uint8_t* records, const uint8_t* cb_plane, const uint8_t* cr_plane,
                     const float* codebook, int n_cb, int64_t height, int64_t width,

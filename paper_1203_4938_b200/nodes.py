@@ -170,16 +170,38 @@ class EncodeNode(NativeNode):
     def launch(self, items, inputs, outputs, stream):
         batch = items // self.blocks
         cbk = inputs["cbk"]
-        if cbk.numel() != self.ncb * 16:
-            raise KernelRuntimeError(f"codebook stream holds {cbk.numel() // 16} centroids, "
-                                     f"node expects {self.ncb}", work_item=0)
+        shared = cbk.numel() == self.ncb * 16
+        if not shared and cbk.numel() != self.ncb * 16 * batch:
+            raise KernelRuntimeError(f"codebook stream holds {cbk.numel() // 16} centroids, node expects "
+                                     f"{self.ncb} (shared) or {self.ncb} per frame", work_item=0)
         rec = torch.empty(items * 3, dtype=torch.uint8, device=cbk.device)
         ops.encode(inputs["px"], 1, self.height, self.width, cbk, rec, outputs["cb"], outputs["cr"],
-                   batch=batch, stream=stream)
+                   batch=batch, shared_codebook=shared, stream=stream)
         r3 = rec.view(-1, 3)
         outputs["mu"].copy_(r3[:, 0])
         outputs["sig"].copy_(r3[:, 1])
         outputs["idx"].copy_(r3[:, 2])
+
+
+class ToComplexNode(NativeNode):
+    """C5 adapter: gray u8 -> complex64 (g, 0) (apps/chain.py)."""
+
+    def __init__(self):
+        super().__init__("to_complex", {"x": ("uchar", 1, _IN), "y": ("float", 2, _OUT)})
+
+    def launch(self, items, inputs, outputs, stream):
+        ops.u8_to_complex(inputs["x"], outputs["y"], stream)
+
+
+class SpectrumU8Node(NativeNode):
+    """C5 adapter: complex64 -> u8 clip(floor(alpha*log(1+|z|))) (apps/chain.py)."""
+
+    def __init__(self, alpha: float):
+        super().__init__("spectrum_u8", {"x": ("float", 2, _IN), "y": ("uchar", 1, _OUT)})
+        self.alpha = alpha
+
+    def launch(self, items, inputs, outputs, stream):
+        ops.spectrum_u8(inputs["x"], outputs["y"], self.alpha, stream)
 
 
 # ---------------------------------------------------------------------------
@@ -251,6 +273,19 @@ def match_codec(node):
         w, h, n = map(int, m.groups())
         if node.body == imgc.encode_kernel(w, h, n).body:
             return EncodeNode(w, h, n)
+    return None
+
+
+@register
+def match_chain(node):
+    from .apps import chain
+    if node.body == chain.to_complex_kernel().body:
+        return ToComplexNode()
+    m = re.search(r"float v = floor\(([0-9.e+-]+)f \* log\(1\.0f \+ m\)\);", node.body)
+    if m:
+        alpha = float(m.group(1))
+        if node.body == chain.spectrum_u8_kernel(alpha).body:
+            return SpectrumU8Node(alpha)
     return None
 
 

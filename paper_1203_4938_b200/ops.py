@@ -216,6 +216,20 @@ def encode(px: torch.Tensor, channels: int, height: int, width: int, codebook: t
         _lib.ptr(norm32), stream_handle(stream)), "imgc encode")
 
 
+def u8_to_complex(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+    _check_cuda(x, "x", torch.uint8)
+    _check_cuda(y, "y")
+    _lib.check(_lib.load().dpp_u8_to_complex(x.data_ptr(), y.data_ptr(), x.numel(), stream_handle(stream)),
+               "to_complex")
+
+
+def spectrum_u8(z: torch.Tensor, y: torch.Tensor, alpha: float, stream=None) -> None:
+    _check_cuda(z, "z")
+    _check_cuda(y, "y", torch.uint8)
+    _lib.check(_lib.load().dpp_spectrum_u8(z.data_ptr(), y.data_ptr(), y.numel(), float(alpha),
+                                           stream_handle(stream)), "spectrum_u8")
+
+
 def decode(records, cb_plane, cr_plane, codebook, height: int, width: int, rgb, stream=None) -> None:
     _lib.check(_lib.load().dpp_imgc_decode(records.data_ptr(), cb_plane.data_ptr(), cr_plane.data_ptr(),
                                            codebook.data_ptr(), codebook.numel() // 16, height, width,

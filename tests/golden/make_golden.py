@@ -172,6 +172,24 @@ def main() -> None:
     except Exception as exc:  # noqa: BLE001
         docs["ours_encode_faults"] = np.array([True])
         docs["ours_encode_fault_msg"] = np.frombuffer(str(exc).encode(), np.uint8)
+    # C5 chain adapters: reference validation + reference-engine outputs
+    from paper_1203_4938_b200.apps import chain as ochain
+    from paper_1203_4938_b200.model import Instance as OInst, Program as OProg
+    cprog = ochain.chain_program(64, 32, 16)
+    docs["ours_chain_valid"] = np.array([validate(parse_program(our_serialize(cprog))).ok])
+    for name, node in (("to_complex", ochain.to_complex_kernel()), ("spectrum_u8", ochain.spectrum_u8_kernel())):
+        one = parse_program(our_serialize(OProg({node.name: node}, (OInst(0, node.name),), ())))
+        docs[f"ours_{name}_valid"] = np.array([validate(one).ok])
+        if name == "to_complex":
+            xin = rs.integers(0, 256, 1024).astype(np.uint8)
+            res = run(LocalBackend(chunk_size=1024), one, {"0.x": StreamFile(DataType("uchar"), xin)})["0.y"]
+        else:
+            mag = np.exp(rs.uniform(-2, 22, 4096))
+            ph = rs.uniform(0, 2 * np.pi, 4096)
+            xin = (mag * np.exp(1j * ph)).astype(np.complex64).view(np.float32)
+            res = run(LocalBackend(chunk_size=4096), one, {"0.x": StreamFile(DataType("float", 2), xin)})["0.y"]
+        docs[f"ours_{name}_in"] = xin
+        docs[f"ours_{name}_out_refengine"] = res.values
     docs["table2_doc"] = np.frombuffer(json.dumps(
         json.loads(serialize_program(parse_program(json.dumps(_table2()).encode())))).encode(), np.uint8)
     np.savez_compressed(HERE / "docs_golden.npz", **docs)

@@ -63,6 +63,18 @@ def test_fft_node_body_means_the_dft_on_the_reference_engine(docs_golden):
         assert np.abs(y[16 * s:16 * (s + 1)] - ref).max() / np.abs(ref).max() < 1e-5
 
 
+def test_chain_documents_validate_and_adapters_are_pinned(docs_golden):
+    """C5 chain: the reference validates the whole graph and each adapter; the
+    oracle adapters equal the reference engine's outputs bit for bit."""
+    from oracle import chain_oracle as co
+    for name in ("chain", "to_complex", "spectrum_u8"):
+        assert bool(docs_golden[f"ours_{name}_valid"][0]), name
+    x = docs_golden["ours_to_complex_in"]
+    assert np.array_equal(co.to_complex(x).view(np.float32), docs_golden["ours_to_complex_out_refengine"])
+    z = docs_golden["ours_spectrum_u8_in"].view(np.complex64)
+    assert np.array_equal(co.spectrum_u8(z), docs_golden["ours_spectrum_u8_out_refengine"])
+
+
 def test_parse_rejections():
     with pytest.raises(ProgramFormatError, match="missing key"):
         parse_program('{"kernels": {}, "nodes": []}')
