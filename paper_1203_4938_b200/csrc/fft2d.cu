@@ -1,106 +1,139 @@
-// 2-D FFT: row pass (1-D kernels of fft.cu) + one column pass.
+// 2-D FFT: row pass (the 1-D kernels of fft.cu) + one column pass.
 //
 // The reference has no 2-D transform; its 2-D result is defined (SURVEY §8d,
 // C3) as the composition fft(rows) then fft(columns) of apps/fft.py:150-174.
 //
-// Column pass kernel (fft_columns_kernel<L1, L2, C, W>): a thread-block
-// cluster of C CTAs owns a tile of W adjacent columns over all L = L1*L2
-// rows.  Rows r = L2*a + b: pass A runs L1-point FFTs over a for the CTA's
-// slice of b (every load is a W-wide contiguous row segment), multiplies by
-// W_L^{b c}, scatters through DSMEM, pass B runs L2-point FFTs over b and
-// stores rows c + L1*d.  One HBM read and one HBM write per element, in place.
-#include <cooperative_groups.h>
+// Column pass (fft_columns_tma<L1, L2, C, W>): a cluster of C CTAs owns a tile
+// of W adjacent columns over all L = L1*L2 rows, rows r = L2*a + b.
+//   - CTA p loads rows {L2*a + b : b in its slice of B1 = L2/C} with ONE 3-D
+//     TMA box (W x B1 x L1) into [a][b][col] order;
+//   - pass A: L1-point FFTs over a for its B1*W (b, col) sequences,
+//     exchanges in conflict-free [element][sequence] rows;
+//   - W_L^{b c} by per-thread recurrence, st.async scatter of every element
+//     to the owner of c (B2 = L1/C values of c per CTA), each store signalling
+//     the owner's receive mbarrier; XOR-swizzled receive rows;
+//   - pass B: L2-point FFTs over b, results staged in [d][c][col] order and
+//     written with ONE 3-D TMA store (rows c + L1*d).
+// One HBM read + one HBM write per element, in place.
 #include <cmath>
 #include <vector>
 
 #include "common.cuh"
 #include "fft_plan.cuh"
 #include "fft_block.cuh"
-
-namespace cg = cooperative_groups;
+#include "tma.cuh"
 
 namespace dpp {
 
 template <int L1, int L2, int C, int W>
 struct ColCfg {
   static constexpr int R = L1 < 16 ? L1 : 16;
-  static_assert(L2 % R == 0, "L2 must be a multiple of the radix");
+  static_assert(L1 % R == 0 && L2 % R == 0, "radix must divide both factors");
   static constexpr int L = L1 * L2;
-  static constexpr int B1 = L2 / C, B2 = L1 / C;  // b-slice in pass A, c-slice in pass B
+  static constexpr int B1 = L2 / C, B2 = L1 / C;  // b per CTA (pass A), c per CTA (pass B)
+  static constexpr int F1 = B1 * W, F2 = B2 * W;  // sequences per CTA
   static constexpr int T1 = L1 / R, T2 = L2 / R;
-  static constexpr int THREADS = B1 * W * T1;
-  static_assert(THREADS == B2 * W * T2, "pass thread counts must agree");
+  static constexpr int THREADS = F1 * T1;
+  static_assert(THREADS == F2 * T2, "pass thread counts must agree");
+  static constexpr int G = 32 / W > 1 ? 32 / W : 1;  // receive swizzle period
   static constexpr int NC = L1 > L2 ? L1 : L2;
   static constexpr int S = L / NC;
   static constexpr int LOGS = ilog2(S);
-  static constexpr int BUF1 = B1 * W * (L1 + 1), BUF2 = B2 * W * (L2 + 1);
-  static constexpr int BUF = BUF1 > BUF2 ? BUF1 : BUF2;
-  static constexpr size_t SMEM = (size_t)(NC + S + BUF) * sizeof(float2);
+  static constexpr int TILE = L1 * F1;
+  static_assert(TILE == L2 * F2, "tile sizes must agree");
+  static constexpr size_t SMEM = (size_t)(NC + TILE) * sizeof(float2);
+};
+
+struct MapRow2 {
+  int w, col;
+  __device__ __forceinline__ int operator()(int e) const { return e * w + col; }
 };
 
 template <int L1, int L2, int C, int W>
-__global__ void __launch_bounds__(ColCfg<L1, L2, C, W>::THREADS)
-fft_columns_kernel(float2* __restrict__ data, int64_t ncols, int64_t image_elems,
-                   const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
+__global__ void __launch_bounds__(ColCfg<L1, L2, C, W>::THREADS, 1024 / ColCfg<L1, L2, C, W>::THREADS)
+fft_columns_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                int64_t tiles_per_image, const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
   using Cfg = ColCfg<L1, L2, C, W>;
-  constexpr int R = Cfg::R, B1 = Cfg::B1, B2 = Cfg::B2, T1 = Cfg::T1, T2 = Cfg::T2;
-  extern __shared__ float2 smem[];
+  constexpr int R = Cfg::R, B1 = Cfg::B1, B2 = Cfg::B2, F1 = Cfg::F1, F2 = Cfg::F2, T1 = Cfg::T1, T2 = Cfg::T2;
+  extern __shared__ __align__(128) float2 smem[];
+  __shared__ uint64_t bars[2];
   float2* coarse = smem;
-  float2* fine = smem + Cfg::NC;
-  float2* buf = fine + Cfg::S;
+  float2* buf = smem + Cfg::NC;
 
-  cg::cluster_group cluster = cg::this_cluster();
-  const int p = (int)cluster.block_rank();
-  const int64_t tile = blockIdx.x / C;               // over images x column tiles
-  const int64_t tiles_per_image = ncols / W;
+  const int p = (int)cluster_ctarank();
+  const int64_t tile = blockIdx.x / C;
   const int64_t img = tile / tiles_per_image;
-  const int64_t c0 = (tile - img * tiles_per_image) * W;
-  float2* base = data + img * image_elems + c0;
+  const int c0 = (int)((tile - img * tiles_per_image) * W);
   const int tid = threadIdx.x;
-
-  // pass A: thread = ((j * B1) + bl) * W + col
-  const int col = tid % W;
-  const int bl = (tid / W) % B1;
-  const int j = tid / (W * B1);
-  const int b = p * B1 + bl;
-  float2 v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = __ldcs(base + (int64_t)(L2 * (j + T1 * i) + b) * ncols + col);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bars[0], (uint32_t)(Cfg::TILE * sizeof(float2)));
+    mbar_arrive_expect_tx(&bars[1], (uint32_t)(Cfg::TILE * sizeof(float2)));
+    tma_load_3d(buf, &tin, c0, p * B1, (int)(img * L1), &bars[0]);
+  }
   for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
-  for (int e = tid; e < Cfg::S; e += Cfg::THREADS) fine[e] = fine_g[e];
   __syncthreads();
-  block_fft<L1, R>(v, j, buf + (bl * W + col) * (L1 + 1), MapIdentity{}, coarse, Cfg::NC / L1);
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int e = b * (j + T1 * i);
-    v[i] = cmul(v[i], cmul(coarse[e >> Cfg::LOGS], fine[e & (Cfg::S - 1)]));
-  }
-  cluster.sync();
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int c = j + T1 * i;
-    const int q = c / B2, cl = c - q * B2;
-    float2* dst = cluster.map_shared_rank(buf, q);
-    dst[(cl * W + col) * (L2 + 1) + b] = v[i];
-  }
-  cluster.sync();
 
-  // pass B: thread = ((j2 * B2) + cl) * W + col
-  const int cl = (tid / W) % B2;
-  const int j2 = tid / (W * B2);
-  float2* seq = buf + (cl * W + col) * (L2 + 1);
+  // pass A: sequence f = (bl, col), FFT over a
+  const int f = tid % F1, j = tid / F1;
+  const int bl = f / W, col = f - bl * W;
+  float2 v[R];
+  mbar_wait(&bars[0], 0);
 #pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = seq[j2 + T2 * i];
+  for (int i = 0; i < R; ++i) v[i] = buf[(j + T1 * i) * F1 + f];
   __syncthreads();
-  block_fft<L2, R>(v, j2, seq, MapIdentity{}, coarse, Cfg::NC / L2);
-  const int c = p * B2 + cl;
+  block_fft<L1, R>(v, j, buf, MapRow2{F1, f}, coarse, Cfg::NC / L1);
+  cluster_arrive_relaxed();  // this CTA no longer reads buf
+  const int b = p * B1 + bl;
+  {
+    auto tw = [&](int e) { return cmul(__ldg(coarse_g + (e >> Cfg::LOGS)), __ldg(fine_g + (e & (Cfg::S - 1)))); };
+    float2 w = tw(b * j);
+    const float2 sw = tw(b * T1);
 #pragma unroll
-  for (int i = 0; i < R; ++i) __stcs(base + (int64_t)(c + L1 * (j2 + T2 * i)) * ncols + col, v[i]);
+    for (int i = 0; i < R; ++i) {
+      v[i] = cmul(v[i], w);
+      w = cmul(w, sw);
+    }
+  }
+  cluster_wait();
+  {
+    const uint32_t base = smem_u32(buf);
+    const uint32_t rbar = smem_u32(&bars[1]);
+    const int swz = (b % Cfg::G) * W;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = j + T1 * i;
+      const int q = c / B2, cl = c - q * B2;
+      const uint32_t off = (uint32_t)((b * F2 + ((cl * W + col) ^ swz)) * sizeof(float2));
+      st_async_f2(mapa_u32(base + off, q), v[i], mapa_u32(rbar, q));
+    }
+  }
+  mbar_wait(&bars[1], 0);
+
+  // pass B: sequence f2 = (cl, col), FFT over b
+  const int f2 = tid % F2, j2 = tid / F2;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int bb = j2 + T2 * i;
+    v[i] = buf[bb * F2 + (f2 ^ ((bb % Cfg::G) * W))];
+  }
+  __syncthreads();
+  block_fft<L2, R>(v, j2, buf, MapRow2{F2, f2}, coarse, Cfg::NC / L2);  // ends with a CTA barrier
+#pragma unroll
+  for (int i = 0; i < R; ++i) buf[(j2 + T2 * i) * F2 + f2] = v[i];  // [d][cl][col] = TMA box order
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_3d(&tout, c0, p * B2, (int)(img * L2), buf);
+    bulk_commit_and_wait_all();
+  }
 }
 
 template <int L1, int L2, int C, int W>
 static int prepare_columns() {
-  auto kern = fft_columns_kernel<L1, L2, C, W>;
+  auto kern = fft_columns_tma<L1, L2, C, W>;
   DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)ColCfg<L1, L2, C, W>::SMEM));
   if (C > 8) DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -108,11 +141,25 @@ static int prepare_columns() {
 }
 
 template <int L1, int L2, int C, int W>
-static int launch_columns(float2* data, int64_t ncols, int64_t image_elems, int64_t batch,
-                          const float2* coarse, const float2* fine, cudaStream_t s) {
+static int launch_columns(float2* data, int64_t ncols, int64_t batch, const float2* coarse, const float2* fine,
+                          cudaStream_t s) {
   using Cfg = ColCfg<L1, L2, C, W>;
+  CUtensorMap tin, tout;
+  {
+    const uint64_t dims[3] = {(uint64_t)ncols, (uint64_t)L2, (uint64_t)(batch * L1)};
+    const uint64_t strides[2] = {(uint64_t)ncols * 8, (uint64_t)ncols * 8 * L2};
+    const uint32_t box[3] = {(uint32_t)W, (uint32_t)Cfg::B1, (uint32_t)L1};
+    if (int rc = make_tmap_c64_3d(&tin, data, dims, strides, box)) return rc;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)ncols, (uint64_t)L1, (uint64_t)(batch * L2)};
+    const uint64_t strides[2] = {(uint64_t)ncols * 8, (uint64_t)ncols * 8 * L1};
+    const uint32_t box[3] = {(uint32_t)W, (uint32_t)Cfg::B2, (uint32_t)L2};
+    if (int rc = make_tmap_c64_3d(&tout, data, dims, strides, box)) return rc;
+  }
+  const int64_t tiles = ncols / W;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(batch * (ncols / W) * C), 1, 1);
+  cfg.gridDim = dim3((unsigned)(batch * tiles * C), 1, 1);
   cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = s;
@@ -123,19 +170,18 @@ static int launch_columns(float2* data, int64_t ncols, int64_t image_elems, int6
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_columns_kernel<L1, L2, C, W>, data, ncols, image_elems,
-                                    coarse, fine));
+  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_columns_tma<L1, L2, C, W>, tin, tout, tiles, coarse, fine));
   return DPP_OK;
 }
 
-// Column schedules: (L1, L2, C, W) with L*W/C = 8192 points per CTA.
+// Column schedules (L, L1, L2, C, W): 4096-8192 points per CTA, 256-512 threads.
 #define DPP_COLUMN_TABLE(X)   \
-  X(256, 16, 16, 1, 32)       \
-  X(512, 16, 32, 1, 16)       \
-  X(1024, 32, 32, 2, 16)      \
-  X(2048, 32, 64, 4, 16)      \
-  X(4096, 64, 64, 8, 16)      \
-  X(8192, 64, 128, 8, 8)      \
+  X(256, 16, 16, 1, 16)       \
+  X(512, 16, 32, 2, 16)       \
+  X(1024, 32, 32, 4, 16)      \
+  X(2048, 32, 64, 8, 16)      \
+  X(4096, 64, 64, 16, 16)     \
+  X(8192, 64, 128, 16, 8)     \
   X(16384, 128, 128, 16, 8)
 
 std::vector<float2> twiddle_table(int64_t n, int64_t count);
@@ -158,8 +204,7 @@ int fft2d_plan_init(FftPlan* p) {
     return fail(DPP_ENOTSUP, "2-D column length %lld not supported (256..16384)", (long long)n0);
   if (rc) return rc;
   if (n1 % width)
-    return fail(DPP_ENOTSUP, "2-D row length %lld must be a multiple of the %d-column tile",
-                (long long)n1, width);
+    return fail(DPP_ENOTSUP, "2-D row length %lld must be a multiple of the %d-column tile", (long long)n1, width);
   p->col_width = width;
   p->col_split = l1;
   p->col_cluster = cl;
@@ -174,8 +219,10 @@ int fft2d_plan_init(FftPlan* p) {
   p->rows->device = p->device;
   rc = fft1d_plan_init(p->rows);
   if (rc) return rc;
-  snprintf(p->desc, sizeof(p->desc), "rows: %s | columns: cluster<%lldx%lld, C=%d, W=%d>",
-           p->rows->desc, (long long)l1, (long long)l2, cl, width);
+  char rows[200];
+  snprintf(rows, sizeof(rows), "%s", p->rows->desc);
+  snprintf(p->desc, sizeof(p->desc), "rows: %s | columns: TMA cluster<%lldx%lld, C=%d, W=%d>", rows,
+           (long long)l1, (long long)l2, cl, width);
   return DPP_OK;
 }
 
@@ -183,7 +230,7 @@ int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   if (batch == 0) return DPP_OK;
   switch (p->n0) {
 #define RUN(L, A, B, C, W) \
-  case L: return launch_columns<A, B, C, W>(data, p->n1, p->n0 * p->n1, batch, p->ctw_a, p->ctw_b, s);
+  case L: return launch_columns<A, B, C, W>(data, p->n1, batch, p->ctw_a, p->ctw_b, s);
     DPP_COLUMN_TABLE(RUN)
 #undef RUN
   }
@@ -194,13 +241,7 @@ int fft2d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
   if (batch == 0) return DPP_OK;
   int rc = fft1d_execute(p->rows, in, out, batch * p->n0, s);
   if (rc) return rc;
-  switch (p->n0) {
-#define RUN(L, A, B, C, W) \
-  case L: return launch_columns<A, B, C, W>(out, p->n1, p->n0 * p->n1, batch, p->ctw_a, p->ctw_b, s);
-    DPP_COLUMN_TABLE(RUN)
-#undef RUN
-  }
-  return fail(DPP_EINVAL, "no column kernel for %lld", (long long)p->n0);
+  return fft2d_columns_execute(p, out, batch, s);
 }
 
 }  // namespace dpp
