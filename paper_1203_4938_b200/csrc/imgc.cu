@@ -76,6 +76,48 @@ __device__ __forceinline__ float vq_dist(const float (&b)[16], const float4* c) 
   return pw16f(p);
 }
 
+// The same distance with sm_100 packed binary32 pairs (FADD2/FMUL2, each lane
+// IEEE round-to-nearest, no contraction): bit-identical, 25 instead of 47 FP
+// instructions.  Components are paired so that every pairwise step of the
+// reduction is a lane-wise add: pair k of a vector is
+//   k=0..3: (v0,v2) (v1,v3) (v4,v6) (v5,v7);  k=4..7: the same +8.
+// Then R = P[k] + P[k+4] gives (r0,r2) (r1,r3) (r4,r6) (r5,r7),
+// R0+R1 = (r0+r1, r2+r3), R2+R3 = (r4+r5, r6+r7), and two scalar adds finish
+// ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)).
+__device__ __forceinline__ int vq_pair_src(int k, int half) {  // component of pair k, lane half
+  const int base = (k & 4) ? 8 : 0, kk = k & 3;
+  return base + (kk >> 1) * 4 + (kk & 1) + half * 2;
+}
+__device__ __forceinline__ void vq_pack(const float (&v)[16], float2 (&pv)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) pv[k] = make_float2(v[vq_pair_src(k, 0)], v[vq_pair_src(k, 1)]);
+}
+__device__ __forceinline__ float vq_dist_pairs(const float2 (&b)[8], const float2* c) {
+  float2 p[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float2 cv = c[k];
+    const float2 d = __fadd2_rn(b[k], make_float2(-cv.x, -cv.y));
+    p[k] = __fmul2_rn(d, d);
+  }
+  // NOTE: ptxas fuses an FMUL2 feeding an FADD2 into FFMA2 even for explicit
+  // add.rn/mul.rn.f32x2 and -fmad=false (checked in SASS), which would break
+  // bit-exactness; the reduction therefore stays scalar (FADD is never fused
+  // with a packed multiply).  31 FP instructions per centroid instead of 47.
+  const float r0 = __fadd_rn(p[0].x, p[4].x), r2 = __fadd_rn(p[0].y, p[4].y);
+  const float r1 = __fadd_rn(p[1].x, p[5].x), r3 = __fadd_rn(p[1].y, p[5].y);
+  const float r4 = __fadd_rn(p[2].x, p[6].x), r6 = __fadd_rn(p[2].y, p[6].y);
+  const float r5 = __fadd_rn(p[3].x, p[7].x), r7 = __fadd_rn(p[3].y, p[7].y);
+  return __fadd_rn(__fadd_rn(__fadd_rn(r0, r1), __fadd_rn(r2, r3)), __fadd_rn(__fadd_rn(r4, r5), __fadd_rn(r6, r7)));
+}
+// codebook -> shared memory in pair order (8 float2 per centroid)
+__device__ __forceinline__ void vq_stage_codebook(const float* cbk, int ncb, float2* s) {
+  for (int e = threadIdx.x; e < ncb * 8; e += blockDim.x) {
+    const int j = e >> 3, k = e & 7;
+    s[e] = make_float2(cbk[j * 16 + vq_pair_src(k, 0)], cbk[j * 16 + vq_pair_src(k, 1)]);
+  }
+}
+
 // "float best = 3.402823e38f" (imgc.py:173) parses to 0x7f7ffffd, not FLT_MAX
 #define VQ_BEST_INIT __int_as_float(0x7f7ffffd)
 
@@ -135,8 +177,8 @@ __global__ void gradient_kernel(const float* __restrict__ lum, float* __restrict
 // codebook (tiled per chunk by the reference host, imgc.py:419).
 __global__ void vqnearest_kernel(const float* __restrict__ blk, const float* __restrict__ cbk,
                                  int32_t* __restrict__ idx, int64_t n, int ncb) {
-  extern __shared__ float4 scb[];
-  for (int e = threadIdx.x; e < ncb * 4; e += blockDim.x) scb[e] = reinterpret_cast<const float4*>(cbk)[e];
+  extern __shared__ float2 scp[];
+  vq_stage_codebook(cbk, ncb, scp);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -146,10 +188,12 @@ __global__ void vqnearest_kernel(const float* __restrict__ blk, const float* __r
     const float4 v = reinterpret_cast<const float4*>(blk)[4 * i + q];
     b[4 * q] = v.x; b[4 * q + 1] = v.y; b[4 * q + 2] = v.z; b[4 * q + 3] = v.w;
   }
+  float2 bp[8];
+  vq_pack(b, bp);
   float best = VQ_BEST_INIT;
   int bj = 0;
   for (int j = 0; j < ncb; ++j) {
-    const float d = vq_dist(b, scb + 4 * j);
+    const float d = vq_dist_pairs(bp, scp + 8 * j);
     if (d < best) { best = d; bj = j; }
   }
   idx[i] = bj;
@@ -189,12 +233,11 @@ __device__ __forceinline__ void load_rgb(const uint8_t* row, int64_t x, float& r
 // normalised blocks (imgc.py:378-388), no chroma, VQ or records.
 template <int CH, bool STATS = false>
 __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
-  __shared__ float4 scb[256 * 4];
+  __shared__ float2 scp[256 * 8];
   __shared__ uint8_t srec[256 * 3];
   const int64_t img = blockIdx.y;
   if constexpr (!STATS) {
-    const float4* cbk = reinterpret_cast<const float4*>(a.codebook + img * a.codebook_stride);
-    for (int e = threadIdx.x; e < a.ncb * 4; e += blockDim.x) scb[e] = cbk[e];
+    vq_stage_codebook(a.codebook + img * a.codebook_stride, a.ncb, scp);
     __syncthreads();
   }
 
@@ -261,7 +304,8 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
           mag[4 * r + c] = __double2float_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(dxd, dxd), __dmul_rn(dyd, dyd))));
         }
       }
-      a.block_grad[img * nblocks + k] = __fdiv_rn(pw16f(mag), 16.0f);
+      // x / 16 and x * 0.0625 are the same real number: identical roundings
+      a.block_grad[img * nblocks + k] = __fmul_rn(pw16f(mag), 0.0625f);
     }
 
     // block statistics in binary64 (imgc.py:384-388)
@@ -293,10 +337,12 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
     }
 
     // exact nearest centroid (vq_program semantics: strict <, first index wins)
+    float2 bp[8];
+    vq_pack(nb, bp);
     float best = VQ_BEST_INIT;
     int bj = 0;
     for (int j = 0; j < a.ncb; ++j) {
-      const float d = vq_dist(nb, scb + 4 * j);
+      const float d = vq_dist_pairs(bp, scp + 8 * j);
       if (d < best) { best = d; bj = j; }
     }
     const int t = threadIdx.x;

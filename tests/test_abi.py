@@ -36,6 +36,46 @@ def test_error_path_without_a_gpu():
     assert lib.dpp_fft_leaf(5, None, None, 0, None) == _lib.DPP_EINVAL
 
 
+def _sass_by_function() -> dict[str, list[str]]:
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    funcs: dict[str, list[str]] = {}
+    cur = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur and re.match(r"\s+/\*[0-9a-f]{4}\*/", line):
+            funcs[cur].append(line)
+    return funcs
+
+
+def test_bit_exact_kernels_contain_no_fused_binary32_multiply_add():
+    """The codec and leaf kernels must keep every binary32 product and sum
+    separately rounded (the reference evaluates them with numpy, no FMA).
+    FFMA2 fusion would silently break the byte-exact bitstream (ptxas fuses
+    FMUL2 -> FADD2 even for explicit .rn PTX), so the SASS is checked here.
+    The only FFMA allowed is the `FFMA R, RZ, x, y` range probe inside the
+    correctly-rounded binary64 division routine."""
+    import shutil
+    if not shutil.which("cuobjdump"):
+        import pytest
+        pytest.skip("cuobjdump not available")
+    exact = ("encode_kernel", "vqnearest_kernel", "ycbcr_kernel", "boxdown_kernel", "gradient_kernel",
+             "leaf_dft_kernel", "decode_kernel", "kpp_update")
+    checked = 0
+    for name, lines in _sass_by_function().items():
+        if not any(k in name for k in exact if k != "kpp_update"):
+            continue
+        checked += 1
+        for ln in lines:
+            assert "FFMA2" not in ln, (name, ln)
+            if re.search(r"\bFFMA\b", ln):
+                assert re.search(r"FFMA R\d+, RZ,", ln), (name, ln)
+    assert checked >= 10
+
+
 def test_library_is_sm100a():
     blob = _lib.LIB_PATH.read_bytes()
     assert b"sm_100a" in blob
