@@ -137,6 +137,18 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
                     uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
                     float* block_grad, float* norm32, void* stream);
 
+/* The encoder's nearest-centroid search runs on the tensor cores (tcgen05
+ * kind::tf32, 3xTF32 split) with an exact binary32 re-check of every
+ * centroid inside the error band, so the output is identical to the
+ * brute-force search (environment DPP_IMGC_VQ=exact selects the latter).
+ * Test hook: the tensor-core encoder for one gray/RGB/RGBA image with the
+ * pruning band scaled by delta_scale; *ambiguous (device counter) is
+ * incremented by the number of blocks that needed the exact re-check. */
+int dpp_imgc_encode_tc_debug(const uint8_t* px, int channels, int64_t height, int64_t width,
+                             const float* codebook, int n_cb, uint8_t* records, uint8_t* cb_plane,
+                             uint8_t* cr_plane, float delta_scale, unsigned long long* ambiguous,
+                             void* stream);
+
 /* Training pass of the codec (imgc.py:378-388): per block the mean gradient
  * magnitude (block_grad, the k-means training filter) and the binary64
  * normalised block (norm64, blocks x 16) — the k-means input. */

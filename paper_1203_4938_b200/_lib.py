@@ -38,6 +38,7 @@ SIGNATURES = {
     "dpp_imgc_encode": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _int, _i64,
                                C.c_double, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dpp_imgc_decode": (_int, [_vp, _vp, _vp, _vp, _int, _i64, _i64, _vp, _vp]),
+    "dpp_imgc_encode_tc_debug": (_int, [_vp, _int, _i64, _i64, _vp, _int, _vp, _vp, _vp, C.c_float, _vp, _vp]),
     "dpp_u8_to_complex": (_int, [_vp, _vp, _i64, _vp]),
     "dpp_spectrum_u8": (_int, [_vp, _vp, _i64, C.c_float, _vp]),
     "dpp_imgc_block_stats": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, C.c_double, _vp, _vp, _vp]),

@@ -231,21 +231,15 @@ __device__ __forceinline__ void load_rgb(const uint8_t* row, int64_t x, float& r
 
 // STATS = true: the k-means training pass — only block_grad and the binary64
 // normalised blocks (imgc.py:378-388), no chroma, VQ or records.
-template <int CH, bool STATS = false>
-__global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
-  __shared__ float2 scp[256 * 8];
-  __shared__ uint8_t srec[256 * 3];
-  const int64_t img = blockIdx.y;
-  if constexpr (!STATS) {
-    vq_stage_codebook(a.codebook + img * a.codebook_stride, a.ncb, scp);
-    __syncthreads();
-  }
-
+// Forward block transform of block k of image img (imgc.py:358-401 steps 1-4
+// for one block): pixels -> Y/Cb/Cr (binary32), chroma planes, optional
+// gradient filter, binary64 mean/std, normalised block.  Returns false in
+// STATS mode (outputs written, nothing left to quantise).
+template <int CH, bool STATS>
+__device__ __forceinline__ bool block_front(const EncodeArgs& a, int64_t img, int64_t k, float (&nb)[16],
+                                            double& mean, double& sd) {
   const int64_t bw = a.width / 4, bh = a.height / 4, nblocks = bw * bh;
-  const int64_t k0 = (int64_t)blockIdx.x * blockDim.x;
-  const int64_t k = k0 + threadIdx.x;
-  const bool active = k < nblocks;
-  if (active) {
+  {
     const int64_t by = k / bw, bx = k - by * bw;
     const uint8_t* base = a.px + img * a.image_stride;
     float yv[16];
@@ -312,22 +306,21 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
     double bd[16], sq[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) bd[i] = (double)yv[i];
-    const double mean = __ddiv_rn(pw16d(bd), 16.0);
+    mean = __ddiv_rn(pw16d(bd), 16.0);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       bd[i] = __dsub_rn(bd[i], mean);
       sq[i] = __dmul_rn(bd[i], bd[i]);
     }
-    const double sd = __dsqrt_rn(__ddiv_rn(pw16d(sq), 16.0));
+    sd = __dsqrt_rn(__ddiv_rn(pw16d(sq), 16.0));
     const double safe = fmax(sd, a.sigma_min);  // np.maximum(sigmas, sigma_min)
     if constexpr (STATS) {
       // training rows for the k-means trainer: normalised blocks in binary64
       double* dst = a.norm64 + (img * nblocks + k) * 16;
 #pragma unroll
       for (int i = 0; i < 16; ++i) dst[i] = __ddiv_rn(bd[i], safe);
-      return;
+      return false;
     }
-    float nb[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) nb[i] = __double2float_rn(__ddiv_rn(bd[i], safe));
     if (a.norm32) {
@@ -335,7 +328,25 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) dst[q] = make_float4(nb[4 * q], nb[4 * q + 1], nb[4 * q + 2], nb[4 * q + 3]);
     }
+  }
+  return true;
+}
 
+template <int CH, bool STATS = false>
+__global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
+  __shared__ float2 scp[256 * 8];
+  __shared__ uint8_t srec[256 * 3];
+  const int64_t img = blockIdx.y;
+  if constexpr (!STATS) {
+    vq_stage_codebook(a.codebook + img * a.codebook_stride, a.ncb, scp);
+    __syncthreads();
+  }
+  const int64_t nblocks = (a.width / 4) * (a.height / 4);
+  const int64_t k0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t k = k0 + threadIdx.x;
+  float nb[16];
+  double mean, sd;
+  if (k < nblocks && block_front<CH, STATS>(a, img, k, nb, mean, sd)) {
     // exact nearest centroid (vq_program semantics: strict <, first index wins)
     float2 bp[8];
     vq_pack(nb, bp);
@@ -357,6 +368,275 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
     uint8_t* rec = a.records + (img * nblocks + k0) * 3;
     for (int e = threadIdx.x; e < nrec; e += blockDim.x) rec[e] = srec[e];
   }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core pruned EXACT vector quantisation (tcgen05, kind::tf32).
+//
+// The exact search costs 31 binary32 ops per (block, centroid).  Here a
+// 128-block tile is multiplied against the whole 256-entry codebook on the
+// 5th-gen tensor cores (3xTF32 split: n_hi.c_hi + n_hi.c_lo + n_lo.c_hi,
+// fp32 accumulation in TMEM), giving approximate scores
+//   s_j = |c_j|^2 - 2 n.c_j  =  D_j - |n|^2  (+- DELTA)
+// One epilogue pass (tcgen05.ld, 6 ops per score) finds the best and second
+// best.  When the runner-up is more than 2*DELTA away, the approximate
+// argmin IS the reference's index; otherwise the block is re-checked with
+// the reference's exact binary32 distance over every centroid whose score is
+// within 2*DELTA of the best, in index order with strict <, so ties resolve
+// to the first index exactly like vq_program (imgc.py:175-178).
+// DELTA bounds |s_j - (D^fp32_j - |n|^2)|: 3xTF32 truncation (3*2^-20 per
+// product), fp32 accumulation of 48 products, the fp32 norm, and the
+// reference's own rounding of D (<= 7u*D); see DESIGN.md.  It is scaled by
+// the codebook's largest norm and checked empirically in tests.
+namespace tc {
+constexpr int M = 128;      // blocks per tile (TMEM lanes)
+constexpr int NCB = 256;    // centroids (padded; TMEM columns)
+constexpr int THREADS = 128;
+// K-major canonical layout, no swizzle: 8-row groups of 8 K-quarters (4 tf32)
+__device__ __forceinline__ uint32_t off(int row, int k) {
+  return (uint32_t)((row >> 3) * 1024 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;    // leading byte offset: next K-quarter
+  d |= (uint64_t)(1024u >> 4) << 32;   // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+  return d;                            // base offset 0, layout SWIZZLE_NONE
+}
+// kind::tf32, fp32 accumulate, A/B K-major, N = 256, M = 128
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCB >> 3) << 17) |
+                           ((uint32_t)(M >> 4) << 24);
+constexpr size_t A_BYTES = M * 32 * 4, B_BYTES = NCB * 32 * 4;
+constexpr size_t SMEM = A_BYTES + B_BYTES + NCB * 8 * sizeof(float2) + NCB * sizeof(float) + 16 * 1024;  // +pad: 2 CTAs/SM
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+}  // namespace tc
+
+template <int CH>
+__global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs a, float delta_scale,
+                                                               unsigned long long* ambiguous) {
+  extern __shared__ __align__(1024) uint8_t tsm[];
+  uint8_t* sA = tsm;
+  uint8_t* sB = tsm + tc::A_BYTES;
+  float2* scp = reinterpret_cast<float2*>(sB + tc::B_BYTES);  // exact codebook, pair order
+  float* scn = reinterpret_cast<float*>(scp + tc::NCB * 8);   // |c_j|^2
+  __shared__ uint8_t srec[tc::M * 3];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ unsigned int cmax_bits;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t img = blockIdx.y;
+  const float* cbk = a.codebook + img * a.codebook_stride;
+
+  // stage the codebook: tf32 hi/lo split (B operand), exact pair-order copy, norms
+  for (int e = tid; e < tc::NCB * 16; e += tc::THREADS) {
+    const int j = e >> 4, k = e & 15;
+    const float c = j < a.ncb ? cbk[j * 16 + k] : 0.f;
+    const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
+    *reinterpret_cast<float*>(sB + tc::off(j, k)) = hi;
+    *reinterpret_cast<float*>(sB + tc::off(j, 16 + k)) = __fsub_rn(c, hi);  // exact remainder
+  }
+  vq_stage_codebook(cbk, a.ncb, scp);
+  if (tid == 0) cmax_bits = 0;
+  __syncthreads();
+  for (int j = tid; j < tc::NCB; j += tc::THREADS) {
+    float s = 0.f;
+    if (j < a.ncb)
+      for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
+    scn[j] = j < a.ncb ? s : 1e30f;
+    if (j < a.ncb) atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  // band half-width: 1.5e-3 at |c| <= 4 (the normalised-block scale), growing
+  // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
+  const float cmax = sqrtf(__uint_as_float(cmax_bits));
+  const float delta2 = 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
+
+  const int64_t nblocks = (a.width / 4) * (a.height / 4);
+  const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
+  uint32_t phase = 0;
+  unsigned long long namb = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
+    const int64_t k = t * tc::M + tid;
+    const bool active = k < nblocks;
+    float nb[16];
+    double mean = 0.0, sd = 0.0;
+    if (active) {
+      block_front<CH, false>(a, img, k, nb, mean, sd);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) nb[i] = 0.f;
+    }
+    // A row: n_hi (K 0..15) and the exact remainder n_lo (K 16..31)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 hi, lo;
+      float* h = &hi.x;
+      float* l = &lo.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        h[e] = __uint_as_float(__float_as_uint(nb[4 * q + e]) & 0xFFFFE000u);
+        l[e] = __fsub_rn(nb[4 * q + e], h[e]);
+      }
+      *reinterpret_cast<float4*>(sA + tc::off(tid, 4 * q)) = hi;
+      *reinterpret_cast<float4*>(sA + tc::off(tid, 16 + 4 * q)) = lo;
+    }
+    fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
+      const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
+#pragma unroll
+      for (int m = 0; m < 6; ++m)
+        tc::mma_tf32(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
+      tc::commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    tc::fence_after();
+
+    // pass 1: best and runner-up approximate score
+    float m1 = 3.0e38f, m2 = 3.0e38f;
+    int i1 = 0;
+#pragma unroll 1
+    for (int ch = 0; ch < tc::NCB / 32; ++ch) {
+      uint32_t r[32];
+      tc::ld32(taddr + ch * 32, r);
+      const float4* cn4 = reinterpret_cast<const float4*>(scn + ch * 32);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 cn = cn4[c4];
+        const float cv[4] = {cn.x, cn.y, cn.z, cn.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float s = fmaf(-2.f, __uint_as_float(r[4 * c4 + e]), cv[e]);
+          const bool p = s < m1;
+          m2 = p ? m1 : fminf(m2, s);
+          i1 = p ? ch * 32 + 4 * c4 + e : i1;
+          m1 = p ? s : m1;
+        }
+      }
+    }
+    const bool amb = active && !(m2 - m1 > delta2);
+    int bj = i1;
+    if (__any_sync(0xffffffffu, amb)) {
+      // pass 2 (rare): exact reference distance for every candidate in the band
+      float2 bp[8];
+      vq_pack(nb, bp);
+      float best = VQ_BEST_INIT;
+      int bx = 0;
+      const float lim = m1 + delta2;
+#pragma unroll 1
+      for (int ch = 0; ch < tc::NCB / 32; ++ch) {
+        uint32_t r[32];
+        tc::ld32(taddr + ch * 32, r);
+        if (amb) {
+#pragma unroll 1
+          for (int c = 0; c < 32; ++c) {
+            const int j = ch * 32 + c;
+            const float s = fmaf(-2.f, __uint_as_float(r[c]), scn[j]);
+            if (s <= lim && j < a.ncb) {
+              const float d = vq_dist_pairs(bp, scp + 8 * j);
+              if (d < best) { best = d; bx = j; }
+            }
+          }
+        }
+      }
+      if (amb) {
+        bj = bx;
+        ++namb;
+      }
+    }
+    if (active) {
+      srec[3 * tid + 0] = q8d(mean);
+      srec[3 * tid + 1] = q8d(__dmul_rn(sd, 4.0));
+      srec[3 * tid + 2] = (uint8_t)bj;
+    }
+    tc::fence_before();
+    __syncthreads();
+    const int64_t k0 = t * tc::M;
+    const int64_t nrec = (nblocks - k0 < tc::M ? nblocks - k0 : tc::M) * 3;
+    uint8_t* rec = a.records + (img * nblocks + k0) * 3;
+    for (int e = tid; e < nrec; e += tc::THREADS) rec[e] = srec[e];
+  }
+  if (ambiguous && namb) atomicAdd(ambiguous, namb);
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// DPP_IMGC_VQ=exact selects the CUDA-core brute force (1), default tensor cores (0)
+static int vq_mode() {
+  const char* e = getenv("DPP_IMGC_VQ");  // read per call: tests flip it at run time
+  return (e && e[0] == 'e') ? 1 : 0;
+}
+
+static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, int64_t nblocks, float delta_scale,
+                            unsigned long long* ambiguous, cudaStream_t s) {
+  static int sm_count = 0;
+  if (!sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (sm_count <= 0) sm_count = 148;
+  }
+  const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
+  int64_t per_image = (2 * (int64_t)sm_count + batch - 1) / batch;
+  if (per_image > ntiles) per_image = ntiles;
+  if (per_image < 1) per_image = 1;
+  dim3 grid((unsigned)per_image, (unsigned)batch);
+  const size_t smem = tc::SMEM;
+  switch (channels) {
+#define TC_CASE(CHN)                                                                                        \
+  case CHN:                                                                                                 \
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(encode_tc_kernel<CHN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        (int)smem));                                                        \
+    encode_tc_kernel<CHN><<<grid, tc::THREADS, smem, s>>>(a, delta_scale, ambiguous);                       \
+    break;
+    TC_CASE(1)
+    TC_CASE(3)
+    TC_CASE(4)
+#undef TC_CASE
+  }
+  DPP_LAUNCH_CHECK("encode_tc_kernel");
+  return DPP_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -479,15 +759,30 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
   dpp::EncodeArgs a{px, height, width, row_stride, image_stride, codebook, n_cb, codebook_stride, sigma_min,
                     records, cb_plane, cr_plane, block_grad, norm32, nullptr};
   const int64_t nblocks = (height / 4) * (width / 4);
-  dim3 grid(dpp::grid1(nblocks, 256), (unsigned)batch);
   auto s = (cudaStream_t)stream;
-  switch (channels) {
-    case 1: dpp::encode_kernel<1><<<grid, 256, 0, s>>>(a); break;
-    case 3: dpp::encode_kernel<3><<<grid, 256, 0, s>>>(a); break;
-    default: dpp::encode_kernel<4><<<grid, 256, 0, s>>>(a); break;
+  if (dpp::vq_mode() == 1) {
+    dim3 grid(dpp::grid1(nblocks, 256), (unsigned)batch);
+    switch (channels) {
+      case 1: dpp::encode_kernel<1><<<grid, 256, 0, s>>>(a); break;
+      case 3: dpp::encode_kernel<3><<<grid, 256, 0, s>>>(a); break;
+      default: dpp::encode_kernel<4><<<grid, 256, 0, s>>>(a); break;
+    }
+    DPP_LAUNCH_CHECK("encode_kernel");
+    return DPP_OK;
   }
-  DPP_LAUNCH_CHECK("encode_kernel");
-  return DPP_OK;
+  return dpp::launch_encode_tc(a, channels, batch, nblocks, 1.0f, nullptr, s);
+}
+
+// Test hook: the tensor-core encoder with a scaled pruning band and a count of
+// blocks that needed the exact re-check (device counter, accumulated).
+int dpp_imgc_encode_tc_debug(const uint8_t* px, int channels, int64_t height, int64_t width, const float* codebook,
+                             int n_cb, uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane, float delta_scale,
+                             unsigned long long* ambiguous, void* stream) {
+  if (height % 4 || width % 4 || n_cb < 1 || n_cb > 256) return dpp::fail(DPP_EINVAL, "bad geometry");
+  dpp::EncodeArgs a{px, height, width, width * channels, height * width * channels, codebook, n_cb, 0, 0.25,
+                    records, cb_plane, cr_plane, nullptr, nullptr, nullptr};
+  return dpp::launch_encode_tc(a, channels, 1, (height / 4) * (width / 4), delta_scale, ambiguous,
+                               (cudaStream_t)stream);
 }
 
 int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,

@@ -153,6 +153,71 @@ def test_c4_full_size_8192_gray(cuda):
     assert np.array_equal(cbp[: 64 * 2048].cpu().numpy(), f["cb"].ravel())
 
 
+# -- tensor-core pruned search: identical to the exact search ------------------------
+
+def _encode_tc(cuda, img, cents, delta_scale=1.0):
+    import ctypes
+
+    import torch
+
+    from paper_1203_4938_b200 import _lib
+    h, w = img.shape[:2]
+    ch = 1 if img.ndim == 2 else img.shape[2]
+    nb = (h // 4) * (w // 4)
+    px = torch.from_numpy(np.ascontiguousarray(img)).to(cuda)
+    cb = torch.from_numpy(np.ascontiguousarray(cents, np.float32)).to(cuda)
+    rec = torch.empty(nb * 3, dtype=torch.uint8, device=cuda)
+    cbp = torch.empty(nb, dtype=torch.uint8, device=cuda)
+    crp = torch.empty(nb, dtype=torch.uint8, device=cuda)
+    amb = torch.zeros(1, dtype=torch.int64, device=cuda)
+    _lib.check(_lib.load().dpp_imgc_encode_tc_debug(px.data_ptr(), ch, h, w, cb.data_ptr(), len(cents),
+                                                    rec.data_ptr(), cbp.data_ptr(), crp.data_ptr(),
+                                                    ctypes.c_float(delta_scale), amb.data_ptr(), None))
+    return rec.view(-1, 3).cpu().numpy(), int(amb.item()), nb
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_tensor_core_search_equals_exact_search(cuda, seed):
+    """Whatever the band width, the TC path must give the exact reference
+    indices: the re-check makes the result independent of the approximation."""
+    img = io.synthetic_image(512, 512, seed=30 + seed)
+    y, _, _ = io.ycbcr(img)
+    cents = io.train_codebook(y, 256, seed)
+    f = io.encode(img, cents)
+    for scale in (1.0, 30.0):
+        rec, amb, nb = _encode_tc(cuda, img, cents, scale)
+        assert np.array_equal(rec[:, 2], f["indices"]), (scale, int((rec[:, 2] != f["indices"]).sum()))
+        assert np.array_equal(rec[:, 0], f["means"]) and np.array_equal(rec[:, 1], f["sigma_idx"])
+    rec, amb, nb = _encode_tc(cuda, img, cents, 1.0)
+    print(f"ambiguous blocks (exact re-check): {amb} of {nb} ({100 * amb / nb:.2f}%)")
+    assert amb < 0.1 * nb
+
+
+def test_tensor_core_search_adversarial_codebooks(cuda):
+    """Duplicated centroids (exact ties -> first index), a tiny codebook, and a
+    codebook with large norms (band scales with |c|max)."""
+    rng = np.random.default_rng(4)
+    img = io.synthetic_image(256, 128, seed=44)
+    y, _, _ = io.ycbcr(img)
+    base = io.train_codebook(y, 64, 0)
+    dup = np.concatenate([base, base[::-1], base[:5]])       # 133 entries, every vector twice+
+    big = (rng.standard_normal((200, 16)) * 6).astype(np.float32)
+    for cents in (dup, base[:3], big):
+        f = io.encode(img, cents)
+        rec, _, _ = _encode_tc(cuda, img, cents)
+        assert np.array_equal(rec[:, 2], f["indices"])
+
+
+def test_default_path_is_tensor_core_and_matches_exact(cuda, imgc_golden, monkeypatch):
+    from paper_1203_4938_b200.apps import imgc
+    blob = imgc_golden["fix512_cb256_s0_blob"].tobytes()
+    ref = imgc.CompressedImage.from_bytes(blob)
+    image = imgc_golden["fix512_cb256_s0_image"]
+    assert imgc.compress(image, 256, codebook=ref.codebook).to_bytes() == blob  # default: TC
+    monkeypatch.setenv("DPP_IMGC_VQ", "exact")
+    assert imgc.compress(image, 256, codebook=ref.codebook).to_bytes() == blob
+
+
 # -- GPU k-means codebook (tolerance parity; SURVEY §8(f) row 2) ----------------------
 
 def test_block_stats_bit_exact(cuda):
