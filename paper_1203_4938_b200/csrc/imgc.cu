@@ -404,10 +404,12 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return d;                            // base offset 0, layout SWIZZLE_NONE
 }
 // kind::tf32, fp32 accumulate, A/B K-major, N = 256, M = 128
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCB >> 3) << 17) |
+constexpr int NH = 128;     // centroids per MMA pass = TMEM columns allocated
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) |
                            ((uint32_t)(M >> 4) << 24);
 constexpr size_t A_BYTES = M * 32 * 4, B_BYTES = NCB * 32 * 4;
-constexpr size_t SMEM = A_BYTES + B_BYTES + NCB * 8 * sizeof(float2) + NCB * sizeof(float) + 16 * 1024;  // +pad: 2 CTAs/SM
+// 49 KB -> 4 CTAs per SM, and 4 x 128 TMEM columns = the whole 512
+constexpr size_t SMEM = A_BYTES + B_BYTES + NCB * sizeof(float);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
@@ -440,8 +442,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   extern __shared__ __align__(1024) uint8_t tsm[];
   uint8_t* sA = tsm;
   uint8_t* sB = tsm + tc::A_BYTES;
-  float2* scp = reinterpret_cast<float2*>(sB + tc::B_BYTES);  // exact codebook, pair order
-  float* scn = reinterpret_cast<float*>(scp + tc::NCB * 8);   // |c_j|^2
+  float* scn = reinterpret_cast<float*>(sB + tc::B_BYTES);  // |c_j|^2
   __shared__ uint8_t srec[tc::M * 3];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
@@ -458,7 +459,6 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
     *reinterpret_cast<float*>(sB + tc::off(j, k)) = hi;
     *reinterpret_cast<float*>(sB + tc::off(j, 16 + k)) = __fsub_rn(c, hi);  // exact remainder
   }
-  vq_stage_codebook(cbk, a.ncb, scp);
   if (tid == 0) cmax_bits = 0;
   __syncthreads();
   for (int j = tid; j < tc::NCB; j += tc::THREADS) {
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
     if (j < a.ncb) atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
   uint32_t phase = 0;
   unsigned long long namb = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t k = t * tc::M + tid;
     const bool active = k < nblocks;
     float nb[16];
@@ -516,73 +516,84 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
       *reinterpret_cast<float4*>(sA + tc::off(tid, 4 * q)) = hi;
       *reinterpret_cast<float4*>(sA + tc::off(tid, 16 + 4 * q)) = lo;
     }
-    fence_proxy_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
-      const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
-#pragma unroll
-      for (int m = 0; m < 6; ++m)
-        tc::mma_tf32(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
-      tc::commit(&bar);
-    }
-    mbar_wait(&bar, phase);
-    tc::fence_after();
-
-    // pass 1: best and runner-up approximate score
+    // two MMA passes of 128 centroids each through the same 128 TMEM columns;
+    // pass 1 keeps the best and runner-up approximate score
     float m1 = 3.0e38f, m2 = 3.0e38f;
     int i1 = 0;
 #pragma unroll 1
-    for (int ch = 0; ch < tc::NCB / 32; ++ch) {
-      uint32_t r[32];
-      tc::ld32(taddr + ch * 32, r);
-      const float4* cn4 = reinterpret_cast<const float4*>(scn + ch * 32);
+    for (int h = 0; h < tc::NCB / tc::NH; ++h) {
+      fence_proxy_async_smem();
+      tc::fence_before();
+      __syncthreads();  // A written (h = 0) / previous half's TMEM reads done (h = 1)
+      if (tid == 0) {
+        tc::fence_after();
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB) + h * (tc::NH / 8) * 1024;
+        // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
+        const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 cn = cn4[c4];
-        const float cv[4] = {cn.x, cn.y, cn.z, cn.w};
+        for (int m = 0; m < 6; ++m)
+          tc::mma_tf32(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
+        tc::commit(&bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      tc::fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < tc::NH / 32; ++ch) {
+        uint32_t r[32];
+        tc::ld32(taddr + ch * 32, r);
+        const int j0 = h * tc::NH + ch * 32;
+        const float4* cn4 = reinterpret_cast<const float4*>(scn + j0);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float s = fmaf(-2.f, __uint_as_float(r[4 * c4 + e]), cv[e]);
-          const bool p = s < m1;
-          m2 = p ? m1 : fminf(m2, s);
-          i1 = p ? ch * 32 + 4 * c4 + e : i1;
-          m1 = p ? s : m1;
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 cn = cn4[c4];
+          const float cv[4] = {cn.x, cn.y, cn.z, cn.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float s = fmaf(-2.f, __uint_as_float(r[4 * c4 + e]), cv[e]);
+            const bool p = s < m1;
+            m2 = p ? m1 : fminf(m2, s);
+            i1 = p ? j0 + 4 * c4 + e : i1;
+            m1 = p ? s : m1;
+          }
         }
       }
     }
     const bool amb = active && !(m2 - m1 > delta2);
     int bj = i1;
-    if (__any_sync(0xffffffffu, amb)) {
-      // pass 2 (rare): exact reference distance for every candidate in the band
+    if (amb) {
+      // rare (~0.05 % of blocks): rescore every centroid on the CUDA cores
+      // (fp32, error << DELTA) and run the reference's exact distance on each
+      // one inside the band, in index order with strict <
       float2 bp[8];
       vq_pack(nb, bp);
       float best = VQ_BEST_INIT;
       int bx = 0;
       const float lim = m1 + delta2;
 #pragma unroll 1
-      for (int ch = 0; ch < tc::NCB / 32; ++ch) {
-        uint32_t r[32];
-        tc::ld32(taddr + ch * 32, r);
-        if (amb) {
-#pragma unroll 1
-          for (int c = 0; c < 32; ++c) {
-            const int j = ch * 32 + c;
-            const float s = fmaf(-2.f, __uint_as_float(r[c]), scn[j]);
-            if (s <= lim && j < a.ncb) {
-              const float d = vq_dist_pairs(bp, scp + 8 * j);
-              if (d < best) { best = d; bx = j; }
-            }
-          }
+      for (int j = 0; j < a.ncb; ++j) {
+        float c[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 hi = *reinterpret_cast<const float4*>(sB + tc::off(j, 4 * q));
+          const float4 lo = *reinterpret_cast<const float4*>(sB + tc::off(j, 16 + 4 * q));
+          c[4 * q] = __fadd_rn(hi.x, lo.x);  // hi + lo == c exactly
+          c[4 * q + 1] = __fadd_rn(hi.y, lo.y);
+          c[4 * q + 2] = __fadd_rn(hi.z, lo.z);
+          c[4 * q + 3] = __fadd_rn(hi.w, lo.w);
+        }
+        float dotv = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dotv = fmaf(nb[i], c[i], dotv);
+        if (fmaf(-2.f, dotv, scn[j]) <= lim) {
+          float2 cp[8];
+          vq_pack(c, cp);
+          const float d = vq_dist_pairs(bp, cp);
+          if (d < best) { best = d; bx = j; }
         }
       }
-      if (amb) {
-        bj = bx;
-        ++namb;
-      }
+      bj = bx;
+      ++namb;
     }
     if (active) {
       srec[3 * tid + 0] = q8d(mean);
@@ -599,7 +610,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   if (ambiguous && namb) atomicAdd(ambiguous, namb);
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 // DPP_IMGC_VQ=exact selects the CUDA-core brute force (1), default tensor cores (0)
@@ -618,7 +629,7 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
     if (sm_count <= 0) sm_count = 148;
   }
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
-  int64_t per_image = (2 * (int64_t)sm_count + batch - 1) / batch;
+  int64_t per_image = (4 * (int64_t)sm_count + batch - 1) / batch;  // 4 resident CTAs per SM
   if (per_image > ntiles) per_image = ntiles;
   if (per_image < 1) per_image = 1;
   dim3 grid((unsigned)per_image, (unsigned)batch);
