@@ -561,17 +561,26 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
     }
     const bool amb = active && !(m2 - m1 > delta2);
     int bj = i1;
-    if (amb) {
-      // rare (~0.05 % of blocks): rescore every centroid on the CUDA cores
-      // (fp32, error << DELTA) and run the reference's exact distance on each
-      // one inside the band, in index order with strict <
+    unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
+    // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block at
+    // a time — each lane rescores 8 centroids on the CUDA cores (fp32, error
+    // << DELTA) and runs the reference's exact distance on those inside the
+    // band; a lexicographic (distance, index) warp minimum then reproduces
+    // "strict <, first index wins" over all 256.
+    const int lane = tid & 31;
+    while (amb_lanes) {
+      const int src = __ffs(amb_lanes) - 1;
+      amb_lanes &= amb_lanes - 1;
+      float nv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) nv[i] = __shfl_sync(0xffffffffu, nb[i], src);
+      const float lim = __shfl_sync(0xffffffffu, m1 + delta2, src);
       float2 bp[8];
-      vq_pack(nb, bp);
+      vq_pack(nv, bp);
       float best = VQ_BEST_INIT;
-      int bx = 0;
-      const float lim = m1 + delta2;
+      int bx = 0x7fffffff;
 #pragma unroll 1
-      for (int j = 0; j < a.ncb; ++j) {
+      for (int j = lane; j < a.ncb; j += 32) {
         float c[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -584,7 +593,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
         }
         float dotv = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dotv = fmaf(nb[i], c[i], dotv);
+        for (int i = 0; i < 16; ++i) dotv = fmaf(nv[i], c[i], dotv);
         if (fmaf(-2.f, dotv, scn[j]) <= lim) {
           float2 cp[8];
           vq_pack(c, cp);
@@ -592,8 +601,16 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
           if (d < best) { best = d; bx = j; }
         }
       }
-      bj = bx;
-      ++namb;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float od = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bx, o);
+        if (od < best || (od == best && oj < bx)) { best = od; bx = oj; }
+      }
+      if (lane == src) {
+        bj = bx == 0x7fffffff ? 0 : bx;
+        ++namb;
+      }
     }
     if (active) {
       srec[3 * tid + 0] = q8d(mean);
