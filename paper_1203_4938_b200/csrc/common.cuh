@@ -75,6 +75,8 @@ __device__ __forceinline__ void dft2(float2& a, float2& b) {
 }
 
 // in: x0..x3 natural, out: natural
+// (folding the -i rotation into FFMA2s with 0/+-1 lane constants was measured:
+// +67 FP and +38 MOV instructions per thread in the 2^16 kernel — kept simple)
 __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
   float2 s02 = cadd(x0, x2), d02 = csub(x0, x2);
   float2 s13 = cadd(x1, x3), d13 = cmul_mi(csub(x1, x3));

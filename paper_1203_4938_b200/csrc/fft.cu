@@ -608,7 +608,8 @@ struct RowsCfg {
   using Base = ClusterCfg<N1, N2, C>;
   static constexpr int TILE = N1 * N2 / C;
   static constexpr int BUF = TILE;
-  static constexpr size_t SMEM = (size_t)(Base::NC + BUF + (SEPRECV ? TILE : 0)) * sizeof(float2);
+  // coarse twiddles as float4 (w, i*w): 2 float2 slots per entry
+  static constexpr size_t SMEM = (size_t)(2 * Base::NC + BUF + (SEPRECV ? TILE : 0)) * sizeof(float2);
 };
 
 template <int N1, int N2, int C, bool SEPRECV>
@@ -620,8 +621,8 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
   constexpr int R = Cfg::R, N = Cfg::N, W1 = Cfg::W1, W2 = Cfg::W2, T1 = Cfg::T1, T2 = Cfg::T2;
   extern __shared__ __align__(128) float2 smem[];
   __shared__ uint64_t bars[2];
-  float2* coarse = smem;
-  float2* buf = smem + Cfg::NC;
+  float4* coarse = reinterpret_cast<float4*>(smem);
+  float2* buf = smem + 2 * Cfg::NC;
   float2* recv = SEPRECV ? buf + RC::TILE : buf;
 
   const int p = (int)cluster_ctarank();
@@ -635,7 +636,10 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
     mbar_arrive_expect_tx(&bars[1], (uint32_t)(N2 * W2 * sizeof(float2)));
     tma_load_2d(buf, &tin, p * W1, (int)(t * N1), &bars[0]);
   }
-  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) {
+    const float2 w = coarse_g[e];
+    coarse[e] = make_float4(w.x, w.y, -w.y, w.x);
+  }
   __syncthreads();
   if constexpr (SEPRECV) cluster_arrive_relaxed();  // mbarriers initialised
 

@@ -41,7 +41,7 @@ struct ColCfg {
   static constexpr int LOGS = ilog2(S);
   static constexpr int TILE = L1 * F1;
   static_assert(TILE == L2 * F2, "tile sizes must agree");
-  static constexpr size_t SMEM = (size_t)(NC + TILE) * sizeof(float2);
+  static constexpr size_t SMEM = (size_t)(2 * NC + TILE) * sizeof(float2);
 };
 
 struct MapRow2 {
@@ -57,8 +57,8 @@ fft_columns_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__
   constexpr int R = Cfg::R, B1 = Cfg::B1, B2 = Cfg::B2, F1 = Cfg::F1, F2 = Cfg::F2, T1 = Cfg::T1, T2 = Cfg::T2;
   extern __shared__ __align__(128) float2 smem[];
   __shared__ uint64_t bars[2];
-  float2* coarse = smem;
-  float2* buf = smem + Cfg::NC;
+  float4* coarse = reinterpret_cast<float4*>(smem);  // (w, i*w)
+  float2* buf = smem + 2 * Cfg::NC;
 
   const int p = (int)cluster_ctarank();
   const int64_t tile = blockIdx.x / C;
@@ -73,7 +73,10 @@ fft_columns_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__
     mbar_arrive_expect_tx(&bars[1], (uint32_t)(Cfg::TILE * sizeof(float2)));
     tma_load_3d(buf, &tin, c0, p * B1, (int)(img * L1), &bars[0]);
   }
-  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) coarse[e] = coarse_g[e];
+  for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) {
+    const float2 w = coarse_g[e];
+    coarse[e] = make_float4(w.x, w.y, -w.y, w.x);
+  }
   __syncthreads();
 
   // pass A: sequence f = (bl, col), FFT over a

@@ -25,9 +25,16 @@ struct MapPad16 {  // one float2 of padding per 16 elements: breaks stride-16 ba
   __device__ __forceinline__ int operator()(int e) const { return e + (e >> 4); }
 };
 
-template <int M, int R, class Map>
+// twiddle multiply from a table entry: float2 = w (rotation built on the fly),
+// float4 = (w, i*w) precomputed so the product is exactly FMUL2 + FFMA2
+__device__ __forceinline__ float2 twmul(float2 v, float2 w) { return cmul(v, w); }
+__device__ __forceinline__ float2 twmul(float2 v, float4 w) {
+  return cmul_pre(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
+}
+
+template <int M, int R, class Map, class TW>
 __device__ __forceinline__ void block_fft(float2 (&v)[R], int j, float2* buf, Map map,
-                                          const float2* tw, int tw_step) {
+                                          const TW* tw, int tw_step) {
   constexpr int T = M / R;
   constexpr int LOGM = ilog2(M);
   constexpr int LOGR = ilog2(R);
@@ -59,7 +66,7 @@ __device__ __forceinline__ void block_fft(float2 (&v)[R], int j, float2* buf, Ma
     if (ns > 1) {
       const int unit = jm * (M / (ns * R));
 #pragma unroll
-      for (int i = 1; i < R; ++i) v[i] = cmul(v[i], tw[(i * unit) * tw_step]);
+      for (int i = 1; i < R; ++i) v[i] = twmul(v[i], tw[(i * unit) * tw_step]);
     }
     dft_r<R>(v);
     if (ns * R < M) {
