@@ -73,7 +73,7 @@ def fft2d_row_sharded(local_rows: torch.Tensor, n0: int, *, group=None, transpos
     send = pack_column_blocks(x, world)             # (P, r, n1/P)
     recv = torch.empty_like(send)
     if world > 1:
-        dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+        _all_to_all(recv, send, group)
     else:
         recv = send
     slab = recv.view(n0, n1 // world)               # rows in global order: already the column slab
@@ -83,7 +83,14 @@ def fft2d_row_sharded(local_rows: torch.Tensor, n0: int, *, group=None, transpos
     back = slab.view(world, r, n1 // world).contiguous()  # block s -> rank s (its rows)
     out = torch.empty_like(back)
     if world > 1:
-        dist.all_to_all_single(out.view(-1), back.view(-1), group=group)
+        _all_to_all(out, back, group)
     else:
         out = back
     return unpack_column_blocks(out)
+
+
+def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group) -> None:
+    """Equal-split all-to-all of complex64 buffers as float32 pairs (NCCL on
+    CUDA tensors, gloo on CPU); block s of `send` goes to rank s."""
+    as_real = (lambda t: torch.view_as_real(t).reshape(-1)) if send.is_complex() else (lambda t: t.reshape(-1))
+    dist.all_to_all_single(as_real(recv), as_real(send), group=group)
