@@ -115,7 +115,8 @@ def max_over_ranks(value: float, world: int) -> float:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64,
+                     device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -188,9 +189,17 @@ def run_ours(args) -> None:
     import torch
 
     world, rank, local = dist_env()
+    # DPP_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo — a smoke test of the
+    # multi-rank code path on a 1-GPU box (NCCL refuses two ranks per device)
+    share = os.environ.get("DPP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 

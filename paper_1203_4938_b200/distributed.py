@@ -93,4 +93,12 @@ def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group) -> None:
     """Equal-split all-to-all of complex64 buffers as float32 pairs (NCCL on
     CUDA tensors, gloo on CPU); block s of `send` goes to rank s."""
     as_real = (lambda t: torch.view_as_real(t).reshape(-1)) if send.is_complex() else (lambda t: t.reshape(-1))
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo cannot exchange CUDA buffers: used only by multi-rank tests that
+        # share one GPU (NCCL refuses two ranks on one device)
+        staged = as_real(send).cpu()
+        got = torch.empty_like(staged)
+        dist.all_to_all_single(got, staged, group=group)
+        as_real(recv).copy_(got)
+        return
     dist.all_to_all_single(as_real(recv), as_real(send), group=group)
