@@ -84,6 +84,10 @@ int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, vo
 
 void dpp_fft_plan_destroy(dpp_fft_plan* plan);
 
+/* The reference's quadratic oracle naive_dft (apps/fft.py:32-42) on the
+ * device: binary64 accumulation, rounded to complex64; `batch` signals of n. */
+int dpp_naive_dft(const float* x, float* y, int64_t n, int64_t batch, void* stream);
+
 /* Leaf DFT node dft{2,4,8} (apps/fft.py:86-123): one dense 2^k-point DFT per
  * work-item over float{2^(k+1)} vectors whose lanes sit at bit-reversed
  * offsets.  Arithmetic is the generated body's exactly: binary32, terms in

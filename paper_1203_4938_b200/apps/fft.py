@@ -28,12 +28,32 @@ from ..model import Instance, Node, Program
 from ..types import DataType, Direction, IOPoint
 from ..wire import DeviceStream, StreamFile
 
-__all__ = ["MAX_LEAF_ORDER", "FftPlan", "fft", "fft_batch", "fft2", "bit_reverse_indices",
+__all__ = ["MAX_LEAF_ORDER", "FftPlan", "fft", "fft_batch", "fft2", "naive_dft", "bit_reverse_indices",
            "leaf_kernel", "leaf_program", "fft_kernel", "fft_program", "fft2d_kernel",
            "fft2d_program", "fft_bench", "BenchRow", "parse_sizes", "NATIVE_TAG"]
 
 MAX_LEAF_ORDER = 3
 NATIVE_TAG = "// dpp-b200 native:"
+
+
+def naive_dft(signal) -> np.ndarray:
+    """Direct O(N^2) DFT (fft.py:32-42) computed on the device in binary64 and
+    rounded to complex64; numpy in -> numpy out, CUDA tensor in -> tensor out."""
+    import torch
+
+    from .. import _lib
+    from .._torch import require_cuda, stream_handle
+    is_t = isinstance(signal, torch.Tensor)
+    x = signal if is_t else torch.from_numpy(np.ascontiguousarray(signal, np.complex64))
+    if x.numel() < 1:
+        raise ValueError("signal must have at least one sample")
+    dev = x.device if is_t and x.is_cuda else require_cuda(None)
+    xd = x.to(dev, torch.complex64).contiguous()
+    n = xd.shape[-1]
+    y = torch.empty_like(xd)
+    _lib.check(_lib.load().dpp_naive_dft(xd.data_ptr(), y.data_ptr(), n, xd.numel() // n, stream_handle()),
+               "naive_dft")
+    return y if is_t and x.is_cuda else y.cpu().numpy()
 
 
 def bit_reverse_indices(n: int) -> np.ndarray:

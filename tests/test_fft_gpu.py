@@ -169,6 +169,31 @@ def test_leaf_nodes_bit_exact_with_reference_engine(cuda, leaf_golden, k):
     assert np.array_equal(y.cpu().numpy(), leaf_golden[f"y_k{k}"])
 
 
+def test_device_naive_dft_and_known_answers(cuda, fft_golden):
+    """naive_dft on the device (fft.py:32-42): the reference's identities
+    (test_fft.py:18-36) and the golden naive outputs; then used as an
+    independent O(N^2) check of the fast 2^16 transform."""
+    from paper_1203_4938_b200.apps.fft import naive_dft
+    assert np.allclose(naive_dft(np.array([1, 0, 0, 0], np.complex64)), np.ones(4), atol=1e-6)
+    assert np.allclose(naive_dft(np.array([1, 2, 3, 4], np.complex64)), [10, -2 + 2j, -2, -2 - 2j], atol=1e-5)
+    out = naive_dft(np.full(8, 2.5, np.complex64))
+    assert abs(out[0] - 20) < 1e-5 and np.abs(out[1:]).max() < 1e-5
+    assert naive_dft(np.array([3 + 4j], np.complex64))[0] == np.complex64(3 + 4j)
+    for m in range(3, 11):
+        n = 1 << m
+        assert rel_l2(naive_dft(fft_golden[f"x_{n}"]), fft_golden[f"naive_{n}"]) < 1e-6
+    x = complex_signals(91, 65536)
+    assert rel_l2(_fft(x, 65536, cuda), naive_dft(x)) <= tol(65536)
+
+
+def test_fft_bench_rows(cuda):  # test_fft.py:143-147, F7
+    from paper_1203_4938_b200.apps.fft import fft_bench
+    rows = fft_bench([32 * 1024, 64 * 1024], ks=(1, 2), warmup=False)
+    assert [(r.nbytes, r.k) for r in rows] == [(32768, 1), (65536, 1), (32768, 2), (65536, 2)]
+    assert all(r.seconds > 0 and r.backend == "b200" for r in rows)
+    assert rows[0].csv().startswith("32768,1,")
+
+
 def test_size_errors(cuda):
     import torch
 
