@@ -19,7 +19,8 @@ def main() -> None:
 
     from paper_1203_4938_b200 import ops
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["fft", "encode", "fft2d"])
+    ap.add_argument("what", choices=["fft", "encode", "fft2d", "chain"])
+    ap.add_argument("--images", type=int, default=64)
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--rows", type=int, default=16384)
@@ -34,6 +35,13 @@ def main() -> None:
         y = torch.empty_like(x)
         for _ in range(a.iters):
             ops.fft_forward(x, a.n, out=y)
+    elif a.what == "chain":
+        from paper_1203_4938_b200 import CudaBackend
+        from paper_1203_4938_b200.apps import chain
+        imgs = torch.randint(0, 256, (a.images, 4096, 4096), dtype=torch.uint8, device=dev, generator=g)
+        cbs = torch.randn((a.images, 256, 16), dtype=torch.float32, device=dev, generator=g)
+        for _ in range(a.iters):
+            chain.run_chain(imgs, cbs, backend=CudaBackend(outputs="device"))
     elif a.what == "fft2d":
         x = torch.randn((a.rows, a.cols), dtype=torch.complex64, device=dev, generator=g)
         for _ in range(a.iters):
