@@ -644,6 +644,11 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
   if constexpr (SEPRECV) cluster_arrive_relaxed();  // mbarriers initialised
 
   const int col = tid % W1, j = tid / W1;
+  const int b = p * W1 + col;
+  // per-thread four-step bases from the global tables (L1-cached, no bank
+  // conflicts), fetched before the tile wait so their latency hides behind it
+  const float2 tw0a = __ldg(coarse_g + ((b * j) >> Cfg::LOGS)), tw0b = __ldg(fine_g + ((b * j) & (Cfg::S - 1)));
+  const float2 tw1a = __ldg(coarse_g + ((b * T1) >> Cfg::LOGS)), tw1b = __ldg(fine_g + ((b * T1) & (Cfg::S - 1)));
   float2 v[R];
   mbar_wait(&bars[0], 0);
 #pragma unroll
@@ -651,12 +656,9 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
   __syncthreads();
   block_fft<N1, R>(v, j, buf, MapRow{W1, col}, coarse, Cfg::NC / N1);
   if constexpr (!SEPRECV) cluster_arrive_relaxed();  // this CTA no longer reads buf
-  const int b = p * W1 + col;
   {
-    // per-thread four-step bases from the global tables (L1-cached, no bank conflicts)
-    auto tw = [&](int e) { return cmul(__ldg(coarse_g + (e >> Cfg::LOGS)), __ldg(fine_g + (e & (Cfg::S - 1)))); };
-    float2 w = tw(b * j);
-    const float2 sw = tw(b * T1);
+    float2 w = cmul(tw0a, tw0b);
+    const float2 sw = cmul(tw1a, tw1b);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       v[i] = cmul(v[i], w);
@@ -817,7 +819,9 @@ int fft1d_plan_init(FftPlan* p) {
   const int lg = ilog2(n);
   if (n < 2 || (n & (n - 1)) != 0)
     return fail(DPP_EINVAL, "transform size must be a power of two, got %lld", (long long)n);
-  if (lg <= 12) {
+  // 2048 and 4096 go through the TMA/row-layout kernel with a 1-CTA "cluster":
+  // the generic small kernel ran 4096-point rows at 1.1 TB/s (C5 profile)
+  if (lg <= 10) {
     p->kind = FftPlan::SMALL;
     int rc = DPP_OK;
     switch (n) {
@@ -845,6 +849,8 @@ int fft1d_plan_init(FftPlan* p) {
     }
     int rc = DPP_OK;
     switch (n) {
+      case 2048: rc = prepare_cluster<32, 64, 1>(p); break;
+      case 4096: rc = prepare_cluster<64, 64, 1>(p); break;
       case 8192: rc = prepare_cluster<64, 128, 1>(p); break;
       case 16384: rc = prepare_cluster<128, 128, 2>(p); break;
       case 32768: rc = prepare_cluster<128, 256, 4>(p); break;
@@ -879,6 +885,8 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
     }
   } else if (p->kind == FftPlan::CLUSTER) {
     switch (p->n0) {
+      case 2048: return launch_cluster<32, 64, 1>(p, in, out, batch, s);
+      case 4096: return launch_cluster<64, 64, 1>(p, in, out, batch, s);
       case 8192: return launch_cluster<64, 128, 1>(p, in, out, batch, s);
       case 16384: return launch_cluster<128, 128, 2>(p, in, out, batch, s);
       case 32768: return launch_cluster<128, 256, 4>(p, in, out, batch, s);

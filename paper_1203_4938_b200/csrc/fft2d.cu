@@ -82,6 +82,10 @@ fft_columns_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__
   // pass A: sequence f = (bl, col), FFT over a
   const int f = tid % F1, j = tid / F1;
   const int bl = f / W, col = f - bl * W;
+  const int b = p * B1 + bl;
+  // four-step twiddle bases fetched before the tile wait (latency hidden)
+  const float2 tw0a = __ldg(coarse_g + ((b * j) >> Cfg::LOGS)), tw0b = __ldg(fine_g + ((b * j) & (Cfg::S - 1)));
+  const float2 tw1a = __ldg(coarse_g + ((b * T1) >> Cfg::LOGS)), tw1b = __ldg(fine_g + ((b * T1) & (Cfg::S - 1)));
   float2 v[R];
   mbar_wait(&bars[0], 0);
 #pragma unroll
@@ -89,11 +93,9 @@ fft_columns_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__
   __syncthreads();
   block_fft<L1, R>(v, j, buf, MapRow2{F1, f}, coarse, Cfg::NC / L1);
   cluster_arrive_relaxed();  // this CTA no longer reads buf
-  const int b = p * B1 + bl;
   {
-    auto tw = [&](int e) { return cmul(__ldg(coarse_g + (e >> Cfg::LOGS)), __ldg(fine_g + (e & (Cfg::S - 1)))); };
-    float2 w = tw(b * j);
-    const float2 sw = tw(b * T1);
+    float2 w = cmul(tw0a, tw0b);
+    const float2 sw = cmul(tw1a, tw1b);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       v[i] = cmul(v[i], w);
