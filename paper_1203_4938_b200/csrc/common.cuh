@@ -248,8 +248,10 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, int x, int y, int
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// wait only until the bulk stores have READ their shared-memory source (the CTA
+// may then exit or reuse it); global visibility is guaranteed at kernel end
 __device__ __forceinline__ void bulk_commit_and_wait_all() {
-  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 // asynchronous store into (possibly remote) shared memory; the destination
 // CTA's mbarrier at `rbar` (same cluster address space) receives 8 tx bytes
