@@ -8,12 +8,13 @@ no CPU fallback anywhere in the product path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import DeviceError, NativeLibraryError, PlanError
 
-LIB_PATH = Path(__file__).resolve().parent / "libdpp_b200.so"
+LIB_PATH = Path(os.environ.get("DPP_LIB_PATH") or Path(__file__).resolve().parent / "libdpp_b200.so")
 ABI_VERSION = 1
 
 DPP_OK, DPP_EINVAL, DPP_ECUDA, DPP_ENCCL, DPP_ENOTSUP = 0, 1, 2, 3, 4

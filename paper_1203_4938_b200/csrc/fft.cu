@@ -612,8 +612,16 @@ struct RowsCfg {
   static constexpr size_t SMEM = (size_t)(2 * Base::NC + BUF + (SEPRECV ? TILE : 0)) * sizeof(float2);
 };
 
+#ifndef DPP_ROWS_MINB256
+#define DPP_ROWS_MINB256 4
+#endif
+template <int THREADS>
+struct RowsMinBlocks {
+  static constexpr int value = THREADS == 256 ? DPP_ROWS_MINB256 : 1024 / THREADS;
+};
+
 template <int N1, int N2, int C, bool SEPRECV>
-__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::THREADS, 1024 / ClusterCfg<N1, N2, C>::THREADS)
+__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::THREADS, RowsMinBlocks<ClusterCfg<N1, N2, C>::THREADS>::value)
 fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out,
                  const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g) {
   using Cfg = ClusterCfg<N1, N2, C>;
