@@ -245,6 +245,11 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, int x, int y, int
                "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
                : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const void* tmap, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -612,6 +612,9 @@ struct RowsCfg {
   static constexpr size_t SMEM = (size_t)(2 * Base::NC + BUF + (SEPRECV ? TILE : 0)) * sizeof(float2);
 };
 
+#ifndef DPP_EXP
+#define DPP_EXP 0  // profiling only: 1 = data movement without the FFT math, 2 = math without HBM traffic
+#endif
 #ifndef DPP_ROWS_MINB256
 #define DPP_ROWS_MINB256 4
 #endif
@@ -640,9 +643,15 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
+#if DPP_EXP == 2
+    mbar_arrive_expect_tx(&bars[0], 0);
+#else
     mbar_arrive_expect_tx(&bars[0], (uint32_t)(N1 * W1 * sizeof(float2)));
+#endif
     mbar_arrive_expect_tx(&bars[1], (uint32_t)(N2 * W2 * sizeof(float2)));
+#if DPP_EXP != 2
     tma_load_2d(buf, &tin, p * W1, (int)(t * N1), &bars[0]);
+#endif
   }
   for (int e = tid; e < Cfg::NC; e += Cfg::THREADS) {
     const float2 w = coarse_g[e];
@@ -662,7 +671,9 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
 #pragma unroll
   for (int i = 0; i < R; ++i) v[i] = buf[(j + T1 * i) * W1 + col];
   __syncthreads();
+#if DPP_EXP != 1
   block_fft<N1, R>(v, j, buf, MapRow{W1, col}, coarse, Cfg::NC / N1);
+#endif
   if constexpr (!SEPRECV) cluster_arrive_relaxed();  // this CTA no longer reads buf
   {
     float2 w = cmul(tw0a, tw0b);
@@ -690,8 +701,13 @@ fft_cluster_rows(const __grid_constant__ CUtensorMap tin, float2* __restrict__ o
 #pragma unroll
   for (int i = 0; i < R; ++i) v[i] = recv[cl * N2 + ((j2 + T2 * i) ^ (cl & 15))];
   if constexpr (!SEPRECV) __syncthreads();  // SEPRECV: pass 2 exchanges in buf, free since pass 1
+#if DPP_EXP != 1
   block_fft<N2, R>(v, j2, buf, MapRow{W2, cl}, coarse, Cfg::NC / N2);
+#endif
   float2* dst = out + t * N + p * W2 + cl;
+#if DPP_EXP == 2
+  if (v[0].x != 1234.5f) return;
+#endif
 #pragma unroll
   for (int i = 0; i < R; ++i) __stcs(dst + (int64_t)(j2 + T2 * i) * N1, v[i]);
 }
@@ -725,6 +741,282 @@ static int launch_rows(const float2* in, float2* out, int64_t batch, const float
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_cluster_rows<N1, N2, C, SEPRECV>, tmap, out, coarse, fine));
+  return DPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// MODE 7 (2^16 = 256 x 256, 16-CTA clusters): warp-local passes.
+//
+// Each warp owns two whole columns of the CTA's 256 x 16 tile: lane l of warp
+// w works on column 2w + ((l >> 3) & 1) with j = (l & 7) | ((l >> 4) << 3), so
+// a column's 16 threads sit in one warp and both Stockham exchanges of a
+// 256-point pass need only __syncwarp (no CTA barrier), while each half-warp
+// covers 8 rows x 2 columns.  One 32 KB buffer per CTA carries everything and
+// a warp only ever touches its own columns' slots:
+//   TMA tile load (128B-swizzled [row][16 cols]) -> pass 1 in place ->
+//   st.async scatter into the peers' buffers ([b][16 cl], same swizzle) ->
+//   pass 2 in place -> output tile staged in place -> one TMA tile store.
+// Slot (row r, column c) = float2 16r + 2((c/2) ^ (r&7)) + (c&1).  Every
+// access pattern below gives a half-warp 8 distinct r&7 x 2 column parities =
+// 16 distinct 8-byte bank pairs (conflict-free, 2 wavefronts per warp):
+//   rows j + 16i (tile read, output staging): r&7 = j&7;
+//   pass-2 receive rows rho(b) = b ^ ((b&1) << 2), which also keeps the two
+//   sending columns (b even/odd) on disjoint chunks at the receiver;
+//   exchange rows xr(e) = 16(e/16) + ((e%16) ^ ((e/16)&7)) for both the write
+//   (e = 16j + i) and the read (e = j + 16i): r&7 = (i ^ j)&7.
+// For the exchange the slot is ((per-thread base) ^ 18(i&7)) + const(i), so
+// each access costs one LOP3 (the XOR lands on bits the base keeps clear).
+// Stage twiddles W_256^{ij}: a [j][i ^ (j&7)] float4 (w, i*w) table.
+// SEP: separate receive buffer (no buffer-free cluster barrier, 3 CTAs/SM).
+#ifdef DPP_PHASES
+// profiling build only: per-CTA clock64 stamps of the MODE 7 phases
+__device__ long long g_phase[65536 * 12];
+extern "C" int dpp_debug_phases(long long* host, long long n) {
+  return cudaMemcpyFromSymbol(host, g_phase, (size_t)n * sizeof(long long)) == cudaSuccess ? 0 : 2;
+}
+#define PHASE(k) \
+  if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase[blockIdx.x * 12 + (k)] = clock64();
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+#define PHASE_EXTRA(k, v) \
+  if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase[blockIdx.x * 12 + (k)] = (v);
+#else
+#define PHASE(k)
+#define PHASE_EXTRA(k, v)
+#endif
+
+namespace w16 {
+constexpr int N1 = 256, N2 = 256, N = N1 * N2, C = 16, W = 16, R = 16, THREADS = 256;
+constexpr int TILE = N1 * W;  // 4096 float2 = 32 KB
+template <bool SEP>
+constexpr size_t smem_bytes() { return 1024 + (size_t)(SEP ? 2 : 1) * TILE * 8 + 256 * 16; }
+__device__ __forceinline__ uint32_t slot(int r, int c) {
+  return (uint32_t)(r * 16 + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1));
+}
+__device__ __forceinline__ float2 lds2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+
+// Per-thread shared-memory bases (bytes) of one 1024-aligned tile buffer.
+struct Lane {
+  uint32_t row;  // rows j + 16i: + 2048 i
+  uint32_t xw;   // exchange write e = 16j + i: (xw ^ 144(i&7)) + 1024 (i>>3)
+  uint32_t xq;   // exchange read  e = j + 16i: (xq ^ 144(i&7)) + 2048 i
+  __device__ __forceinline__ Lane(uint32_t buf, int w, int par, int j) {
+    const int j7 = j & 7;
+    const uint32_t z = (uint32_t)(18 * j7 ^ 2 * w);
+    row = buf + 8u * (uint32_t)(16 * j + 2 * (w ^ j7) + par);
+    xw = buf + 8u * ((uint32_t)(256 * j + par) | z);
+    xq = buf + 8u * ((uint32_t)(16 * (j & 8) + par) | z);
+  }
+};
+
+// 256-point Stockham transform of one column held as v[i] = x[j + 16 i]; on
+// exit v[i] = X[j + 16 i].  The column's slots serve as the exchange scratch.
+__device__ __forceinline__ void col256(float2 (&v)[R], const Lane& L, uint32_t twj, int j) {
+  dft16(v);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < R; ++i) sts2((L.xw ^ (144u * (i & 7))) + 1024u * (i >> 3), v[i]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = lds2((L.xq ^ (144u * (i & 7))) + 2048u * i);
+  (void)j;
+#pragma unroll
+  for (int i = 1; i < R; ++i) v[i] = twmul(v[i], lds4((twj ^ (16u * (i & 7))) + 128u * (i >> 3)));
+  dft16(v);
+}
+}  // namespace w16
+
+// PERSIST (MODE 9): ceil(batch / G) transforms per cluster, G = the
+// co-resident cluster count (31 on B200: a 16-CTA cluster needs 16 free slots
+// in one GPC, so at most 3.35 of the 4 slots per SM hold CTAs; launching one
+// cluster per transform averages 2.98, profiles/micro/phases.py).  The next
+// tile's TMA load is issued once the previous output store has read the
+// buffer.  Measured slower (1.64 vs 1.39 ms): without a second tile buffer
+// the load latency is exposed every iteration and each cluster runs at the
+// pace of its busiest SM.  Kept as a documented variant.
+template <bool SEP, bool PERSIST>
+__global__ void __launch_bounds__(w16::THREADS, SEP ? 3 : 4)
+fft_warp_65536(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+               const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g, int64_t batch) {
+  static_assert(!(SEP && PERSIST), "the separate-receive variant runs one transform per cluster");
+  using namespace w16;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t bars[2];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  float2* buf = reinterpret_cast<float2*>(smem_raw + pad);
+  float2* recv = SEP ? buf + TILE : buf;
+  float4* tw = reinterpret_cast<float4*>(buf + (SEP ? 2 : 1) * TILE);
+
+  const int p = (int)cluster_ctarank();
+  const int64_t stride = PERSIST ? (int64_t)(gridDim.x / C) : batch;
+  int64_t t = blockIdx.x / C;
+  const int tid = threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const int par = (lane >> 3) & 1, j = (lane & 7) | ((lane >> 4) << 3);
+  const int col = 2 * w + par;
+  PHASE(0)
+  PHASE_EXTRA(8, smid())
+  PHASE_EXTRA(9, gtimer())
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if (t < batch) {
+      mbar_arrive_expect_tx(&bars[0], (uint32_t)(TILE * 8));
+      tma_load_2d(buf, &tin, p * W, (int)(t * N1), &bars[0]);
+      mbar_arrive_expect_tx(&bars[1], (uint32_t)(TILE * 8));
+    }
+  }
+  {
+    // stage-twiddle table: entry [jj][ii ^ (jj & 7)] = W_256^{ii*jj} as (w, i*w)
+    const int jj = tid >> 4, ii = tid & 15;
+    const float2 x = __ldg(coarse_g + ((ii * jj) & 255));
+    tw[jj * 16 + (ii ^ (jj & 7))] = make_float4(x.x, x.y, -x.y, x.x);
+  }
+  const int b = p * W + col;
+  // four-step twiddle W_N^{b (j + 16 i)} = W_N^{bj} (W_N^{16b})^i from the
+  // coarse W_256 x fine W_N tables, fetched before the tile wait
+  const float2 w0 = cmul(__ldg(coarse_g + ((b * j) >> 8)), __ldg(fine_g + ((b * j) & 255)));
+  const float2 sw = cmul(__ldg(coarse_g + ((b * 16) >> 8)), __ldg(fine_g + ((b * 16) & 255)));
+  const uint32_t twj = smem_u32(tw) + 256u * (uint32_t)j + 16u * (uint32_t)(j & 7);
+  __syncthreads();
+  if constexpr (SEP) cluster_arrive_relaxed();  // mbarriers initialised
+
+  for (uint32_t k = 0; t < batch; t += stride, ++k) {
+    const uint32_t ph = k & 1;
+    float2 v[R];
+    {
+      const Lane L(smem_u32(buf), w, par, j);
+      mbar_wait(&bars[0], ph);
+      PHASE(1)
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = lds2(L.row + 2048u * i);
+      col256(v, L, twj, j);
+    }
+    PHASE(2)
+    if constexpr (!SEP) cluster_arrive_relaxed();  // this CTA no longer reads buf
+    {
+      float2 x = w0;
+      // opaque per iteration: otherwise the 16 loop-invariant twiddles are
+      // hoisted out of the persistent loop and spilled
+      asm volatile("" : "+f"(x.x), "+f"(x.y));
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        v[i] = cmul(v[i], x);
+        x = cmul(x, sw);
+      }
+    }
+    cluster_wait();
+    PHASE(3)
+    {
+      // Z[b][c = j + 16 i] belongs to CTA i, local column j, row rho(b)
+      const int rb = b ^ ((b & 1) << 2);
+      const uint32_t scatter_off = smem_u32(recv) + 8u * slot(rb, j);
+      const uint32_t rbar = smem_u32(&bars[1]);
+#pragma unroll
+      for (int i = 0; i < R; ++i) st_async_f2(mapa_u32(scatter_off, i), v[i], mapa_u32(rbar, i));
+    }
+    // pass 2: column c = 16 p + col over b = j + 16 i (received at row rho(b))
+    const Lane L(smem_u32(recv), w, par, j);
+    PHASE(4)
+    const int jr = j ^ ((j & 1) << 2);
+    const uint32_t rrow = smem_u32(recv) + 8u * (uint32_t)(16 * jr + 2 * (w ^ (jr & 7)) + par);
+    mbar_wait(&bars[1], ph);
+    PHASE(5)
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = lds2(rrow + 2048u * i);
+    col256(v, L, twj, j);
+    PHASE(6)
+    // X[c + 256 k2], k2 = j + 16 i: staged at row k2, column col; one TMA store
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i) sts2(L.row + 2048u * i, v[i]);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_2d(&tout, p * W, (int)(t * N2), recv);
+      bulk_commit_and_wait_all();
+      const int64_t tn = t + stride;
+      if (tn < batch) {
+        mbar_arrive_expect_tx(&bars[0], (uint32_t)(TILE * 8));
+        tma_load_2d(buf, &tin, p * W, (int)(tn * N1), &bars[0]);
+        mbar_arrive_expect_tx(&bars[1], (uint32_t)(TILE * 8));
+      }
+      PHASE(7)
+      PHASE_EXTRA(10, gtimer())
+    }
+  }
+}
+
+template <bool SEP, bool PERSIST>
+static int prepare_warp65536(int* max_clusters) {
+  auto kern = fft_warp_65536<SEP, PERSIST>;
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)w16::smem_bytes<SEP>()));
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  *max_clusters = 0;
+  if (PERSIST) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(w16::C * 1024, 1, 1);
+    cfg.blockDim = dim3(w16::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = w16::smem_bytes<SEP>();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = w16::C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DPP_CUDA_CHECK(cudaOccupancyMaxActiveClusters(max_clusters, kern, &cfg));
+    if (*max_clusters < 1) return fail(DPP_ECUDA, "no 16-CTA cluster of the 2^16 kernel fits on this device");
+  }
+  return DPP_OK;
+}
+
+template <bool SEP, bool PERSIST>
+static int launch_warp65536(const float2* in, float2* out, int64_t batch, const float2* coarse, const float2* fine,
+                            int max_clusters, cudaStream_t s) {
+  using namespace w16;
+  CUtensorMap tin, tout;
+  int rc = make_tmap_c64(&tin, in, (uint64_t)batch * N1, N2, N1, W, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_tmap_c64(&tout, out, (uint64_t)batch * N2, N1, N2, W, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  const int64_t clusters = PERSIST ? (batch < max_clusters ? batch : max_clusters) : batch;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(clusters * C), 1, 1);
+  cfg.blockDim = dim3(THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem_bytes<SEP>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_warp_65536<SEP, PERSIST>, tin, tout, coarse, fine, batch));
   return DPP_OK;
 }
 
@@ -766,7 +1058,7 @@ static int cluster_mode() {
   if (g_cluster_mode < 0) {
     const char* e = getenv("DPP_FFT_CLUSTER_MODE");
     g_cluster_mode = e ? (e[0] - '0') : 5;
-    if (g_cluster_mode < 0 || g_cluster_mode > 6) g_cluster_mode = 5;
+    if (g_cluster_mode < 0 || g_cluster_mode > 9) g_cluster_mode = 5;
   }
   return g_cluster_mode;
 }
@@ -783,7 +1075,12 @@ static int prepare_cluster_mode() {
 template <int N1, int N2, int C>
 static int prepare_cluster(FftPlan* p) {
   p->mode = cluster_mode();
+  // MODE 7-9: the warp-local 2^16 kernel (other sizes use MODE 5)
+  if (p->mode >= 7 && !(N1 == 256 && N2 == 256 && C == 16)) p->mode = 5;
   switch (p->mode) {
+    case 7: return prepare_warp65536<false, false>(&p->max_clusters);
+    case 8: return prepare_warp65536<true, false>(&p->max_clusters);
+    case 9: return prepare_warp65536<false, true>(&p->max_clusters);
     case 0: return prepare_cluster_mode<N1, N2, C, 0>();
     case 1: return prepare_cluster_mode<N1, N2, C, 1>();
     case 2: return prepare_cluster_mode<N1, N2, C, 2>();
@@ -803,6 +1100,11 @@ static int launch_cluster(const FftPlan* p, const float2* in, float2* out, int64
   if (p->mode == 4) return launch_pair<N1, N2, C>(in, out, batch, coarse, fine, s);
   if (p->mode == 5) return launch_rows<N1, N2, C, false>(in, out, batch, coarse, fine, s);
   if (p->mode == 6) return launch_rows<N1, N2, C, true>(in, out, batch, coarse, fine, s);
+  if constexpr (N1 == 256 && N2 == 256 && C == 16) {
+    if (p->mode == 7) return launch_warp65536<false, false>(in, out, batch, coarse, fine, 0, s);
+    if (p->mode == 8) return launch_warp65536<true, false>(in, out, batch, coarse, fine, 0, s);
+    if (p->mode == 9) return launch_warp65536<false, true>(in, out, batch, coarse, fine, p->max_clusters, s);
+  }
   auto kern = p->mode == 0   ? fft_cluster_kernel<N1, N2, C, 0>
               : p->mode == 1 ? fft_cluster_kernel<N1, N2, C, 1>
                              : fft_cluster_kernel<N1, N2, C, 2>;
@@ -871,12 +1173,15 @@ int fft1d_plan_init(FftPlan* p) {
     const int64_t nc = p->n1a > p->n2a ? p->n1a : p->n2a;
     if (upload_table(twiddle_table(nc, nc), &p->tw_a)) return DPP_ECUDA;
     if (upload_table(twiddle_table(n, n / nc), &p->tw_b)) return DPP_ECUDA;
-    static const char* modes[7] = {"push", "pull", "async", "persistent TMA + st.async",
-                                   "column pairs, TMA tile + st.async", "row layouts, TMA tile + st.async",
-                                   "row layouts, separate receive buffer"};
+    static const char* modes[10] = {"push", "pull", "async", "persistent TMA + st.async",
+                                    "column pairs, TMA tile + st.async", "row layouts, TMA tile + st.async",
+                                    "row layouts, separate receive buffer",
+                                    "warp-local passes, swizzled TMA tile in/out",
+                                    "warp-local passes, separate receive buffer",
+                                    "warp-local passes, persistent clusters"};
     snprintf(p->desc, sizeof(p->desc), "cluster<%lldx%lld, C=%d> four-step over DSMEM (%s%s)",
              (long long)p->n1a, (long long)p->n2a, p->cluster, modes[p->mode],
-             p->mode == 3 ? (std::string(", ") + std::to_string(p->max_clusters) + " clusters").c_str() : "");
+             (p->mode == 3 || p->mode == 9) ? (std::string(", ") + std::to_string(p->max_clusters) + " clusters").c_str() : "");
     return DPP_OK;
   }
   return fail(DPP_ENOTSUP, "1-D transform size 2^%d is above the 2^17 single-pass limit", lg);

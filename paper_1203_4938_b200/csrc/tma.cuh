@@ -11,9 +11,12 @@
 namespace dpp {
 
 // Row-major 2-D array of 8-byte elements (complex64): `rows` x `cols`,
-// boxes of box_rows x box_cols elements.
+// boxes of box_rows x box_cols elements; `swizzle` = the shared-memory layout
+// of the box (CU_TENSOR_MAP_SWIZZLE_128B: 16-byte chunk k of 128-byte row r
+// lands at chunk k ^ (r & 7), buffer 1024-byte aligned).
 inline int make_tmap_c64(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                         uint32_t box_rows, uint32_t box_cols) {
+                         uint32_t box_rows, uint32_t box_cols,
+                         CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -28,7 +31,7 @@ inline int make_tmap_c64(CUtensorMap* map, const void* base, uint64_t rows, uint
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides,
-                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DPP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DPP_OK;

@@ -205,3 +205,36 @@ def test_size_errors(cuda):
         ops.fft_forward(x, 16)
     with pytest.raises(PlanError):
         ops.fft_forward(torch.zeros(1 << 19, dtype=torch.complex64, device=cuda), 1 << 19)
+
+
+_MODE_CHECK = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+from conftest import complex_signals, rel_l2
+from oracle import fft_oracle as fo
+from paper_1203_4938_b200 import ops
+n = 65536
+x = complex_signals(11, (37, n))
+got = ops.fft_forward(torch.from_numpy(x).cuda(), n).cpu().numpy()
+ref = fo.fft_rows(x)
+print(max(rel_l2(g, r) for g, r in zip(got, ref)))
+"""
+
+
+@pytest.mark.parametrize("mode", [4, 6, 7, 8, 9])
+def test_2e16_exchange_variants(cuda, mode):
+    # the DSMEM exchange variants selectable by DPP_FFT_CLUSTER_MODE (read once
+    # per process, hence the subprocess); 37 transforms = a ragged persistent grid
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = _MODE_CHECK.format(root=str(root), tests=str(root / "tests"))
+    env = dict(os.environ, DPP_FFT_CLUSTER_MODE=str(mode))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= tol(65536)
