@@ -794,10 +794,16 @@ __device__ __forceinline__ int smid() {
 #endif
 
 namespace w16 {
-constexpr int N1 = 256, N2 = 256, N = N1 * N2, C = 16, W = 16, R = 16, THREADS = 256;
-constexpr int TILE = N1 * W;  // 4096 float2 = 32 KB
-template <bool SEP>
-constexpr size_t smem_bytes() { return 1024 + (size_t)(SEP ? 2 : 1) * TILE * 8 + 256 * 16; }
+constexpr int N1 = 256, N2 = 256, W = 16, R = 16;
+constexpr int TILE = N1 * W;  // one 256 x 16 sub-tile: 4096 float2 = 32 KB
+// cluster of CC CTAs: each CTA holds SUB = 16/CC sub-tiles (8 warps each)
+template <int CC>
+struct Shape {
+  static constexpr int SUB = 16 / CC, THREADS = 256 * SUB, W2 = 16 * SUB;
+  static constexpr int MINB = CC == 16 ? 4 : 2;
+};
+template <int CC, bool SEP>
+constexpr size_t smem_bytes() { return 1024 + (size_t)(SEP ? 2 : 1) * Shape<CC>::SUB * TILE * 8 + 256 * 16; }
 __device__ __forceinline__ uint32_t slot(int r, int c) {
   return (uint32_t)(r * 16 + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1));
 }
@@ -855,26 +861,30 @@ __device__ __forceinline__ void col256(float2 (&v)[R], const Lane& L, uint32_t t
 // buffer.  Measured slower (1.64 vs 1.39 ms): without a second tile buffer
 // the load latency is exposed every iteration and each cluster runs at the
 // pace of its busiest SM.  Kept as a documented variant.
-template <bool SEP, bool PERSIST>
-__global__ void __launch_bounds__(w16::THREADS, SEP ? 3 : 4)
+template <int CC, bool SEP, bool PERSIST>
+__global__ void __launch_bounds__(w16::Shape<CC>::THREADS, SEP ? (CC == 16 ? 3 : 1) : w16::Shape<CC>::MINB)
 fft_warp_65536(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                const float2* __restrict__ coarse_g, const float2* __restrict__ fine_g, int64_t batch) {
   static_assert(!(SEP && PERSIST), "the separate-receive variant runs one transform per cluster");
   using namespace w16;
+  constexpr int SUB = Shape<CC>::SUB;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t bars[2];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   float2* buf = reinterpret_cast<float2*>(smem_raw + pad);
-  float2* recv = SEP ? buf + TILE : buf;
-  float4* tw = reinterpret_cast<float4*>(buf + (SEP ? 2 : 1) * TILE);
+  float2* recv = SEP ? buf + SUB * TILE : buf;
+  float4* tw = reinterpret_cast<float4*>(buf + (SEP ? 2 : 1) * SUB * TILE);
 
   const int p = (int)cluster_ctarank();
-  const int64_t stride = PERSIST ? (int64_t)(gridDim.x / C) : batch;
-  int64_t t = blockIdx.x / C;
+  const int64_t stride = PERSIST ? (int64_t)(gridDim.x / CC) : batch;
+  int64_t t = blockIdx.x / CC;
   const int tid = threadIdx.x;
   const int w = tid >> 5, lane = tid & 31;
+  const int sub = w >> 3, wl = w & 7;  // sub-tile and warp within it
   const int par = (lane >> 3) & 1, j = (lane & 7) | ((lane >> 4) << 3);
-  const int col = 2 * w + par;
+  const int col = 2 * wl + par;        // column within the sub-tile
+  const uint32_t mybuf = smem_u32(buf) + (uint32_t)(sub * TILE * 8);
+  const uint32_t myrecv = smem_u32(recv) + (uint32_t)(sub * TILE * 8);
   PHASE(0)
   PHASE_EXTRA(8, smid())
   PHASE_EXTRA(9, gtimer())
@@ -883,18 +893,19 @@ fft_warp_65536(const __grid_constant__ CUtensorMap tin, const __grid_constant__ 
     mbar_init(&bars[1], 1);
     fence_mbar_init();
     if (t < batch) {
-      mbar_arrive_expect_tx(&bars[0], (uint32_t)(TILE * 8));
-      tma_load_2d(buf, &tin, p * W, (int)(t * N1), &bars[0]);
-      mbar_arrive_expect_tx(&bars[1], (uint32_t)(TILE * 8));
+      mbar_arrive_expect_tx(&bars[0], (uint32_t)(SUB * TILE * 8));
+#pragma unroll
+      for (int s = 0; s < SUB; ++s) tma_load_2d(buf + s * TILE, &tin, (p * SUB + s) * W, (int)(t * N1), &bars[0]);
+      mbar_arrive_expect_tx(&bars[1], (uint32_t)(SUB * TILE * 8));
     }
   }
-  {
+  if (tid < 256) {
     // stage-twiddle table: entry [jj][ii ^ (jj & 7)] = W_256^{ii*jj} as (w, i*w)
     const int jj = tid >> 4, ii = tid & 15;
     const float2 x = __ldg(coarse_g + ((ii * jj) & 255));
     tw[jj * 16 + (ii ^ (jj & 7))] = make_float4(x.x, x.y, -x.y, x.x);
   }
-  const int b = p * W + col;
+  const int b = (p * SUB + sub) * W + col;
   // four-step twiddle W_N^{b (j + 16 i)} = W_N^{bj} (W_N^{16b})^i from the
   // coarse W_256 x fine W_N tables, fetched before the tile wait
   const float2 w0 = cmul(__ldg(coarse_g + ((b * j) >> 8)), __ldg(fine_g + ((b * j) & 255)));
@@ -907,7 +918,7 @@ fft_warp_65536(const __grid_constant__ CUtensorMap tin, const __grid_constant__ 
     const uint32_t ph = k & 1;
     float2 v[R];
     {
-      const Lane L(smem_u32(buf), w, par, j);
+      const Lane L(mybuf, wl, par, j);
       mbar_wait(&bars[0], ph);
       PHASE(1)
 #pragma unroll
@@ -930,38 +941,42 @@ fft_warp_65536(const __grid_constant__ CUtensorMap tin, const __grid_constant__ 
     cluster_wait();
     PHASE(3)
     {
-      // Z[b][c = j + 16 i] belongs to CTA i, local column j, row rho(b)
+      // Z[b][c = j + 16 i] belongs to CTA i / SUB, sub-tile i % SUB, column j, row rho(b)
       const int rb = b ^ ((b & 1) << 2);
       const uint32_t scatter_off = smem_u32(recv) + 8u * slot(rb, j);
       const uint32_t rbar = smem_u32(&bars[1]);
 #pragma unroll
-      for (int i = 0; i < R; ++i) st_async_f2(mapa_u32(scatter_off, i), v[i], mapa_u32(rbar, i));
+      for (int i = 0; i < R; ++i)
+        st_async_f2(mapa_u32(scatter_off + (uint32_t)((i % SUB) * TILE * 8), i / SUB), v[i],
+                    mapa_u32(rbar, i / SUB));
     }
-    // pass 2: column c = 16 p + col over b = j + 16 i (received at row rho(b))
-    const Lane L(smem_u32(recv), w, par, j);
+    // pass 2: column c = W2 p + 16 sub + col over b = j + 16 i (received at row rho(b))
+    const Lane L(myrecv, wl, par, j);
     PHASE(4)
     const int jr = j ^ ((j & 1) << 2);
-    const uint32_t rrow = smem_u32(recv) + 8u * (uint32_t)(16 * jr + 2 * (w ^ (jr & 7)) + par);
+    const uint32_t rrow = myrecv + 8u * (uint32_t)(16 * jr + 2 * (wl ^ (jr & 7)) + par);
     mbar_wait(&bars[1], ph);
     PHASE(5)
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = lds2(rrow + 2048u * i);
     col256(v, L, twj, j);
     PHASE(6)
-    // X[c + 256 k2], k2 = j + 16 i: staged at row k2, column col; one TMA store
+    // X[c + 256 k2], k2 = j + 16 i: staged at row k2, column col; TMA tile stores
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < R; ++i) sts2(L.row + 2048u * i, v[i]);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      tma_store_2d(&tout, p * W, (int)(t * N2), recv);
+#pragma unroll
+      for (int s = 0; s < SUB; ++s) tma_store_2d(&tout, (p * SUB + s) * W, (int)(t * N2), recv + s * TILE);
       bulk_commit_and_wait_all();
       const int64_t tn = t + stride;
       if (tn < batch) {
-        mbar_arrive_expect_tx(&bars[0], (uint32_t)(TILE * 8));
-        tma_load_2d(buf, &tin, p * W, (int)(tn * N1), &bars[0]);
-        mbar_arrive_expect_tx(&bars[1], (uint32_t)(TILE * 8));
+        mbar_arrive_expect_tx(&bars[0], (uint32_t)(SUB * TILE * 8));
+#pragma unroll
+        for (int s = 0; s < SUB; ++s) tma_load_2d(buf + s * TILE, &tin, (p * SUB + s) * W, (int)(tn * N1), &bars[0]);
+        mbar_arrive_expect_tx(&bars[1], (uint32_t)(SUB * TILE * 8));
       }
       PHASE(7)
       PHASE_EXTRA(10, gtimer())
@@ -969,32 +984,32 @@ fft_warp_65536(const __grid_constant__ CUtensorMap tin, const __grid_constant__ 
   }
 }
 
-template <bool SEP, bool PERSIST>
+template <int CC, bool SEP, bool PERSIST>
 static int prepare_warp65536(int* max_clusters) {
-  auto kern = fft_warp_65536<SEP, PERSIST>;
+  auto kern = fft_warp_65536<CC, SEP, PERSIST>;
   DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)w16::smem_bytes<SEP>()));
-  DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                                      (int)w16::smem_bytes<CC, SEP>()));
+  if (CC > 8) DPP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   *max_clusters = 0;
   if (PERSIST) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(w16::C * 1024, 1, 1);
-    cfg.blockDim = dim3(w16::THREADS, 1, 1);
-    cfg.dynamicSmemBytes = w16::smem_bytes<SEP>();
+    cfg.gridDim = dim3(CC * 1024, 1, 1);
+    cfg.blockDim = dim3(w16::Shape<CC>::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = w16::smem_bytes<CC, SEP>();
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = w16::C;
+    attr[0].val.clusterDim.x = CC;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     DPP_CUDA_CHECK(cudaOccupancyMaxActiveClusters(max_clusters, kern, &cfg));
-    if (*max_clusters < 1) return fail(DPP_ECUDA, "no 16-CTA cluster of the 2^16 kernel fits on this device");
+    if (*max_clusters < 1) return fail(DPP_ECUDA, "no cluster of the 2^16 kernel fits on this device");
   }
   return DPP_OK;
 }
 
-template <bool SEP, bool PERSIST>
+template <int CC, bool SEP, bool PERSIST>
 static int launch_warp65536(const float2* in, float2* out, int64_t batch, const float2* coarse, const float2* fine,
                             int max_clusters, cudaStream_t s) {
   using namespace w16;
@@ -1005,18 +1020,18 @@ static int launch_warp65536(const float2* in, float2* out, int64_t batch, const 
   if (rc) return rc;
   const int64_t clusters = PERSIST ? (batch < max_clusters ? batch : max_clusters) : batch;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(clusters * C), 1, 1);
-  cfg.blockDim = dim3(THREADS, 1, 1);
-  cfg.dynamicSmemBytes = smem_bytes<SEP>();
+  cfg.gridDim = dim3((unsigned)(clusters * CC), 1, 1);
+  cfg.blockDim = dim3(Shape<CC>::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem_bytes<CC, SEP>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.x = CC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_warp_65536<SEP, PERSIST>, tin, tout, coarse, fine, batch));
+  DPP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fft_warp_65536<CC, SEP, PERSIST>, tin, tout, coarse, fine, batch));
   return DPP_OK;
 }
 
@@ -1076,11 +1091,13 @@ template <int N1, int N2, int C>
 static int prepare_cluster(FftPlan* p) {
   p->mode = cluster_mode();
   // MODE 7-9: the warp-local 2^16 kernel (other sizes use MODE 5)
-  if (p->mode >= 7 && !(N1 == 256 && N2 == 256 && C == 16)) p->mode = 5;
+  if (p->mode >= 7 && !(N1 == 256 && N2 == 256 && (C == 16 || C == 8))) p->mode = 5;
+  if constexpr (N1 == 256 && N2 == 256 && (C == 16 || C == 8)) {
+    if (p->mode == 7) return prepare_warp65536<C, false, false>(&p->max_clusters);
+    if (p->mode == 8) return prepare_warp65536<C, true, false>(&p->max_clusters);
+    if (p->mode == 9) return prepare_warp65536<C, false, true>(&p->max_clusters);
+  }
   switch (p->mode) {
-    case 7: return prepare_warp65536<false, false>(&p->max_clusters);
-    case 8: return prepare_warp65536<true, false>(&p->max_clusters);
-    case 9: return prepare_warp65536<false, true>(&p->max_clusters);
     case 0: return prepare_cluster_mode<N1, N2, C, 0>();
     case 1: return prepare_cluster_mode<N1, N2, C, 1>();
     case 2: return prepare_cluster_mode<N1, N2, C, 2>();
@@ -1100,10 +1117,10 @@ static int launch_cluster(const FftPlan* p, const float2* in, float2* out, int64
   if (p->mode == 4) return launch_pair<N1, N2, C>(in, out, batch, coarse, fine, s);
   if (p->mode == 5) return launch_rows<N1, N2, C, false>(in, out, batch, coarse, fine, s);
   if (p->mode == 6) return launch_rows<N1, N2, C, true>(in, out, batch, coarse, fine, s);
-  if constexpr (N1 == 256 && N2 == 256 && C == 16) {
-    if (p->mode == 7) return launch_warp65536<false, false>(in, out, batch, coarse, fine, 0, s);
-    if (p->mode == 8) return launch_warp65536<true, false>(in, out, batch, coarse, fine, 0, s);
-    if (p->mode == 9) return launch_warp65536<false, true>(in, out, batch, coarse, fine, p->max_clusters, s);
+  if constexpr (N1 == 256 && N2 == 256 && (C == 16 || C == 8)) {
+    if (p->mode == 7) return launch_warp65536<C, false, false>(in, out, batch, coarse, fine, 0, s);
+    if (p->mode == 8) return launch_warp65536<C, true, false>(in, out, batch, coarse, fine, 0, s);
+    if (p->mode == 9) return launch_warp65536<C, false, true>(in, out, batch, coarse, fine, p->max_clusters, s);
   }
   auto kern = p->mode == 0   ? fft_cluster_kernel<N1, N2, C, 0>
               : p->mode == 1 ? fft_cluster_kernel<N1, N2, C, 1>
