@@ -37,6 +37,14 @@ void fft_plan_release(FftPlan* p) {
   if (p->ctw_a) cudaFree(p->ctw_a);
   if (p->ctw_b) cudaFree(p->ctw_b);
   p->tw_a = p->tw_b = p->ctw_a = p->ctw_b = nullptr;
+  if (p->l2_tw) cudaFree(p->l2_tw);
+  if (p->l2_scratch) cudaFree(p->l2_scratch);
+  if (p->l2_ctrl) cudaFree(p->l2_ctrl);
+  if (p->l2_done) cudaEventDestroy(p->l2_done);
+  p->l2_tw = nullptr;
+  p->l2_scratch = nullptr;
+  p->l2_ctrl = nullptr;
+  p->l2_done = nullptr;
   if (p->rows) {
     fft_plan_release(p->rows);
     delete p->rows;

@@ -1162,6 +1162,17 @@ int fft1d_plan_init(FftPlan* p) {
     snprintf(p->desc, sizeof(p->desc), "small<%lld> radix-16 stockham, 1 CTA", (long long)n);
     return DPP_OK;
   }
+  if (n == 65536) {
+    const char* e = getenv("DPP_FFT_L2");
+    if (!e || atoi(e) != 0) {
+      p->kind = FftPlan::L2X;
+      if (int rc = fft65536_l2x_init(p)) return rc;
+      snprintf(p->desc, sizeof(p->desc),
+               "two-pass 256x256 four-step, L2-resident exchange (ring %d, lag %d), 32 KB SMEM transpose per item",
+               p->l2_ring, p->l2_lag);
+      return DPP_OK;
+    }
+  }
   if (lg <= 17) {
     // split n = N1 * N2 with N1 <= N2, cluster C so that each CTA holds <= 8192 points
     p->kind = FftPlan::CLUSTER;
@@ -1213,6 +1224,8 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
       SMALL_CASE(128) SMALL_CASE(256) SMALL_CASE(512) SMALL_CASE(1024) SMALL_CASE(2048) SMALL_CASE(4096)
 #undef SMALL_CASE
     }
+  } else if (p->kind == FftPlan::L2X) {
+    return fft65536_l2x_execute(p, in, out, batch, s);
   } else if (p->kind == FftPlan::CLUSTER) {
     switch (p->n0) {
       case 2048: return launch_cluster<32, 64, 1>(p, in, out, batch, s);

@@ -9,7 +9,7 @@ struct dpp_fft_plan;  // public opaque name (include/dpp_b200.h)
 namespace dpp {
 
 struct FftPlan {
-  enum Kind { SMALL = 1, CLUSTER = 2 };
+  enum Kind { SMALL = 1, CLUSTER = 2, L2X = 3 };
   int rank = 1;
   int64_t n0 = 0, n1 = 0, batch = 0;  // rank 1: n0 points; rank 2: n0 rows x n1 cols
   int device = 0;
@@ -29,6 +29,13 @@ struct FftPlan {
   int col_width = 0;         // columns per tile
   float2* ctw_a = nullptr;
   float2* ctw_b = nullptr;
+  // L2X (n = 2^16 two-pass, fft_l2.cu): scratch ring, ticket/counters, tables
+  int l2_lag = 0, l2_ring = 0;
+  float4* l2_tw = nullptr;
+  float2* l2_scratch = nullptr;
+  int* l2_ctrl = nullptr;
+  size_t l2_ctrl_bytes = 0;
+  cudaEvent_t l2_done = nullptr;
   char desc[256] = {0};
 };
 
@@ -38,6 +45,8 @@ int fft2d_plan_init(FftPlan* p);
 int fft2d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s);
 void fft_plan_release(FftPlan* p);
+int fft65536_l2x_init(FftPlan* p);
+int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
 
 }  // namespace dpp

@@ -44,7 +44,8 @@ def main() -> None:
         ms.append(e0.elapsed_time(e1))
     ms.sort()
     med = ms[len(ms) // 2]
-    peaks = json.loads((Path(__file__).resolve().parents[2] / "MEASURED_PEAKS.json").read_text())
+    pfile = Path(__file__).resolve().parents[2] / "MEASURED_PEAKS.json"
+    peaks = json.loads(pfile.read_text()) if pfile.exists() else {"hbm_fallback": 6650.0}
     hbm = None
     for k, v in peaks.items():
         if "hbm" in k.lower() and isinstance(v, (int, float)):
