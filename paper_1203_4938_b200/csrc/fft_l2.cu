@@ -392,6 +392,59 @@ struct Args {
   int batch, lag, ring;
 };
 
+
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+// v * (c + i s) for a compile-time rotation: FMUL2 with a broadcast scalar, then
+// FFMA2 on the swapped/negated pair (operand modifiers, no register pairs)
+__device__ __forceinline__ float2 cmulc(float2 v, float c, float s) {
+  return __ffma2_rn(make_float2(-v.y, v.x), make_float2(s, s), __fmul2_rn(v, make_float2(c, c)));
+}
+__device__ __forceinline__ void dft4c(float2& x0, float2& x1, float2& x2, float2& x3) {
+  float2 s02 = cadd(x0, x2), d02 = csub(x0, x2);
+  float2 s13 = cadd(x1, x3), d13 = csub(x1, x3);
+  d13 = make_float2(d13.y, -d13.x);  // * -i
+  x0 = cadd(s02, s13);
+  x2 = csub(s02, s13);
+  x1 = cadd(d02, d13);
+  x3 = csub(d02, d13);
+}
+// natural-order 16-point DFT (4 x 4), constant twiddles through cmulc
+__device__ __forceinline__ void dft16c(float2 (&v)[16]) {
+  dft4c(v[0], v[4], v[8], v[12]);
+  dft4c(v[1], v[5], v[9], v[13]);
+  dft4c(v[2], v[6], v[10], v[14]);
+  dft4c(v[3], v[7], v[11], v[15]);
+  const float c1 = 0.92387953251128676f, s1 = 0.38268343236508977f, h = 0.70710678118654752f;
+  v[5] = cmulc(v[5], c1, -s1);    // W16^1
+  v[9] = cmulc(v[9], h, -h);      // W16^2
+  v[13] = cmulc(v[13], s1, -c1);  // W16^3
+  v[6] = cmulc(v[6], h, -h);      // W16^2
+  v[10] = make_float2(v[10].y, -v[10].x);  // W16^4 = -i
+  v[14] = cmulc(v[14], -h, -h);   // W16^6
+  v[7] = cmulc(v[7], s1, -c1);    // W16^3
+  v[11] = cmulc(v[11], -h, -h);   // W16^6
+  v[15] = cmulc(v[15], -c1, s1);  // W16^9
+  float2 r[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    float2 a0 = v[4 * k1 + 0], a1 = v[4 * k1 + 1], a2 = v[4 * k1 + 2], a3 = v[4 * k1 + 3];
+    dft4c(a0, a1, a2, a3);
+    r[k1 + 0] = a0;
+    r[k1 + 4] = a1;
+    r[k1 + 8] = a2;
+    r[k1 + 12] = a3;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = r[i];
+}
+
 __device__ __forceinline__ int swz(int r, int c) { return r * 16 + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1); }
 
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
@@ -411,6 +464,40 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* tmap, int x, int y, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+      "{%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const void* tmap, int x, int y, const void* src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(tmap),
+               "r"(x), "r"(y), "r"(smem_u32(src)), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_l2_hint(float2* p, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
 
 template <int S, int MINB, bool DISCARD>
 __global__ void __launch_bounds__(THREADS, MINB)
@@ -444,6 +531,7 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
   if (warp == CW) {
     // ------------------------------------------------------------ producer
     if (lane != 0) return;
+    const uint64_t stream_pol = policy_evict_first();
     int head = 0, i = 0;
     auto publish = [&](int k) {
       const int s = k % S;
@@ -454,7 +542,7 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
         l2x::red_release_add(cnt1 + t, 1);
       } else {
         if (t + a.ring < a.batch) l2x::red_release_add(cnt2 + t, 1);  // lines discarded by the compute warps
-        tma_store_2d(&tout, 16 * g, t * 256, smem + s * TILE);
+        tma_store_2d_hint(&tout, 16 * g, t * 256, smem + s * TILE, stream_pol);
         bulk_commit();
       }
     };
@@ -465,7 +553,6 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
         publish(head);
         ++head;
       }
-      bulk_wait_read0();  // the stage's previous output tile has left shared memory
       const int tick = atomicAdd(a.ctrl, 1);
       if (tick >= total) {
         s_tick[s] = -1;
@@ -482,18 +569,19 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
             publish(head);
             ++head;
           } else {
-            __nanosleep(64);
+            __nanosleep(32);
           }
         }
       }
+      bulk_wait_read0();  // the stage's previous output tile has left shared memory
       s_tick[s] = tick;
       float2* buf = smem + s * TILE;
       mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
       if (pass == 1) {
-        tma_load_2d(buf, &tin, 16 * g, t * 256, &full[s]);
+        tma_load_2d_hint(buf, &tin, 16 * g, t * 256, &full[s], stream_pol);
       } else {
         l2x::fence_proxy_async_global();
-        bulk_g2s(buf, a.scratch + (size_t)(t % a.ring) * l2x::N + 4096 * g, TILE * sizeof(float2), &full[s]);
+        bulk_g2s(buf, a.scratch + (size_t)(t & (a.ring - 1)) * l2x::N + 4096 * g, TILE * sizeof(float2), &full[s]);
       }
     }
     while (head < i) {
@@ -506,9 +594,22 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
   }
 
   // -------------------------------------------------------------- compute
-  // a half-warp = 8 rows x 2 columns: 16 distinct 8-byte bank pairs
+  // a half-warp = 8 rows x 2 columns: 16 distinct 8-byte bank pairs.  All
+  // tile addresses are a per-thread base (+ an XOR pattern) + immediates:
+  //   tile rows r = 16 j + idx:        base + offA + 2048 j
+  //   exchange write (idx | k):        ((base + offW) ^ 144 (k&7)) + 1024 (k>>3)
+  //   exchange read  (k | idx):        ((base + offR) ^ 144 (k&7)) + 2048 k
+  // (derived from swz(); the XOR only touches address bits 4..9 and every
+  // stage is 1024-byte aligned).
   const int col = 2 * warp + (lane & 1);
   const int idx = lane >> 1;
+  const int q = idx & 7, p = lane & 1;
+  const uint32_t x9 = 16u * (uint32_t)((9 * q) ^ warp);
+  const uint32_t offA = 128u * idx + 16u * (uint32_t)(warp ^ q) + 8u * p;
+  const uint32_t offW = 2048u * idx + 8u * p + x9;
+  const uint32_t offR = 1024u * (idx >> 3) + 8u * p + x9;
+  const uint32_t sbase = smem_u32(smem);
+  const uint64_t keep_pol = policy_evict_last();
   float2 v[16];
   for (int i = 0;; ++i) {
     const int s = i % S;
@@ -518,42 +619,43 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
     int pass, t;
     l2x::decode(tick >> 4, a.batch, a.lag, pass, t);
     const int g = tick & 15;
-    float2* buf = smem + s * TILE;
+    const uint32_t b = sbase + (uint32_t)s * (TILE * 8);
+    float2* slot = a.scratch + (size_t)(t & (a.ring - 1)) * l2x::N;
     // the P2 block is in shared memory: drop its scratch lines (no HBM write-back)
-    if (DISCARD && pass == 2) l2x::discard_l2(a.scratch + (size_t)(t % a.ring) * l2x::N + 4096 * g + 16 * (tid & 255));
-    // stage A: rows 16 j + idx of column col
+    if (DISCARD && pass == 2) l2x::discard_l2(slot + 4096 * g + 16 * (tid & 255));
+    const uint32_t bA = b + offA;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = buf[swz(16 * j + idx, col)];
-    dft16(v);
+    for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
+    dft16c(v);
 #pragma unroll
     for (int k = 1; k < 16; ++k) v[k] = twmul(v[k], tw[16 * k + idx]);
     __syncwarp();
-    // exchange within the column: (row idx | k) -> (k | row idx)
+    const uint32_t bW = b + offW, bR = b + offR;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) buf[swz(16 * idx + (k ^ (idx & 7)), col)] = v[k];
+    for (int k = 0; k < 16; ++k) sts64((bW ^ (144u * (k & 7))) + 1024 * (k >> 3), v[k]);
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = buf[swz(16 * k + (idx ^ (k & 7)), col)];
-    dft16(v);
+    for (int k = 0; k < 16; ++k) v[k] = lds64((bR ^ (144u * (k & 7))) + 2048 * k);
+    dft16c(v);
     if (pass == 1) {
       // W_N^{b c}, b = 16 g + col, c = idx + 16 c1
-      const int b = 16 * g + col;
+      const int bb = 16 * g + col;
       float2 w = cmul(t4096[g * idx], t65536[col * idx]);
-      const float2 step = t4096[b];
+      const float2 step = t4096[bb];
       v[0] = cmul(v[0], w);
 #pragma unroll
       for (int c1 = 1; c1 < 16; ++c1) {
         w = cmul(w, step);
         v[c1] = cmul(v[c1], w);
       }
-      float2* dst = a.scratch + (size_t)(t % a.ring) * l2x::N + swz(b, idx);
+      float2* dst = slot + swz(bb, idx);
 #pragma unroll
-      for (int c1 = 0; c1 < 16; ++c1) l2x::st_l2(dst + 4096 * c1, v[c1]);
+      for (int c1 = 0; c1 < 16; ++c1) st_l2_hint(dst + 4096 * c1, v[c1], keep_pol);
     } else {
       __syncwarp();
       // output tile row d = idx + 16 d1, column col
 #pragma unroll
-      for (int d1 = 0; d1 < 16; ++d1) buf[swz(idx + 16 * d1, col)] = v[d1];
+      for (int d1 = 0; d1 < 16; ++d1) sts64(bA + 2048 * d1, v[d1]);
     }
     fence_proxy_async_smem();
     __syncwarp();
@@ -694,11 +796,16 @@ int fft65536_l2x_init(FftPlan* p) {
     if (g_l2_version == 3)
       if (int rc = l2w_prepare()) return rc;
   }
-  p->l2_lag = 40;
-  p->l2_ring = 96;
+  p->l2_lag = 48;
+  p->l2_ring = 128;
   if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e);
   if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e);
   if (p->l2_ring <= p->l2_lag) p->l2_ring = p->l2_lag + 1;
+  {  // a power of two (slot = t & (ring - 1))
+    int r = 1;
+    while (r < p->l2_ring) r <<= 1;
+    p->l2_ring = r;
+  }
   const auto t256 = rot_table(256, 256);
   const auto tn = rot_table(N, 4096);
   std::vector<float4> all(t256);
