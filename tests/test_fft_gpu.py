@@ -220,21 +220,52 @@ n = 65536
 x = complex_signals(11, (37, n))
 got = ops.fft_forward(torch.from_numpy(x).cuda(), n).cpu().numpy()
 ref = fo.fft_rows(x)
+xt = torch.from_numpy(x).cuda()
+ops.fft_forward(xt, n, out=xt)  # in place
+assert np.array_equal(xt.cpu().numpy(), got)
 print(max(rel_l2(g, r) for g, r in zip(got, ref)))
 """
 
 
-@pytest.mark.parametrize("mode", [4, 6, 7, 8, 9])
-def test_2e16_exchange_variants(cuda, mode):
-    # the DSMEM exchange variants selectable by DPP_FFT_CLUSTER_MODE (read once
-    # per process, hence the subprocess); 37 transforms = a ragged persistent grid
+_VARIANTS = [
+    # DSMEM cluster kernels (DPP_FFT_L2=0 selects them for 2^16)
+    *({"DPP_FFT_L2": "0", "DPP_FFT_CLUSTER_MODE": str(m)} for m in (4, 5, 6, 7, 8, 9)),
+    # L2-ring two-pass kernels: v1 (non-persistent), v2 (persistent, CTA barriers)
+    {"DPP_FFT_L2": "1"}, {"DPP_FFT_L2": "2"},
+    # v3 (default) with a 4-slot ring and lag 2, so slots are reused ~9 times
+    # per launch and both cross-CTA waits (P2 on P1, P1 on slot release) fire
+    {"DPP_FFT_L2_RING": "4", "DPP_FFT_L2_LAG": "2"},
+    {"DPP_FFT_L2_DISCARD": "0"}, {"DPP_FFT_L2_CFG": "1"},
+]
+
+
+@pytest.mark.parametrize("env", _VARIANTS, ids=lambda e: ",".join(f"{k[8:]}={v}" for k, v in e.items()))
+def test_2e16_kernel_variants(cuda, env):
+    # variant switches are read once per process, hence the subprocess;
+    # 37 transforms = a ragged persistent grid
     import os
     import subprocess
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     code = _MODE_CHECK.format(root=str(root), tests=str(root / "tests"))
-    env = dict(os.environ, DPP_FFT_CLUSTER_MODE=str(mode))
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= tol(65536)
+
+
+@pytest.mark.parametrize("n, rows", [(65536, 600), (1024, 70000)])
+def test_pinned_host_pipeline_matches_device(cuda, n, rows):
+    # apps.fft.fft_batch on pinned host tensors: chunked H2D / FFT / D2H on three
+    # streams (ragged last chunk) == the device-resident transform, bit for bit
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    from paper_1203_4938_b200.apps import fft as afft
+    g = torch.Generator().manual_seed(n + rows)
+    host = torch.randn((rows, n), dtype=torch.complex64, generator=g).pin_memory()
+    out = torch.empty_like(host).pin_memory()
+    afft.fft_batch(host, n, out=out)
+    ref = ops.fft_forward(host.to(cuda), n).cpu()
+    assert torch.equal(out, ref)
