@@ -610,6 +610,7 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
   const uint32_t offR = 1024u * (idx >> 3) + 8u * p + x9;
   const uint32_t sbase = smem_u32(smem);
   const uint64_t keep_pol = policy_evict_last();
+  const float2 w1 = make_float2(tw[16 + idx].x, tw[16 + idx].y);  // W256^idx
   float2 v[16];
   for (int i = 0;; ++i) {
     const int s = i % S;
@@ -627,8 +628,14 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
     dft16c(v);
+    float2 wk = w1;
 #pragma unroll
-    for (int k = 1; k < 16; ++k) v[k] = twmul(v[k], tw[16 * k + idx]);
+    for (int k = 1; k < 16; ++k) {
+      // W256^{idx k} by recurrence from the per-thread constant W256^idx: FMA-pipe
+      // work instead of 15 LDS.128 per item (shared memory is the busier pipe)
+      v[k] = cmul(v[k], wk);
+      wk = cmul(wk, w1);
+    }
     __syncwarp();
     const uint32_t bW = b + offW, bR = b + offR;
 #pragma unroll
