@@ -437,7 +437,7 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }  // namespace tc
 
 template <int CH>
-__global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs a, float delta_scale,
+__global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs a, int64_t batch, float delta_scale,
                                                                unsigned long long* ambiguous) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   uint8_t* sA = tsm;
@@ -448,26 +448,36 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t img = blockIdx.y;
-  const float* cbk = a.codebook + img * a.codebook_stride;
+  // Each CTA owns a contiguous range of the flat (image, tile) space, so the
+  // grid is one balanced wave for any batch; the codebook (B operand, norms,
+  // band) is restaged only when the range crosses into the next image.
+  auto stage_codebook = [&](int64_t img) {
+    const float* cbk = a.codebook + img * a.codebook_stride;
+    for (int e = tid; e < tc::NCB * 16; e += tc::THREADS) {
+      const int j = e >> 4, k = e & 15;
+      const float c = j < a.ncb ? cbk[j * 16 + k] : 0.f;
+      const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
+      *reinterpret_cast<float*>(sB + tc::off(j, k)) = hi;
+      *reinterpret_cast<float*>(sB + tc::off(j, 16 + k)) = __fsub_rn(c, hi);  // exact remainder
+    }
+    if (tid == 0) cmax_bits = 0;
+    __syncthreads();
+    for (int j = tid; j < tc::NCB; j += tc::THREADS) {
+      float s = 0.f;
+      if (j < a.ncb)
+        for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
+      scn[j] = j < a.ncb ? s : 1e30f;
+      if (j < a.ncb) atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
+    }
+  };
+  const int64_t nblocks = (a.width / 4) * (a.height / 4);
+  const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
+  const int64_t all_tiles = ntiles * batch;
+  const int64_t t_lo = all_tiles * blockIdx.x / gridDim.x, t_hi = all_tiles * (blockIdx.x + 1) / gridDim.x;
+  int64_t img = t_lo / ntiles;
+  stage_codebook(img);
 
-  // stage the codebook: tf32 hi/lo split (B operand), exact pair-order copy, norms
-  for (int e = tid; e < tc::NCB * 16; e += tc::THREADS) {
-    const int j = e >> 4, k = e & 15;
-    const float c = j < a.ncb ? cbk[j * 16 + k] : 0.f;
-    const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
-    *reinterpret_cast<float*>(sB + tc::off(j, k)) = hi;
-    *reinterpret_cast<float*>(sB + tc::off(j, 16 + k)) = __fsub_rn(c, hi);  // exact remainder
-  }
-  if (tid == 0) cmax_bits = 0;
-  __syncthreads();
-  for (int j = tid; j < tc::NCB; j += tc::THREADS) {
-    float s = 0.f;
-    if (j < a.ncb)
-      for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
-    scn[j] = j < a.ncb ? s : 1e30f;
-    if (j < a.ncb) atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
-  }
+
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -484,14 +494,24 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
   // band half-width: 1.5e-3 at |c| <= 4 (the normalised-block scale), growing
   // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
-  const float cmax = sqrtf(__uint_as_float(cmax_bits));
-  const float delta2 = 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
+  auto band = [&]() {
+    const float cmax = sqrtf(__uint_as_float(cmax_bits));
+    return 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
+  };
+  float delta2 = band();
 
-  const int64_t nblocks = (a.width / 4) * (a.height / 4);
-  const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
   uint32_t phase = 0;
   unsigned long long namb = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (int64_t ft = t_lo; ft < t_hi; ++ft) {
+    if (ft / ntiles != img) {  // next image: its codebook (the previous MMAs have completed)
+      img = ft / ntiles;
+      __syncthreads();
+      stage_codebook(img);
+      fence_proxy_async_smem();
+      __syncthreads();
+      delta2 = band();
+    }
+    const int64_t t = ft - img * ntiles;
     const int64_t k = t * tc::M + tid;
     const bool active = k < nblocks;
     float nb[16];
@@ -646,17 +666,16 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
     if (sm_count <= 0) sm_count = 148;
   }
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
-  int64_t per_image = (4 * (int64_t)sm_count + batch - 1) / batch;  // 4 resident CTAs per SM
-  if (per_image > ntiles) per_image = ntiles;
-  if (per_image < 1) per_image = 1;
-  dim3 grid((unsigned)per_image, (unsigned)batch);
+  const int64_t all_tiles = ntiles * batch;
+  const int64_t resident = 4 * (int64_t)sm_count;  // 4 CTAs per SM (SMEM, TMEM columns)
+  dim3 grid((unsigned)(all_tiles < resident ? all_tiles : resident));
   const size_t smem = tc::SMEM;
   switch (channels) {
 #define TC_CASE(CHN)                                                                                        \
   case CHN:                                                                                                 \
     DPP_CUDA_CHECK(cudaFuncSetAttribute(encode_tc_kernel<CHN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         (int)smem));                                                        \
-    encode_tc_kernel<CHN><<<grid, tc::THREADS, smem, s>>>(a, delta_scale, ambiguous);                       \
+    encode_tc_kernel<CHN><<<grid, tc::THREADS, smem, s>>>(a, batch, delta_scale, ambiguous);                       \
     break;
     TC_CASE(1)
     TC_CASE(3)
