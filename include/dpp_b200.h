@@ -15,7 +15,8 @@
  * Conventions
  *  - All data pointers are DEVICE pointers owned by the caller (PyTorch
  *    allocates).  No entry point allocates device memory except plan
- *    creation (twiddle tables, freed by *_destroy).
+ *    creation (twiddle tables; for n = 2^16 also the L2 exchange ring,
+ *    128 slots x 512 KB, and its counters), freed by *_destroy.
  *  - Every launch is asynchronous on `stream` (cudaStream_t; NULL = legacy).
  *  - Return 0 (DPP_OK) or an error code; dpp_last_error() returns the
  *    thread-local message of the last failure.  Host mapping:
@@ -24,6 +25,9 @@
  *      DPP_ENCCL   -> EngineRuntimeError (DeviceError)
  *  - Entry points are re-entrant; plans are immutable after creation and may
  *    be shared by threads (engine.py:292-317 runs chunks on thread pools).
+ *    Executions of one plan that owns an exchange ring are ordered on the
+ *    device (each launch waits on an event recorded by the previous one),
+ *    whatever streams the callers use.
  *  - Complex data is interleaved (re, im) binary32, exactly the reference's
  *    complex64 view (fft.py:160-163).
  */
@@ -68,7 +72,8 @@ int dpp_fft_plan_create(dpp_fft_plan** plan, int rank, int64_t n0, int64_t n1,
 /* Human-readable kernel schedule of a plan (for logs and bench lines). */
 int dpp_fft_plan_describe(const dpp_fft_plan* plan, char* buf, size_t len);
 
-/* Execute: in/out hold batch * n0 (* n1) complex64; in == out is allowed. */
+/* Execute: in/out hold batch * n0 (* n1) complex64; in == out is allowed.
+ * `workspace` is reserved (pass NULL): scratch is plan-owned. */
 int dpp_fft_c2c_forward(const dpp_fft_plan* plan, const float* in, float* out,
                         void* workspace, void* stream);
 
