@@ -231,15 +231,22 @@ int fft2d_plan_init(FftPlan* p) {
   p->rows->device = p->device;
   rc = fft1d_plan_init(p->rows);
   if (rc) return rc;
+  rc = fft2d_colring_init(p);
+  if (rc != DPP_OK && rc != DPP_ENOTSUP) return rc;
   char rows[200];
   snprintf(rows, sizeof(rows), "%s", p->rows->desc);
-  snprintf(p->desc, sizeof(p->desc), "rows: %s | columns: TMA cluster<%lldx%lld, C=%d, W=%d>", rows,
-           (long long)l1, (long long)l2, cl, width);
+  if (p->col_ring)
+    snprintf(p->desc, sizeof(p->desc), "rows: %s | columns: L2-ring four-step 256x%lld (ring %d, lag %d)", rows,
+             (long long)(n0 / 256), p->l2_ring, p->l2_lag);
+  else
+    snprintf(p->desc, sizeof(p->desc), "rows: %s | columns: TMA cluster<%lldx%lld, C=%d, W=%d>", rows,
+             (long long)l1, (long long)l2, cl, width);
   return DPP_OK;
 }
 
 int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s) {
   if (batch == 0) return DPP_OK;
+  if (p->col_ring) return fft2d_colring_execute(p, data, batch, s);
   if (p->n0 == 4096 && p->col_width == 32)
     return launch_columns<64, 64, 16, 32>(data, p->n1, batch, p->ctw_a, p->ctw_b, s);
   switch (p->n0) {

@@ -1,0 +1,391 @@
+// 2-D column pass through the L2 exchange ring (columns of R = 256 * B rows,
+// B = 16: 4096-row images, B = 64: 16384-row images).
+//
+// The column FFT of length R for a tile of 16 adjacent columns is a four-step
+// with r = 256 b + a (a < 256, b < B) and k = k1 + B k2:
+//   P1(u, g): rows r = 256 b + a for the A = 4096 / (16 B) values a in
+//             [A g, A g + A) and every b — one 3-D TMA box (16 x A x B) —
+//             B-point FFTs over b (B = 16: one sequence per thread, no
+//             exchange; B = 64: 4 lanes per sequence, one in-warp exchange),
+//             twiddle W_R^{a k1}, written to the ring slot of unit u as
+//             S[k1][a][16 columns] (128B-swizzled rows).
+//   P2(u, k1): the 32 KB block S[k1] by one bulk copy, 256-point FFTs over a
+//             (exactly the 1-D kernel's P2, csrc/fft_l2.cu), output rows
+//             k1 + B k2 by one 3-D TMA store (16 x 1 x 256).
+// A unit u is one (image, 16-column tile); P1 and P2 each have B items per
+// unit, ordered, published and waited for exactly like the 1-D kernel's
+// transforms (same producer / compute-warp structure, same deadlock argument).
+// In place: P2(u) writes unit u's columns only after every P1(u) has read them.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "fft_plan.cuh"
+#include "l2ring.cuh"
+#include "tma.cuh"
+
+namespace dpp {
+namespace colring {
+
+using namespace ring;
+
+constexpr int CW = 8;
+constexpr int THREADS = (CW + 1) * 32;
+constexpr int TILE = 4096;
+constexpr int S = 2;
+
+struct Args {
+  float2* scratch;
+  int* ctrl;
+  const float2* twr;   // W_R^m, m < R
+  const float4* tw256; // W256^m as (w, i*w), m < 256
+  int units, tiles_per_image, lag, ring;
+};
+
+// P1, B = 16: thread = one (column, a) sequence over b; no exchange
+__device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
+                                       const Args& a, uint64_t keep_pol) {
+  const int col = lane & 15, alo = 2 * warp + (lane >> 4);
+#pragma unroll
+  for (int bb = 0; bb < 16; ++bb) v[bb] = lds64(b + 8u * swz(16 * bb + alo, col));
+  dft16c(v);  // v[k1]
+  const int ar = 16 * g + alo;
+  const float2 wa = __ldg(a.twr + ar);  // W_R^a
+  float2 w = wa;
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) {
+    v[k1] = cmul(v[k1], w);
+    w = cmul(w, wa);
+  }
+  float2* dst = slot + swz(ar, col);
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) st_l2_hint(dst + 4096 * k1, v[k1], keep_pol);
+}
+
+// P1, B = 64: four lanes per (column, a) sequence; b = 4 b1 + b0 with b1 in
+// registers, k1 = m0 + 16 m1.  Exchange slot of (b0, m0): row 4 beta + a_lo,
+// beta = g(m0) ^ b0, g(m0) = 4 m0 | ((m0 >> 2) & 1): both the write (fixed m0)
+// and the read (fixed b0) give a half-warp 2 distinct row parities x 8 columns
+// = 16 distinct bank pairs.
+__device__ __forceinline__ int gbeta(int m0) { return (m0 << 2) | ((m0 >> 2) & 1); }
+
+__device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
+                                       const Args& a, uint64_t keep_pol) {
+  const int alo = warp >> 1, col = 8 * (warp & 1) + (lane & 7), b0 = lane >> 3;
+#pragma unroll
+  for (int b1 = 0; b1 < 16; ++b1) v[b1] = lds64(b + 8u * swz(16 * b1 + 4 * b0 + alo, col));
+  dft16c(v);  // v[m0]
+  {
+    const float2 wb = __ldg(a.twr + 256 * b0);  // W64^b0 = W_R^{256 b0}
+    float2 w = wb;
+#pragma unroll
+    for (int m0 = 1; m0 < 16; ++m0) {
+      v[m0] = cmul(v[m0], w);
+      w = cmul(w, wb);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int m0 = 0; m0 < 16; ++m0) sts64(b + 8u * swz(4 * (gbeta(m0) ^ b0) + alo, col), v[m0]);
+  __syncwarp();
+  const int j = b0;  // after the exchange this lane owns m0 = 4 j + i
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[4 * i + c] = lds64(b + 8u * swz(4 * (gbeta(4 * j + i) ^ c) + alo, col));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dft4c(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);  // v[4 i + m1]
+  // W_R^{a k1}, a = 4 g + a_lo, k1 = 4 j + i + 16 m1
+  const int ar = 4 * g + alo;
+  const float2 s1 = __ldg(a.twr + ar), s16 = __ldg(a.twr + 16 * ar);
+  float2 wi = __ldg(a.twr + 4 * ar * j);
+  float2* base = slot + swz(ar, col);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 w = wi;
+#pragma unroll
+    for (int m1 = 0; m1 < 4; ++m1) {
+      st_l2_hint(base + 4096 * (4 * j + i + 16 * m1), cmul(v[4 * i + m1], w), keep_pol);
+      w = cmul(w, s16);
+    }
+    wi = cmul(wi, s1);
+  }
+}
+
+template <int B, bool DISCARD>
+__global__ void __launch_bounds__(THREADS, 3)
+fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
+  constexpr int A = TILE / (16 * B);  // a values per P1 item
+  constexpr int LOGB = B == 16 ? 4 : 6;
+  extern __shared__ __align__(1024) float2 smem[];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(8) uint64_t done[S];
+  __shared__ int s_tick[S];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int total = 2 * B * a.units;
+  int* cnt1 = a.ctrl + 32;
+  int* cnt2 = cnt1 + a.units;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], CW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int R = 256 * B;
+
+  if (warp == CW) {
+    // ------------------------------------------------------------ producer
+    if (lane != 0) return;
+    const uint64_t stream_pol = policy_evict_first();
+    int head = 0, i = 0;
+    auto publish = [&](int k) {
+      const int s = k % S;
+      int pass, u;
+      decode(s_tick[s] >> LOGB, a.units, a.lag, pass, u);
+      const int g = s_tick[s] & (B - 1);
+      if (pass == 1) {
+        red_release_add(cnt1 + u, 1);
+      } else {
+        if (u + a.ring < a.units) red_release_add(cnt2 + u, 1);  // lines discarded by the compute warps
+        const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image;
+        tma_store_3d(&tout, 16 * ct, g, img * 256, smem + s * TILE);
+        bulk_commit();
+      }
+    };
+    for (;; ++i) {
+      const int s = i % S;
+      while (head <= i - S) {
+        mbar_wait(&done[head % S], (head / S) & 1);
+        publish(head);
+        ++head;
+      }
+      const int tick = atomicAdd(a.ctrl, 1);
+      if (tick >= total) {
+        s_tick[s] = -1;
+        mbar_arrive1(&full[s]);
+        break;
+      }
+      int pass, u;
+      decode(tick >> LOGB, a.units, a.lag, pass, u);
+      const int g = tick & (B - 1);
+      const int* dep = pass == 2 ? cnt1 + u : (u >= a.ring ? cnt2 + (u - a.ring) : nullptr);
+      if (dep) {
+        while (ld_acquire(dep) < B) {
+          if (head < i && mbar_try(&done[head % S], (head / S) & 1)) {
+            publish(head);
+            ++head;
+          } else {
+            __nanosleep(32);
+          }
+        }
+      }
+      bulk_wait_read0();
+      s_tick[s] = tick;
+      float2* buf = smem + s * TILE;
+      mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
+      if (pass == 1) {
+        const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image;
+        tma_load_3d(buf, &tin, 16 * ct, A * g, img * B, &full[s]);
+      } else {
+        fence_proxy_async_global();
+        bulk_g2s(buf, a.scratch + (size_t)(u & (a.ring - 1)) * (16 * R) + 4096 * g, TILE * sizeof(float2),
+                 &full[s]);
+      }
+    }
+    while (head < i) {
+      mbar_wait(&done[head % S], (head / S) & 1);
+      publish(head);
+      ++head;
+    }
+    bulk_wait0();
+    return;
+  }
+
+  // -------------------------------------------------------------- compute
+  // P2 = the 1-D kernel's P2 (warp w owns columns 2w, 2w+1; half-warp = 8 rows
+  // x 2 columns; XOR-immediate exchange addresses), see csrc/fft_l2.cu.
+  const int col = 2 * warp + (lane & 1);
+  const int idx = lane >> 1;
+  const int q = idx & 7, p = lane & 1;
+  const uint32_t x9 = 16u * (uint32_t)((9 * q) ^ warp);
+  const uint32_t offA = 128u * idx + 16u * (uint32_t)(warp ^ q) + 8u * p;
+  const uint32_t offW = 2048u * idx + 8u * p + x9;
+  const uint32_t offR = 1024u * (idx >> 3) + 8u * p + x9;
+  const uint32_t sbase = smem_u32(smem);
+  const uint64_t keep_pol = policy_evict_last();
+  const float4 t1 = __ldg(a.tw256 + idx);
+  const float2 w1 = make_float2(t1.x, t1.y);  // W256^idx
+  float2 v[16];
+  for (int i = 0;; ++i) {
+    const int s = i % S;
+    mbar_wait(&full[s], (i / S) & 1);
+    const int tick = s_tick[s];
+    if (tick < 0) break;
+    int pass, u;
+    decode(tick >> LOGB, a.units, a.lag, pass, u);
+    const int g = tick & (B - 1);
+    const uint32_t b = sbase + (uint32_t)s * (TILE * 8);
+    float2* slot = a.scratch + (size_t)(u & (a.ring - 1)) * (16 * R);
+    if (pass == 1) {
+      if constexpr (B == 16)
+        p1_b16(v, b, warp, lane, g, slot, a, keep_pol);
+      else
+        p1_b64(v, b, warp, lane, g, slot, a, keep_pol);
+    } else {
+      if (DISCARD) discard_l2(slot + 4096 * g + 16 * (tid & 255));
+      const uint32_t bA = b + offA;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
+      dft16c(v);
+      float2 wk = w1;
+#pragma unroll
+      for (int k = 1; k < 16; ++k) {
+        v[k] = cmul(v[k], wk);
+        wk = cmul(wk, w1);
+      }
+      __syncwarp();
+      const uint32_t bW = b + offW, bR = b + offR;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sts64((bW ^ (144u * (k & 7))) + 1024 * (k >> 3), v[k]);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = lds64((bR ^ (144u * (k & 7))) + 2048 * k);
+      dft16c(v);
+      __syncwarp();
+#pragma unroll
+      for (int d1 = 0; d1 < 16; ++d1) sts64(bA + 2048 * d1, v[d1]);  // output row k2 = idx + 16 d1
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&done[s]);
+  }
+}
+
+}  // namespace colring
+
+// ---------------------------------------------------------------------------
+// host side
+
+static int g_col_discard = -1;
+
+static size_t colring_smem() { return (size_t)colring::S * colring::TILE * sizeof(float2); }
+
+template <int B>
+static int colring_prepare(int* ctas) {
+  const size_t smem = colring_smem();
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  int per_sm = 0, dev = 0, sms = 0;
+  DPP_CUDA_CHECK(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, colring::fft_cols_l2w<B, true>, colring::THREADS, smem));
+  DPP_CUDA_CHECK(cudaGetDevice(&dev));
+  DPP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (per_sm < 1) return fail(DPP_ECUDA, "fft_cols_l2w does not fit on an SM");
+  *ctas = per_sm * sms;
+  return DPP_OK;
+}
+
+// Set up the column ring for an n0-row, n1-column rank-2 plan; returns
+// DPP_ENOTSUP (plan falls back to the cluster column kernel) when the shape
+// has no ring schedule.
+int fft2d_colring_init(FftPlan* p) {
+  const int64_t R = p->n0;
+  if (!(R == 4096 || R == 16384) || p->n1 % 16) return DPP_ENOTSUP;
+  if (const char* e = getenv("DPP_FFT_COLRING"))
+    if (atoi(e) == 0) return DPP_ENOTSUP;
+  if (g_col_discard < 0) {
+    const char* e = getenv("DPP_FFT_L2_DISCARD");
+    g_col_discard = e ? atoi(e) != 0 : 1;
+  }
+  const int B = (int)(R / 256);
+  int rc = B == 16 ? colring_prepare<16>(&p->col_ring_ctas) : colring_prepare<64>(&p->col_ring_ctas);
+  if (rc) return rc;
+  p->l2_lag = 768 / B;
+  if (const char* e = getenv("DPP_FFT_COL_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
+  int ring = 1;
+  while (ring < 2 * p->l2_lag + 8) ring <<= 1;
+  if (const char* e = getenv("DPP_FFT_COL_RING")) {
+    int r = 1;
+    while (r < atoi(e)) r <<= 1;
+    if (r > p->l2_lag) ring = r;
+  }
+  p->l2_ring = ring;
+  const int64_t units = p->batch * (p->n1 / 16);
+  if (units > 0x7fffffff / (2 * B)) return fail(DPP_EINVAL, "2-D batch too large for the column ring");
+  std::vector<float2> twr((size_t)R);
+  for (int64_t m = 0; m < R; ++m) {
+    const double ang = -2.0 * M_PI * (double)m / (double)R;
+    twr[(size_t)m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  std::vector<float4> t256(256);
+  for (int m = 0; m < 256; ++m) {
+    const double ang = -2.0 * M_PI * (double)m / 256.0;
+    const float c = (float)std::cos(ang), s = (float)std::sin(ang);
+    t256[(size_t)m] = make_float4(c, s, -s, c);
+  }
+  DPP_CUDA_CHECK(cudaMalloc(&p->l2_tw, 256 * sizeof(float4) + (size_t)R * sizeof(float2)));
+  DPP_CUDA_CHECK(cudaMemcpy(p->l2_tw, t256.data(), 256 * sizeof(float4), cudaMemcpyHostToDevice));
+  DPP_CUDA_CHECK(cudaMemcpy(reinterpret_cast<float2*>(p->l2_tw + 256), twr.data(), (size_t)R * sizeof(float2),
+                            cudaMemcpyHostToDevice));
+  DPP_CUDA_CHECK(cudaMalloc(&p->l2_scratch, (size_t)ring * 16 * R * sizeof(float2)));
+  p->l2_ctrl_bytes = (32 + 2 * (size_t)(units > 0 ? units : 1)) * sizeof(int);
+  DPP_CUDA_CHECK(cudaMalloc(&p->l2_ctrl, p->l2_ctrl_bytes));
+  DPP_CUDA_CHECK(cudaEventCreateWithFlags(&p->l2_done, cudaEventDisableTiming));
+  p->col_ring = 1;
+  return DPP_OK;
+}
+
+int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s) {
+  const int64_t R = p->n0, C = p->n1;
+  const int B = (int)(R / 256);
+  const int64_t units = batch * (C / 16);
+  if (units == 0) return DPP_OK;
+  CUtensorMap tin, tout;
+  {
+    const uint64_t dims[3] = {(uint64_t)C, 256, (uint64_t)(B * batch)};
+    const uint64_t strides[2] = {(uint64_t)C * 8, (uint64_t)C * 8 * 256};
+    const uint32_t box[3] = {16, (uint32_t)(colring::TILE / (16 * B)), (uint32_t)B};
+    if (int rc = make_tmap_c64_3d(&tin, data, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch)};
+    const uint64_t strides[2] = {(uint64_t)C * 8, (uint64_t)C * 8 * B};
+    const uint32_t box[3] = {16, 1, 256};
+    if (int rc = make_tmap_c64_3d(&tout, data, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  }
+  colring::Args a;
+  a.scratch = p->l2_scratch;
+  a.ctrl = p->l2_ctrl;
+  a.tw256 = p->l2_tw;
+  a.twr = reinterpret_cast<const float2*>(p->l2_tw + 256);
+  a.units = (int)units;
+  a.tiles_per_image = (int)(C / 16);
+  a.lag = (int)(units < p->l2_lag ? units : p->l2_lag);
+  a.ring = p->l2_ring;
+  DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
+  DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
+  const int64_t items = 2 * (int64_t)B * units;
+  const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
+  const size_t smem = colring_smem();
+  if (B == 16) {
+    if (g_col_discard)
+      colring::fft_cols_l2w<16, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    else
+      colring::fft_cols_l2w<16, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  } else {
+    if (g_col_discard)
+      colring::fft_cols_l2w<64, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    else
+      colring::fft_cols_l2w<64, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  }
+  DPP_LAUNCH_CHECK("fft_cols_l2w");
+  DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
+  return DPP_OK;
+}
+
+}  // namespace dpp

@@ -40,7 +40,7 @@ inline int make_tmap_c64(CUtensorMap* map, const void* base, uint64_t rows, uint
 // 3-D view of 8-byte elements: dims {d0 (inner), d1, d2}, byte strides
 // {s1, s2} for dims 1 and 2, box {b0, b1, b2}.
 inline int make_tmap_c64_3d(CUtensorMap* map, const void* base, const uint64_t dims[3], const uint64_t strides[2],
-                            const uint32_t box[3]) {
+                            const uint32_t box[3], CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -55,7 +55,7 @@ inline int make_tmap_c64_3d(CUtensorMap* map, const void* base, const uint64_t d
   const cuuint32_t bx[3] = {box[0], box[1], box[2]};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), d, st, bx, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DPP_ECUDA, "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
   return DPP_OK;

@@ -269,3 +269,43 @@ def test_pinned_host_pipeline_matches_device(cuda, n, rows):
     afft.fft_batch(host, n, out=out)
     ref = ops.fft_forward(host.to(cuda), n).cpu()
     assert torch.equal(out, ref)
+
+
+_COL_CHECK = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+from conftest import complex_signals, rel_l2
+from paper_1203_4938_b200 import ops
+worst = 0.0
+for (r, c, b) in ((4096, 64, 5), (16384, 32, 3)):
+    x = complex_signals(r + c, (b, r, c))
+    xt = torch.from_numpy(x).cuda()
+    got = ops.fft2d_forward(xt, r, c).cpu().numpy()
+    ops.fft2d_forward(xt, r, c, out=xt)
+    assert np.array_equal(xt.cpu().numpy(), got)
+    ref = np.fft.fft2(x.astype(np.complex128), axes=(-2, -1))
+    worst = max(worst, max(rel_l2(g, f) for g, f in zip(got, ref)) / np.log2(r * c))
+print(worst)
+"""
+
+
+@pytest.mark.parametrize("env", [{"DPP_FFT_COL_RING": "4", "DPP_FFT_COL_LAG": "2"}, {"DPP_FFT_L2_DISCARD": "0"},
+                                 {"DPP_FFT_COLRING": "0"}],
+                         ids=["ring4-lag2", "no-discard", "cluster-columns"])
+def test_2d_column_pass_variants(cuda, env):
+    # the L2-ring column pass (4096- and 16384-row images) with a 4-slot ring
+    # (every slot reused, both waits fire), without L2 discards, and the
+    # cluster column kernel it replaced; in place == out of place, numpy fft2
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = _COL_CHECK.format(root=str(root), tests=str(root / "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= 1e-5
