@@ -1201,6 +1201,17 @@ int fft1d_plan_init(FftPlan* p) {
     const int64_t nc = p->n1a > p->n2a ? p->n1a : p->n2a;
     if (upload_table(twiddle_table(nc, nc), &p->tw_a)) return DPP_ECUDA;
     if (upload_table(twiddle_table(n, n / nc), &p->tw_b)) return DPP_ECUDA;
+    if (n == 16384) {
+      const char* e = getenv("DPP_FFT_L2");
+      if (!e || atoi(e) != 0) {
+        if (int rc2 = fft16k_l2_init(p)) return rc2;
+        p->ring16k = 1;
+        snprintf(p->desc, sizeof(p->desc),
+                 "two-pass 256x64 four-step, L2-resident exchange (ring %d, lag %d), units of 4 transforms",
+                 p->l2_ring, p->l2_lag);
+        return DPP_OK;
+      }
+    }
     static const char* modes[10] = {"push", "pull", "async", "persistent TMA + st.async",
                                     "column pairs, TMA tile + st.async", "row layouts, TMA tile + st.async",
                                     "row layouts, separate receive buffer",
@@ -1227,6 +1238,12 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
   } else if (p->kind == FftPlan::L2X) {
     return fft65536_l2x_execute(p, in, out, batch, s);
   } else if (p->kind == FftPlan::CLUSTER) {
+    if (p->ring16k) {
+      const int64_t main = batch & ~int64_t(3);
+      if (int rc = fft16k_l2_execute(p, in, out, main, s)) return rc;
+      if (main == batch) return DPP_OK;
+      return launch_cluster<128, 128, 2>(p, in + main * 16384, out + main * 16384, batch - main, s);
+    }
     switch (p->n0) {
       case 2048: return launch_cluster<32, 64, 1>(p, in, out, batch, s);
       case 4096: return launch_cluster<64, 64, 1>(p, in, out, batch, s);

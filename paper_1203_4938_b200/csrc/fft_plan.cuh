@@ -38,6 +38,8 @@ struct FftPlan {
   cudaEvent_t l2_done = nullptr;
   // rank 2: column pass through the L2 ring (fft2d_l2.cu) instead of the cluster kernel
   int col_ring = 0, col_ring_ctas = 0;
+  // rank 1, n = 2^14: L2-ring kernel for batches of 4 (fft16k_l2.cu), cluster kernel for the rest
+  int ring16k = 0;
   char desc[256] = {0};
 };
 
@@ -51,6 +53,8 @@ int fft65536_l2x_init(FftPlan* p);
 int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_colring_init(FftPlan* p);
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s);
+int fft16k_l2_init(FftPlan* p);
+int fft16k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
 
 }  // namespace dpp

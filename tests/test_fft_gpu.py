@@ -216,7 +216,7 @@ sys.path.insert(0, {tests!r})
 from conftest import complex_signals, rel_l2
 from oracle import fft_oracle as fo
 from paper_1203_4938_b200 import ops
-n = 65536
+n = {n}
 x = complex_signals(11, (37, n))
 got = ops.fft_forward(torch.from_numpy(x).cuda(), n).cpu().numpy()
 ref = fo.fft_rows(x)
@@ -241,6 +241,18 @@ _VARIANTS = [
 
 @pytest.mark.parametrize("env", _VARIANTS, ids=lambda e: ",".join(f"{k[8:]}={v}" for k, v in e.items()))
 def test_2e16_kernel_variants(cuda, env):
+    _run_variant(env, 65536)
+
+
+@pytest.mark.parametrize("env", [{}, {"DPP_FFT_L2_RING": "4", "DPP_FFT_L2_LAG": "2"}, {"DPP_FFT_L2": "0"}],
+                         ids=["default", "ring4-lag2", "cluster"])
+def test_2e14_kernel_variants(cuda, env):
+    # n = 2^14: the L2-ring kernel runs units of 4 transforms (36 of the 37
+    # here) and the cluster kernel the remainder; DPP_FFT_L2=0 is cluster-only
+    _run_variant(env, 16384)
+
+
+def _run_variant(env, n):
     # variant switches are read once per process, hence the subprocess;
     # 37 transforms = a ragged persistent grid
     import os
@@ -248,11 +260,11 @@ def test_2e16_kernel_variants(cuda, env):
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
-    code = _MODE_CHECK.format(root=str(root), tests=str(root / "tests"))
+    code = _MODE_CHECK.format(root=str(root), tests=str(root / "tests"), n=n)
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
-    assert float(r.stdout.strip().splitlines()[-1]) <= tol(65536)
+    assert float(r.stdout.strip().splitlines()[-1]) <= tol(n)
 
 
 @pytest.mark.parametrize("n, rows", [(65536, 600), (1024, 70000)])
