@@ -1201,6 +1201,16 @@ int fft1d_plan_init(FftPlan* p) {
     const int64_t nc = p->n1a > p->n2a ? p->n1a : p->n2a;
     if (upload_table(twiddle_table(nc, nc), &p->tw_a)) return DPP_ECUDA;
     if (upload_table(twiddle_table(n, n / nc), &p->tw_b)) return DPP_ECUDA;
+    if (n == 4096) {
+      const char* e = getenv("DPP_FFT_WS4K");
+      if (!e || atoi(e) != 0) {
+        if (int rc2 = fft4096_ws_init(p)) return rc2;
+        p->ws4k = 1;
+        snprintf(p->desc, sizeof(p->desc),
+                 "256x16 in one CTA, warp-specialised TMA pipeline (2 stages, P1 warp-local, P2 in-thread)");
+        return DPP_OK;
+      }
+    }
     if (n == 16384) {
       const char* e = getenv("DPP_FFT_L2");
       if (!e || atoi(e) != 0) {
@@ -1238,6 +1248,7 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
   } else if (p->kind == FftPlan::L2X) {
     return fft65536_l2x_execute(p, in, out, batch, s);
   } else if (p->kind == FftPlan::CLUSTER) {
+    if (p->ws4k) return fft4096_ws_execute(p, in, out, batch, s);
     if (p->ring16k) {
       const int64_t main = batch & ~int64_t(3);
       if (int rc = fft16k_l2_execute(p, in, out, main, s)) return rc;

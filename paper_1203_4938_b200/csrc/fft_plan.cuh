@@ -40,6 +40,8 @@ struct FftPlan {
   int col_ring = 0, col_ring_ctas = 0;
   // rank 1, n = 2^14: L2-ring kernel for batches of 4 (fft16k_l2.cu), cluster kernel for the rest
   int ring16k = 0;
+  // rank 1, n = 4096: warp-specialised single-CTA kernel (fft4k.cu)
+  int ws4k = 0;
   char desc[256] = {0};
 };
 
@@ -55,6 +57,8 @@ int fft2d_colring_init(FftPlan* p);
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s);
 int fft16k_l2_init(FftPlan* p);
 int fft16k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
+int fft4096_ws_init(FftPlan* p);
+int fft4096_ws_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
 
 }  // namespace dpp
