@@ -565,6 +565,12 @@ static int l2p_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
 }
 
 
+#ifndef DPP_L2W_S
+#define DPP_L2W_S 2  // default schedule: stages per CTA
+#endif
+#ifndef DPP_L2W_MINB
+#define DPP_L2W_MINB 3  // and CTAs per SM
+#endif
 static int g_l2w_cfg = 0;  // 0: S=2 x 3 CTAs/SM, 1: S=3 x 2 CTAs/SM
 static int g_l2w_ctas = 0;
 
@@ -579,17 +585,17 @@ static size_t l2w_smem(int S) { return (size_t)S * l2x::l2w::TILE * sizeof(float
 
 static int l2w_prepare() {
   if (const char* e = getenv("DPP_FFT_L2_CFG")) g_l2w_cfg = atoi(e) == 1 ? 1 : 0;
-  const int S = g_l2w_cfg ? 3 : 2;
+  const int S = g_l2w_cfg ? 3 : DPP_L2W_S;
   const size_t smem = l2w_smem(S);
   int rc = g_l2w_cfg ? (l2w_prepare_one<3, 2, true>(smem) || l2w_prepare_one<3, 2, false>(smem))
-                     : (l2w_prepare_one<2, 3, true>(smem) || l2w_prepare_one<2, 3, false>(smem));
+                     : (l2w_prepare_one<DPP_L2W_S, DPP_L2W_MINB, true>(smem) || l2w_prepare_one<DPP_L2W_S, DPP_L2W_MINB, false>(smem));
   if (rc) return DPP_ECUDA;
   int per_sm = 0, dev = 0, sms = 0;
   if (g_l2w_cfg)
     DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2x::l2w::fft65536_l2w<3, 2, true>,
                                                                  l2x::l2w::THREADS, smem));
   else
-    DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2x::l2w::fft65536_l2w<2, 3, true>,
+    DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, true>,
                                                                  l2x::l2w::THREADS, smem));
   DPP_CUDA_CHECK(cudaGetDevice(&dev));
   DPP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -613,14 +619,14 @@ static int l2w_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
   a.ring = p->l2_ring;
   const int64_t items = 2 * l2x::ITEMS * batch;
   const unsigned grid = (unsigned)(items < g_l2w_ctas ? items : g_l2w_ctas);
-  const int S = g_l2w_cfg ? 3 : 2;
+  const int S = g_l2w_cfg ? 3 : DPP_L2W_S;
   const size_t smem = l2w_smem(S);
   if (g_l2w_cfg) {
     if (g_discard) l2x::l2w::fft65536_l2w<3, 2, true><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
     else l2x::l2w::fft65536_l2w<3, 2, false><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
   } else {
-    if (g_discard) l2x::l2w::fft65536_l2w<2, 3, true><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
-    else l2x::l2w::fft65536_l2w<2, 3, false><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
+    if (g_discard) l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, true><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
+    else l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, false><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
   }
   DPP_LAUNCH_CHECK("fft65536_l2w");
   return DPP_OK;

@@ -473,7 +473,16 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   const int64_t nblocks = (a.width / 4) * (a.height / 4);
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
   const int64_t all_tiles = ntiles * batch;
-  const int64_t t_lo = all_tiles * blockIdx.x / gridDim.x, t_hi = all_tiles * (blockIdx.x + 1) / gridDim.x;
+#ifndef DPP_TC_CONTIG
+#define DPP_TC_CONTIG 0
+#endif
+  // DPP_TC_CONTIG: each CTA a contiguous range of the flat tile space (one
+  // codebook stage per image boundary); default: grid-stride over the flat
+  // space (neighbouring CTAs on neighbouring tiles, codebook restaged when a
+  // CTA's stride crosses into the next image)
+  const int64_t t_lo = DPP_TC_CONTIG ? all_tiles * blockIdx.x / gridDim.x : blockIdx.x;
+  const int64_t t_hi = DPP_TC_CONTIG ? all_tiles * (blockIdx.x + 1) / gridDim.x : all_tiles;
+  const int64_t t_step = DPP_TC_CONTIG ? 1 : gridDim.x;
   int64_t img = t_lo / ntiles;
   stage_codebook(img);
 
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
 
   uint32_t phase = 0;
   unsigned long long namb = 0;
-  for (int64_t ft = t_lo; ft < t_hi; ++ft) {
+  for (int64_t ft = t_lo; ft < t_hi; ft += t_step) {
     if (ft / ntiles != img) {  // next image: its codebook (the previous MMAs have completed)
       img = ft / ntiles;
       __syncthreads();
