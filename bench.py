@@ -354,6 +354,23 @@ def run_ours(args) -> None:
               "mpixel_s": round(world * nimg * side * side / (ms_chain / 1e3) / 1e6, 1)}
     del imgs, cbs
 
+    # secondary: C1 — one N=1024 signal through the graph API (numpy in/out:
+    # H2D, the fft1024 node, D2H), latency; the reference's fft() takes 8.35 ms
+    # here, mostly plan/compile
+    rng = np.random.default_rng(42)
+    x1 = (rng.standard_normal(1024) + 1j * rng.standard_normal(1024)).astype(np.complex64)
+    for _ in range(5):
+        afft.fft(x1)
+    lat = []
+    for _ in range(50):
+        t0 = time.perf_counter()
+        afft.fft(x1)
+        lat.append((time.perf_counter() - t0) * 1e3)
+    lat.sort()
+    c1 = {"metric": "C1 latency (ms, lower is better)", "config": "fft(x), N=1024, numpy complex64 in/out through "
+                                                                   "the fft1024 graph node (configs[0])",
+          "median_ms": round(lat[len(lat) // 2], 4), "p10_ms": round(lat[len(lat) // 10], 4)}
+
     if rank == 0:
         cpu = cpu_baseline(len(os.sched_getaffinity(0)), seconds=10.0) if world == 1 and not args.no_cpu \
             else None
@@ -375,7 +392,7 @@ def run_ours(args) -> None:
                     "api": "apps.fft.fft_batch(pinned host tensor)"},
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
-            "secondary": {"compression_c4": compression, "fft2d_c3": fft2d, "chain_c5": chain5},
+            "secondary": {"c1_latency": c1, "compression_c4": compression, "fft2d_c3": fft2d, "chain_c5": chain5},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
