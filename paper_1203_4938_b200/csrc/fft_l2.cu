@@ -337,7 +337,10 @@ struct Args {
 };
 
 
-template <int S, int MINB, bool DISCARD>
+#ifndef DPP_L2_PF
+#define DPP_L2_PF 0  // L2 prefetch distance in item-times (measured: no gain, profiles/r1_fft_l2.md)
+#endif
+template <int S, int MINB, bool DISCARD, int PF = DPP_L2_PF>
 __global__ void __launch_bounds__(THREADS, MINB)
 fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
   extern __shared__ __align__(1024) float2 smem[];
@@ -400,6 +403,17 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
       int pass, t;
       l2x::decode(tick >> 4, a.batch, a.lag, pass, t);
       const int g = tick & 15;
+      if (PF > 0) {
+        // tickets are consumed at ~gridDim.x per item time: warm L2 with the P1
+        // tile PF item-times ahead (whichever CTA takes that ticket then loads
+        // it from L2 instead of HBM; P2 blocks are in L2 already)
+        const int ft = tick + PF * (int)gridDim.x;
+        if (ft < total) {
+          int fp, fu;
+          l2x::decode(ft >> 4, a.batch, a.lag, fp, fu);
+          if (fp == 1) tma_prefetch_2d(&tin, 16 * (ft & 15), fu * 256);
+        }
+      }
       const int* dep = pass == 2 ? cnt1 + t : (t >= a.ring ? cnt2 + (t - a.ring) : nullptr);
       if (dep) {
         while (l2x::ld_acquire(dep) < l2x::ITEMS) {
