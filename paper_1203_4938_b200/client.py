@@ -16,6 +16,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from .errors import ClientError
 from .model import as_program, free_points
 from .types import Direction
@@ -33,6 +35,10 @@ class CudaBackend:
     parallelism / pool: accepted for signature compatibility with
       LocalBackend (client.py:29-35); the device engine pipelines on streams.
     outputs: "host" (StreamFile, default) or "device" (DeviceStream).
+    max_in_flight: chunks in flight when host streams are chunked (the
+      reference's run_stream knob, engine.py:255): with a chunk size set and
+      host inputs/outputs, chunk c+1's H2D, chunk c's kernels and chunk c-1's
+      D2H run concurrently on three CUDA streams over this many device slots.
     """
 
     parallelism: int = 1
@@ -41,6 +47,7 @@ class CudaBackend:
     device: object = None
     stream: object = None
     outputs: str = "host"
+    max_in_flight: int = 3
 
 
 LocalBackend = CudaBackend
@@ -82,17 +89,27 @@ def run(backend: CudaBackend | None, program, inputs: dict) -> dict:
         if isinstance(sf, DeviceStream):
             arrays[name] = sf.tensor if sf.tensor.device == dev else sf.tensor.to(dev)
         elif isinstance(sf, StreamFile):
-            arrays[name] = to_device(sf.values, dev)
+            arrays[name] = sf.values if (p.chunk_size is not None and backend.outputs == "host"
+                                         and backend.max_in_flight > 1 and backend.stream is None
+                                         and name not in p.broadcast) else to_device(sf.values, dev)
         else:
             raise ClientError(f"stream {name!r}: expected StreamFile or DeviceStream")
     if len(counts) > 1:
         raise ClientError(f"input streams disagree on element count: {sorted(counts)}")
+    host_in = {name for name, sf in ((n, inputs[n]) for n in free_in) if isinstance(sf, StreamFile)}
+    total = counts.pop() if counts else 0
+    if (p.chunk_size is not None and host_in and backend.outputs == "host" and backend.max_in_flight > 1
+            and total > p.chunk_size and backend.stream is None):
+        return _run_pipelined(p, inputs, host_in, arrays, total, backend.max_in_flight)
     parts: dict[str, list] = {fp.stream: [] for fp in p.free_outputs}
 
     def collect(chunk):
         for name, buf in chunk.buffers.items():
             parts[name].append(buf)
 
+    for name in host_in:  # not pipelined after all: stage whole streams
+        if not isinstance(arrays[name], torch.Tensor):
+            arrays[name] = to_device(arrays[name], dev)
     stream = backend.stream
     with torch.cuda.device(dev):
         run_stream(p, chunk_arrays(p, arrays), writer=collect, workers=backend.parallelism,
@@ -106,3 +123,103 @@ def run(backend: CudaBackend | None, program, inputs: dict) -> dict:
             out[fp.stream] = DeviceStream(fp.data, t) if backend.outputs == "device" else \
                 StreamFile(fp.data, t.cpu().numpy())
     return out
+
+
+def _copy_parallel(dst, src, pool) -> None:
+    """numpy -> pinned staging with several threads (numpy releases the GIL)."""
+    n = src.size
+    parts = 8 if n >= (1 << 22) else 1
+    step = (n + parts - 1) // parts
+    futs = [pool.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
+_POOL = None
+
+
+def _run_pipelined(p, inputs: dict, host_in: set, arrays: dict, total: int, slots: int) -> dict:
+    """Chunked host streams: H2D / kernels / D2H of consecutive chunks overlap.
+
+    Each chunk of a host input is copied (8 threads) into a page-locked
+    staging slot and sent H2D asynchronously; free outputs land, chunk by
+    chunk, in one page-locked host buffer per stream.  Staging and device
+    slots are reused round robin once their chunk's copy / kernels are done.
+    Results are identical to the one-stream path (same kernels, same chunks)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from fractions import Fraction
+
+    from ._torch import torch_dtype
+    from .executor import Chunk, run_chunk
+
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(8)
+    dev = p.device
+    w = p.chunk_size
+    nchunks = (total + w - 1) // w
+    nslot = min(slots, nchunks)
+    widths = {fp.stream: fp.data.width for fp in p.free_inputs}
+    host_np = {name: np.ascontiguousarray(arrays[name]).reshape(-1) for name in host_in}
+    stage = [{name: torch.empty(w * widths[name], dtype=torch.from_numpy(host_np[name][:1]).dtype, pin_memory=True)
+              for name in host_in} for _ in range(nslot)]
+    dev_slots = [{name: torch.empty(w * widths[name], dtype=stage[0][name].dtype, device=dev) for name in host_in}
+                 for _ in range(nslot)]
+    staged = [None] * nslot   # H2D of the slot's last chunk done (staging reusable)
+    ran = [None] * nslot      # kernels of the slot's last chunk done (device slot reusable)
+    out_host, out_off = {}, {fp.stream: 0 for fp in p.free_outputs}
+    s_h2d, s_run, s_d2h = (torch.cuda.Stream(dev) for _ in range(3))
+    s_h2d.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.device(dev):
+        for index in range(nchunks):
+            lo, hi = index * w, min((index + 1) * w, total)
+            k = index % nslot
+            if staged[k] is not None:
+                staged[k].synchronize()  # the CPU is about to overwrite this staging slot
+            bufs, cnts = {}, {}
+            for name in host_in:
+                wd = widths[name]
+                _copy_parallel(stage[k][name].numpy()[:(hi - lo) * wd], host_np[name][lo * wd:hi * wd], _POOL)
+            if ran[k] is not None:
+                s_h2d.wait_event(ran[k])
+            with torch.cuda.stream(s_h2d):
+                for fp in p.free_inputs:
+                    name, wd = fp.stream, widths[fp.stream]
+                    if name in p.broadcast:
+                        bufs[name] = arrays[name]
+                        continue
+                    if name in host_in:
+                        dst = dev_slots[k][name][:(hi - lo) * wd]
+                        dst.copy_(stage[k][name][:(hi - lo) * wd], non_blocking=True)
+                        bufs[name] = dst
+                    else:
+                        bufs[name] = arrays[name][lo * wd:hi * wd]
+                    cnts[name] = hi - lo
+                ev = torch.cuda.Event()
+                ev.record(s_h2d)
+                staged[k] = ev
+            s_run.wait_event(ev)
+            with torch.cuda.stream(s_run):
+                out = run_chunk(p, Chunk(index, bufs, cnts), s_run)
+                ev = torch.cuda.Event()
+                ev.record(s_run)
+                ran[k] = ev
+            s_d2h.wait_event(ev)
+            with torch.cuda.stream(s_d2h):
+                for fp in p.free_outputs:
+                    buf = out.buffers[fp.stream]
+                    if fp.stream not in out_host:  # chunk 0 is full: its ratio sizes the stream
+                        n_out = Fraction(buf.numel(), min(w, total)) * total
+                        out_host[fp.stream] = torch.empty(int(n_out), dtype=buf.dtype, pin_memory=True)
+                    o = out_off[fp.stream]
+                    out_host[fp.stream][o:o + buf.numel()].copy_(buf, non_blocking=True)
+                    out_off[fp.stream] = o + buf.numel()
+                    buf.record_stream(s_d2h)
+        s_d2h.synchronize()
+    result = {}
+    for fp in p.free_outputs:
+        t = out_host.get(fp.stream)
+        t = torch.zeros(0, dtype=torch_dtype(fp.data)) if t is None else t[:out_off[fp.stream]]
+        result[fp.stream] = StreamFile(fp.data, t.numpy())
+    return result

@@ -130,3 +130,23 @@ def test_reference_codec_nodes_through_run(cuda, imgc_golden):
               {"0.blk": StreamFile(DataType("float", 16), blocks.ravel()),
                "0.cbk": StreamFile(DataType("float", 16), np.tile(cents, (4, 1)).ravel())})
     assert np.array_equal(out["0.idx"].values, imgc_golden["vq_idx"])
+
+
+def test_chunked_host_streams_pipeline(cuda):
+    # chunk size set + host streams: H2D / kernels / D2H of consecutive chunks on
+    # three streams (client._run_pipelined); identical to the one-slot path,
+    # ragged last chunk, outputs in order
+    from paper_1203_4938_b200 import CudaBackend, DataType, StreamFile, run
+    from paper_1203_4938_b200.apps.fft import fft_program, leaf_program
+    x = complex_signals(11, (301, 1024))
+    sf = StreamFile(DataType("float", 2), x.reshape(-1).view(np.float32))
+    outs = [run(CudaBackend(chunk_size=1024 * 32, max_in_flight=m), fft_program(1024), {"0.x": sf})["0.y"].values
+            for m in (1, 2, 3)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    got = outs[2].view(np.complex64).reshape(301, 1024)
+    for g, r in zip(got[::37], fo.fft_rows(x[::37])):
+        assert rel_l2(g, r) <= 1e-5 * 10
+    y = np.random.default_rng(5).standard_normal(16 * 10007).astype(np.float32)
+    sf = StreamFile(DataType("float", 16), y)
+    a = run(CudaBackend(chunk_size=1000, max_in_flight=3), leaf_program(3), {"0.x": sf})["0.y"].values
+    assert np.array_equal(a, fo.leaf_eval(3, y).ravel())
