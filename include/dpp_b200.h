@@ -185,6 +185,28 @@ int dpp_imgc_decode(const uint8_t* records, const uint8_t* cb_plane, const uint8
                     const float* codebook, int n_cb, int64_t height, int64_t width,
                     uint8_t* rgb, void* stream);
 
+/* ------------------------------------------------------------------------
+ * JIT of kernel-language node bodies
+ * ------------------------------------------------------------------------ */
+
+/* A node body with no hand-written implementation is translated to CUDA C
+ * (paper_1203_4938_b200/kernel/codegen.py: the reference evaluator's
+ * semantics, kernel/interp.py) and compiled here with NVRTC for sm_100a
+ * (cubin, -fmad=false).  Replaces: engine.plan's compile_kernel + the
+ * interpreter run_lanes (/root/reference/pkg/src/dpp/engine.py:82-135,
+ * kernel/interp.py:471-485) for such nodes.  Compiling needs no GPU.
+ *   log: nullable buffer for the NVRTC log (log_len bytes). */
+typedef struct dpp_jit_kernel dpp_jit_kernel;
+int dpp_jit_compile(const char* source, const char* name, dpp_jit_kernel** kernel, char* log,
+                    size_t log_len);
+
+/* Launch `items` work-items (256 threads per CTA) on `stream`.  params: the
+ * generated kernel's 64-bit parameter block (point pointers, element
+ * counts, items, global size, first work-item id, fault word, detail). */
+int dpp_jit_launch(dpp_jit_kernel* kernel, const uint64_t* params, int nparams, int64_t items,
+                   void* stream);
+void dpp_jit_destroy(dpp_jit_kernel* kernel);
+
 #ifdef __cplusplus
 }
 #endif

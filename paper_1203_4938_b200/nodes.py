@@ -6,8 +6,9 @@ each kernel against the registered native implementations by
 (name, io signature, exact body text) — the bodies are the ones the
 reference's own program builders generate (apps/fft.py:86-123,
 apps/imgc.py:128-185) plus this framework's self-describing whole-transform
-and fused-codec nodes — and refuses to plan anything it cannot bind
-(``PlanError``): there is no interpreter and no CPU fallback.
+and fused-codec nodes — and compiles any other body to sm_100a with NVRTC (``jit.py``); bodies that
+do not parse or type-check are a ``PlanError``.  There is no interpreter and
+no CPU fallback.
 
 Each ``NativeNode.launch`` receives flat device tensors exactly as the
 reference's ``_run_instance`` receives flat numpy buffers (item count, inputs
@@ -298,8 +299,10 @@ def resolve(node) -> NativeNode:
                 raise PlanError(f"kernel {node.name!r}: io {_io_of(node)} does not match the native "
                                 f"{native.kind} signature {native.io}")
             return native
-    raise PlanError(f"kernel {node.name!r} has no sm_100a implementation; this engine runs registered "
-                    f"native nodes only ({', '.join(registered_kinds())})")
+    # no hand-written kernel: compile the body itself for sm_100a (NVRTC);
+    # parse / type errors surface as PlanError like the reference's plan()
+    from .jit import jit_node
+    return jit_node(node)
 
 
 _ = DataType

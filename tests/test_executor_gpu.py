@@ -78,10 +78,18 @@ def test_device_resident_chain_fft_then_leaf(cuda):
     assert np.allclose(y.tensor.cpu().numpy(), ref, rtol=1e-5, atol=1e-3)
 
 
-def test_unbound_kernels_are_plan_errors(cuda):
-    from paper_1203_4938_b200 import PlanError, parse_program, plan
-    with pytest.raises(PlanError, match="no sm_100a implementation"):
-        plan(parse_program(json.dumps(table2_doc())))
+def test_table2_graph_runs_through_the_jit(cuda):
+    # bodies with no hand-written kernel are compiled for sm_100a (jit.py);
+    # the reference's Table II graph: z = fan.x + rot(fan.y)
+    from paper_1203_4938_b200 import DataType, PlanError, StreamFile, parse_program, plan, run
+    prog = parse_program(json.dumps(table2_doc()))
+    assert all(k.kind.startswith("jit:") for k in plan(prog).kernels.values())
+    zin = np.random.default_rng(4).standard_normal(2 * 999).astype(np.float32)
+    out = run(None, prog, {"0.z": StreamFile(DataType("float", 2), zin)})["2.z"].values
+    assert np.array_equal(out, zin[0::2] + zin[1::2] * np.float32(65536.0))
+    # ill-typed as printed in the paper (a shift on float points): PlanError, like the reference
+    with pytest.raises(PlanError, match="shift requires integer operands"):
+        plan(parse_program(json.dumps(table2_doc(rot_body="int i=get_global_id(0);\ny[i]=x[i]<<16;\n"))))
 
 
 def test_client_errors(cuda):
