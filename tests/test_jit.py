@@ -122,3 +122,30 @@ def test_jit_matches_reference_evaluator(cuda, case, jit_meta, jit_arrays):
             fin = np.isfinite(ref)
             assert np.array_equal(np.isfinite(got), fin)
             assert _ulps(got[fin], ref[fin]).max() <= 4
+
+
+def _app_cases():
+    meta = json.loads((GOLD / "jit_golden.json").read_text())
+    return [dict(name=k, body=v["body"], io={p: tuple(t) for p, t in v["io"].items()}, items=v["items"])
+            for k, v in sorted(meta.items()) if v.get("app")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", _app_cases(), ids=lambda c: c["name"])
+def test_jit_runs_the_reference_app_nodes_bit_exact(cuda, case, jit_arrays):
+    # the reference's own generated bodies (leaf dft2/4/8, ycbcr, chroma box,
+    # gradient, vq) compiled by the JIT instead of the hand-written kernels
+    import torch
+
+    from paper_1203_4938_b200.jit import JitNode
+    from paper_1203_4938_b200.types import DataType
+    jn = JitNode(_node(case))
+    items = case["items"]
+    ins = {p: torch.from_numpy(jit_arrays[f"{case['name']}/in/{p}"]).to(cuda)
+           for p, (b, w, d) in case["io"].items() if d == "in"}
+    outs = {p: torch.empty(items * w, dtype=getattr(torch, DataType(b, w).dtype.name), device=cuda)
+            for p, (b, w, d) in case["io"].items() if d == "out"}
+    jn.launch(items, ins, outs, None)
+    for p, t in outs.items():
+        got, ref = t.cpu().numpy(), jit_arrays[f"{case['name']}/out/{p}"]
+        assert got.tobytes() == ref.tobytes(), (p, np.flatnonzero(got != ref)[:5])
