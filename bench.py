@@ -338,6 +338,8 @@ def run_ours(args) -> None:
     nimg, side = 64, 4096
     imgs = torch.randint(0, 256, (nimg, side, side), dtype=torch.uint8, device=dev, generator=gen)
     cbs = torch.randn((nimg, 256, 16), dtype=torch.float32, device=dev, generator=gen)
+    # codebooks as k-means leaves them: centroids of normalised blocks (zero mean, unit deviation)
+    cbs = (cbs - cbs.mean(-1, keepdim=True)) / cbs.std(-1, unbiased=False, keepdim=True)
     be = CudaBackend(outputs="device")
     achain.run_chain(imgs, cbs, backend=be)
     torch.cuda.synchronize()

@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
+  __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
   const int tid = threadIdx.x, warp = tid >> 5;
   // Each CTA owns a contiguous range of the flat (image, tile) space, so the
   // grid is one balanced wave for any batch; the codebook (B operand, norms,
@@ -460,14 +461,30 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
       *reinterpret_cast<float*>(sB + tc::off(j, k)) = hi;
       *reinterpret_cast<float*>(sB + tc::off(j, 16 + k)) = __fsub_rn(c, hi);  // exact remainder
     }
-    if (tid == 0) cmax_bits = 0;
+    if (tid == 0) {
+      cmax_bits = 0;
+      zero_key = ~0ull;
+    }
     __syncthreads();
     for (int j = tid; j < tc::NCB; j += tc::THREADS) {
       float s = 0.f;
       if (j < a.ncb)
         for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
       scn[j] = j < a.ncb ? s : 1e30f;
-      if (j < a.ncb) atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
+      if (j < a.ncb) {
+        atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
+        // a constant block normalises to exactly 0: its index is the exact
+        // (reference-order) argmin of |c_j|^2, strict <, first index — every
+        // centroid of a normalised codebook ties within the band otherwise
+        float c[16];
+        for (int k = 0; k < 16; ++k) c[k] = cbk[j * 16 + k];
+        float2 zp[8], cp[8];
+        const float zero16[16] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        vq_pack(zero16, zp);
+        vq_pack(c, cp);
+        const float d = vq_dist_pairs(zp, cp);
+        if (d < VQ_BEST_INIT) atomicMin(&zero_key, ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)j);
+      }
     }
   };
   const int64_t nblocks = (a.width / 4) * (a.height / 4);
@@ -588,8 +605,11 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
         }
       }
     }
-    const bool amb = active && !(m2 - m1 > delta2);
-    int bj = i1;
+    bool zero = active;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) zero = zero && nb[e] == 0.f;
+    const bool amb = active && !zero && !(m2 - m1 > delta2);
+    int bj = zero ? (zero_key == ~0ull ? 0 : (int)(zero_key & 0xffffffffu)) : i1;
     unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
     // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block at
     // a time — each lane rescores 8 centroids on the CUDA cores (fp32, error

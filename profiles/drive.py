@@ -40,6 +40,8 @@ def main() -> None:
         from paper_1203_4938_b200.apps import chain
         imgs = torch.randint(0, 256, (a.images, 4096, 4096), dtype=torch.uint8, device=dev, generator=g)
         cbs = torch.randn((a.images, 256, 16), dtype=torch.float32, device=dev, generator=g)
+        # codebooks as k-means leaves them: centroids of normalised blocks (zero mean, unit deviation)
+        cbs = (cbs - cbs.mean(-1, keepdim=True)) / cbs.std(-1, unbiased=False, keepdim=True)
         for _ in range(a.iters):
             chain.run_chain(imgs, cbs, backend=CudaBackend(outputs="device"))
     elif a.what == "fft2d":

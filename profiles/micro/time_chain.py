@@ -28,6 +28,8 @@ def main() -> None:
     g = torch.Generator(device=dev).manual_seed(0)
     imgs = torch.randint(0, 256, (b, side, side), dtype=torch.uint8, device=dev, generator=g)
     cbs = torch.randn((b, 256, 16), dtype=torch.float32, device=dev, generator=g)
+    # codebooks as k-means leaves them: centroids of normalised blocks (zero mean, unit deviation)
+    cbs = (cbs - cbs.mean(-1, keepdim=True)) / cbs.std(-1, unbiased=False, keepdim=True)
     z = torch.empty((b, side, side), dtype=torch.complex64, device=dev)
     spec = torch.empty((b, side, side), dtype=torch.uint8, device=dev)
     nb = side * side // 16

@@ -208,6 +208,25 @@ def test_tensor_core_search_adversarial_codebooks(cuda):
         assert np.array_equal(rec[:, 2], f["indices"])
 
 
+def test_flat_blocks_take_the_zero_block_index(cuda):
+    """Constant 4x4 blocks normalise to exactly 0; against a normalised codebook
+    every centroid is then at |c_j|^2 = 16 (+- rounding), i.e. inside the band.
+    The encoder resolves them with the precomputed exact argmin for the zero
+    block (no re-check): same indices as the reference, and no ambiguous count."""
+    rng = np.random.default_rng(12)
+    img = io.synthetic_image(256, 256, seed=51)
+    img[:128, :, :] = 117                       # flat half (R=G=B -> constant luma blocks)
+    img[128:, :64, :] = rng.integers(0, 256, 3, dtype=np.uint8)
+    cents = rng.standard_normal((256, 16)).astype(np.float64)
+    cents = ((cents - cents.mean(1, keepdims=True)) / cents.std(1, keepdims=True)).astype(np.float32)
+    cents[[17, 200]] = cents[[5, 5]]            # exact duplicates of a candidate
+    f = io.encode(img, cents)
+    rec, amb, nb = _encode_tc(cuda, img, cents)
+    assert np.array_equal(rec[:, 2], f["indices"]) and np.array_equal(rec[:, 1], f["sigma_idx"])
+    flat = int((f["sigma_idx"] == 0).sum())
+    assert flat >= nb // 2 and amb < nb - flat  # flat blocks never reach the re-check
+
+
 def test_default_path_is_tensor_core_and_matches_exact(cuda, imgc_golden, monkeypatch):
     from paper_1203_4938_b200.apps import imgc
     blob = imgc_golden["fix512_cb256_s0_blob"].tobytes()
