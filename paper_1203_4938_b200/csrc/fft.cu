@@ -1211,14 +1211,14 @@ int fft1d_plan_init(FftPlan* p) {
         return DPP_OK;
       }
     }
-    if (n == 16384) {
+    if (n == 8192 || n == 16384 || n == 32768) {
       const char* e = getenv("DPP_FFT_L2");
       if (!e || atoi(e) != 0) {
         if (int rc2 = fft16k_l2_init(p)) return rc2;
         p->ring16k = 1;
         snprintf(p->desc, sizeof(p->desc),
-                 "two-pass 256x64 four-step, L2-resident exchange (ring %d, lag %d), units of 4 transforms",
-                 p->l2_ring, p->l2_lag);
+                 "two-pass 256x%lld four-step, L2-resident exchange (ring %d, lag %d), units of %lld transforms",
+                 (long long)(n / 256), p->l2_ring, p->l2_lag, (long long)(65536 / n));
         return DPP_OK;
       }
     }
@@ -1250,10 +1250,14 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
   } else if (p->kind == FftPlan::CLUSTER) {
     if (p->ws4k) return fft4096_ws_execute(p, in, out, batch, s);
     if (p->ring16k) {
-      const int64_t main = batch & ~int64_t(3);
+      const int64_t tpu = 65536 / p->n0;  // transforms per ring unit
+      const int64_t main = batch - batch % tpu;
       if (int rc = fft16k_l2_execute(p, in, out, main, s)) return rc;
       if (main == batch) return DPP_OK;
-      return launch_cluster<128, 128, 2>(p, in + main * 16384, out + main * 16384, batch - main, s);
+      const int64_t n = p->n0, rest = batch - main;
+      if (n == 8192) return launch_cluster<64, 128, 1>(p, in + main * n, out + main * n, rest, s);
+      if (n == 16384) return launch_cluster<128, 128, 2>(p, in + main * n, out + main * n, rest, s);
+      return launch_cluster<128, 256, 4>(p, in + main * n, out + main * n, rest, s);
     }
     switch (p->n0) {
       case 2048: return launch_cluster<32, 64, 1>(p, in, out, batch, s);
