@@ -87,6 +87,15 @@ int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* 
  * (SURVEY §8(e) C3). */
 int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, void* stream);
 
+/* C5 fusion: to_complex -> 2-D FFT -> spectrum_u8 in two passes.  in: batch
+ * n0 x n1 u8 images; out: batch n0 x n1 u8 spectra (the spectrum_u8 node's
+ * arithmetic); work: batch * n0 * n1 complex64 (the row-pass result).  Needs
+ * n1 = 4096 and n0 in {4096, 16384} (DPP_ENOTSUP otherwise: run the three
+ * nodes separately).  The executor uses it when the graph has exactly that
+ * chain with no other consumer of the intermediate edges. */
+int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* out, float alpha, float* work,
+                          int64_t batch, void* stream);
+
 void dpp_fft_plan_destroy(dpp_fft_plan* plan);
 
 /* The reference's quadratic oracle naive_dft (apps/fft.py:32-42) on the

@@ -46,6 +46,7 @@ SIGNATURES = {
     "dpp_imgc_block_stats": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, C.c_double, _vp, _vp, _vp]),
     "dpp_kmeans": (_int, [_vp, _i64, _int, _i64, C.POINTER(C.c_double), _int, _vp,
                           C.POINTER(C.c_double), C.POINTER(_int), _vp]),
+    "dpp_fft2d_u8_spectrum": (_int, [_vp, _vp, _vp, C.c_float, _vp, _i64, _vp]),
     "dpp_jit_compile": (_int, [C.c_char_p, C.c_char_p, C.POINTER(_vp), C.c_char_p, _sz]),
     "dpp_jit_launch": (_int, [_vp, C.POINTER(C.c_uint64), _int, _i64, _vp]),
     "dpp_jit_destroy": (None, [_vp]),

@@ -121,6 +121,24 @@ int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, vo
                                     static_cast<cudaStream_t>(stream));
 }
 
+int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* out, float alpha, float* work,
+                          int64_t batch, void* stream) {
+  if (!plan) return dpp::fail(DPP_EINVAL, "plan is NULL");
+  const dpp::FftPlan& p = plan->impl;
+  if (p.rank != 2) return dpp::fail(DPP_EINVAL, "the fused u8 -> 2-D FFT -> spectrum path needs a rank-2 plan");
+  if (batch < 0 || batch > p.batch)
+    return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch, (long long)p.batch);
+  if (!p.rows || !p.rows->ws4k || !p.col_ring)
+    return dpp::fail(DPP_ENOTSUP, "no fused schedule for %lld x %lld (needs 4096 columns and a ring column pass)",
+                     (long long)p.n0, (long long)p.n1);
+  if (batch == 0) return DPP_OK;
+  if (!in || !out || !work) return dpp::fail(DPP_EINVAL, "NULL data pointer");
+  auto s = static_cast<cudaStream_t>(stream);
+  auto* w = reinterpret_cast<float2*>(work);
+  if (int rc = dpp::fft4096_ws_execute_u8(p.rows, in, w, batch * p.n0, s)) return rc;
+  return dpp::fft2d_colring_execute(&p, w, batch, s, out, alpha);
+}
+
 void dpp_fft_plan_destroy(dpp_fft_plan* plan) {
   if (!plan) return;
   dpp::fft_plan_release(&plan->impl);

@@ -34,14 +34,8 @@ __global__ void __launch_bounds__(256) u8_to_complex_kernel(const uchar2* __rest
   }
 }
 
-// m = sqrt(z.x*z.x + z.y*z.y); v = floor(alpha * log(1 + m)); y = (uchar)clamp(v, 0, 255)
-// The squares and the sum are binary32 exactly as the node body; sqrt and
-// log use the SFU (MUFU.SQRT / MUFU.LG2, <= 2 ulp) — the adapter is a
-// transcendental node, compared with the reference as a mismatch count.
 __device__ __forceinline__ unsigned char spectrum_one(float re, float im, float alpha) {
-  const float m = sqrtf(__fadd_rn(__fmul_rn(re, re), __fmul_rn(im, im)));
-  const float v = floorf(__fmul_rn(alpha, __logf(__fadd_rn(1.0f, m))));
-  return (unsigned char)fminf(fmaxf(v, 0.f), 255.f);
+  return spectrum_u8_one(re, im, alpha);  // common.cuh
 }
 
 __global__ void __launch_bounds__(256) spectrum_u8_kernel(const float4* __restrict__ z, uchar2* __restrict__ y,

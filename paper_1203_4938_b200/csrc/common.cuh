@@ -141,6 +141,16 @@ template <> __device__ __forceinline__ void dft_r<4>(float2 (&v)[4]) { dft4(v[0]
 template <> __device__ __forceinline__ void dft_r<8>(float2 (&v)[8]) { dft8(v); }
 template <> __device__ __forceinline__ void dft_r<16>(float2 (&v)[16]) { dft16(v); }
 
+// C5 adapter node body (apps/chain.py): m = sqrt(re^2 + im^2) in binary32,
+// v = floor(alpha * log(1 + m)), u8 clamp; sqrt/log on the SFU (a
+// transcendental node, compared with the reference as a mismatch count).
+// Shared by the standalone node and the fused 2-D column pass.
+__device__ __forceinline__ unsigned char spectrum_u8_one(float re, float im, float alpha) {
+  const float m = sqrtf(__fadd_rn(__fmul_rn(re, re), __fmul_rn(im, im)));
+  const float v = floorf(__fmul_rn(alpha, __logf(__fadd_rn(1.0f, m))));
+  return (unsigned char)fminf(fmaxf(v, 0.f), 255.f);
+}
+
 __host__ __device__ constexpr int ilog2(long long n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
 // ---------------------------------------------------------------------------

@@ -40,6 +40,7 @@ struct Args {
   const float2* twr;   // W_R^m, m < R
   const float4* tw256; // W256^m as (w, i*w), m < 256
   int units, tiles_per_image, lag, ring;
+  float alpha;         // SPEC: spectrum_u8 scale
 };
 
 // P1, B = 16: thread = one (column, a) sequence over b; no exchange
@@ -112,7 +113,9 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
   }
 }
 
-template <int B, bool DISCARD>
+// SPEC: the C5 chain's spectrum_u8 node fused into the output: P2 stages
+// u8 = spectrum(X) (a 16 x 256 byte tile per stage) and TMA-stores bytes.
+template <int B, bool DISCARD, bool SPEC = false>
 __global__ void __launch_bounds__(THREADS, 3)
 fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
   constexpr int A = TILE / (16 * B);  // a values per P1 item
@@ -151,7 +154,9 @@ fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
       } else {
         if (u + a.ring < a.units) red_release_add(cnt2 + u, 1);  // lines discarded by the compute warps
         const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image;
-        tma_store_3d(&tout, 16 * ct, g, img * 256, smem + s * TILE);
+        tma_store_3d(&tout, 16 * ct, g, img * 256,
+                     SPEC ? reinterpret_cast<const void*>(reinterpret_cast<const uint8_t*>(smem + S * TILE) + s * 4096)
+                          : reinterpret_cast<const void*>(smem + s * TILE));
         bulk_commit();
       }
     };
@@ -254,9 +259,15 @@ fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = lds64((bR ^ (144u * (k & 7))) + 2048 * k);
       dft16c(v);
-      __syncwarp();
+      if constexpr (SPEC) {
+        uint8_t* o = reinterpret_cast<uint8_t*>(smem + S * TILE) + s * 4096 + 16 * idx + col;
 #pragma unroll
-      for (int d1 = 0; d1 < 16; ++d1) sts64(bA + 2048 * d1, v[d1]);  // output row k2 = idx + 16 d1
+        for (int d1 = 0; d1 < 16; ++d1) o[256 * d1] = spectrum_u8_one(v[d1].x, v[d1].y, a.alpha);  // row k2
+      } else {
+        __syncwarp();
+#pragma unroll
+        for (int d1 = 0; d1 < 16; ++d1) sts64(bA + 2048 * d1, v[d1]);  // output row k2 = idx + 16 d1
+      }
     }
     fence_proxy_async_smem();
     __syncwarp();
@@ -271,7 +282,9 @@ fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
 
 static int g_col_discard = -1;
 
-static size_t colring_smem() { return (size_t)colring::S * colring::TILE * sizeof(float2); }
+static size_t colring_smem(bool spec = false) {
+  return (size_t)colring::S * (colring::TILE * sizeof(float2) + (spec ? 4096 : 0));
+}
 
 template <int B>
 static int colring_prepare(int* ctas) {
@@ -280,6 +293,8 @@ static int colring_prepare(int* ctas) {
                                       (int)smem));
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
   int per_sm = 0, dev = 0, sms = 0;
   DPP_CUDA_CHECK(
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, colring::fft_cols_l2w<B, true>, colring::THREADS, smem));
@@ -340,7 +355,9 @@ int fft2d_colring_init(FftPlan* p) {
   return DPP_OK;
 }
 
-int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s) {
+// spec_out != nullptr: fused spectrum_u8 — the column pass writes u8 spectra there
+int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s, uint8_t* spec_out,
+                          float alpha) {
   const int64_t R = p->n0, C = p->n1;
   const int B = (int)(R / 256);
   const int64_t units = batch * (C / 16);
@@ -352,7 +369,12 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
     const uint32_t box[3] = {16, (uint32_t)(colring::TILE / (16 * B)), (uint32_t)B};
     if (int rc = make_tmap_c64_3d(&tin, data, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
   }
-  {
+  if (spec_out) {
+    const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch)};
+    const uint64_t strides[2] = {(uint64_t)C, (uint64_t)C * B};
+    const uint32_t box[3] = {16, 1, 256};
+    if (int rc = make_tmap_u8_3d(&tout, spec_out, dims, strides, box)) return rc;
+  } else {
     const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch)};
     const uint64_t strides[2] = {(uint64_t)C * 8, (uint64_t)C * 8 * B};
     const uint32_t box[3] = {16, 1, 256};
@@ -367,12 +389,18 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   a.tiles_per_image = (int)(C / 16);
   a.lag = (int)(units < p->l2_lag ? units : p->l2_lag);
   a.ring = p->l2_ring;
+  a.alpha = alpha;
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
   const int64_t items = 2 * (int64_t)B * units;
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
-  const size_t smem = colring_smem();
-  if (B == 16) {
+  const size_t smem = colring_smem(spec_out != nullptr);
+  if (spec_out) {
+    if (B == 16)
+      colring::fft_cols_l2w<16, true, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    else
+      colring::fft_cols_l2w<64, true, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  } else if (B == 16) {
     if (g_col_discard)
       colring::fft_cols_l2w<16, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
     else

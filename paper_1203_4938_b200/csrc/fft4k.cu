@@ -15,6 +15,7 @@
 // 2 CTAs per SM: 72 -> 96 registers removed the spills, 0.78 -> 0.71 ms); no scratch, no cross-CTA dependencies: per point 8 B read +
 // 8 B written in HBM, 48 B through shared memory.
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -42,10 +43,14 @@ constexpr int S = DPP_WS4K_S;
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ int rotl4(int x) { return ((x << 1) | (x >> 3)) & 15; }
 
+// U8: real u8 input (the C5 chain's to_complex node fused in): each stage also
+// carries the transform's 4 KB of pixels, widened to (x, 0) in stage A.
+template <bool U8>
 __global__ void __launch_bounds__(THREADS, DPP_WS4K_MINB)
-fft4096_ws(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, int batch,
-           const float2* __restrict__ twn, const float4* __restrict__ tw256) {
+fft4096_ws(const __grid_constant__ CUtensorMap tin, const uint8_t* __restrict__ inu8, float2* __restrict__ out,
+           int batch, const float2* __restrict__ twn, const float4* __restrict__ tw256) {
   extern __shared__ __align__(1024) float2 smem[];
+  const uint8_t* pix = reinterpret_cast<const uint8_t*>(smem + S * TILE);  // U8: S x 4 KB
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t done[S];
   const int tid = threadIdx.x;
@@ -67,8 +72,13 @@ fft4096_ws(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, in
     for (int t = blockIdx.x; t < batch; t += G, ++i) {
       const int s = i % S;
       if (i >= S) mbar_wait(&done[s], ((i - S) / S) & 1);
-      mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
-      tma_load_2d_hint(smem + s * TILE, &tin, 0, t * 256, &full[s], stream_pol);
+      if constexpr (U8) {
+        mbar_arrive_expect_tx(&full[s], N);
+        bulk_g2s(const_cast<uint8_t*>(pix) + s * N, inu8 + (size_t)t * N, N, &full[s]);
+      } else {
+        mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
+        tma_load_2d_hint(smem + s * TILE, &tin, 0, t * 256, &full[s], stream_pol);
+      }
     }
     return;
   }
@@ -90,9 +100,15 @@ fft4096_ws(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, in
     mbar_wait(&full[s], (i / S) & 1);
     const uint32_t b = sbase + (uint32_t)s * (TILE * 8);
     // P1: 256-point FFTs over a, warp-local (see fft_l2.cu)
-    const uint32_t bA = b + offA;
+    if constexpr (U8) {
+      const uint8_t* px = pix + s * N + idx * 16 + col;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
+      for (int j = 0; j < 16; ++j) v[j] = make_float2((float)px[256 * j], 0.f);  // row a = 16 j + idx
+    } else {
+      const uint32_t bA = b + offA;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
+    }
     dft16c(v);
     float2 wk = w1;
 #pragma unroll
@@ -131,7 +147,7 @@ fft4096_ws(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, in
     for (int bb = 0; bb < 16; ++bb) v[bb] = lds64(b + 8u * (16 * k1 + (bb ^ rotl4(k1 & 15))));
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) mbar_arrive1(&done[s]);  // stage free for the next TMA load
+    if (lane == 0) mbar_arrive1(&done[s]);  // stage free for the next load
     dft16c(v);  // v[k2]
     float2* dst = out + (size_t)t * N + k1;
 #pragma unroll
@@ -143,13 +159,18 @@ fft4096_ws(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, in
 
 static int g_ws4k_ctas = 0;
 
+static size_t ws4k_smem(bool u8) { return (size_t)ws4k::S * (ws4k::TILE * sizeof(float2) + (u8 ? ws4k::N : 0)); }
+
 int fft4096_ws_init(FftPlan* p) {
   using namespace ws4k;
-  const size_t smem = (size_t)S * TILE * sizeof(float2);
-  DPP_CUDA_CHECK(cudaFuncSetAttribute(fft4096_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = ws4k_smem(false);
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(fft4096_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(fft4096_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ws4k_smem(true)));
   if (!g_ws4k_ctas) {
     int per_sm = 0, dev = 0, sms = 0;
-    DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft4096_ws, THREADS, smem));
+    DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft4096_ws<true>, THREADS,
+                                                                 ws4k_smem(true)));
     DPP_CUDA_CHECK(cudaGetDevice(&dev));
     DPP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) return fail(DPP_ECUDA, "fft4096_ws does not fit on an SM");
@@ -180,9 +201,23 @@ int fft4096_ws_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
   CUtensorMap tin;
   if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 256, 16, 256, 16, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
   const unsigned grid = (unsigned)(batch < g_ws4k_ctas ? batch : g_ws4k_ctas);
-  fft4096_ws<<<grid, THREADS, (size_t)S * TILE * sizeof(float2), s>>>(
-      tin, out, (int)batch, reinterpret_cast<const float2*>(p->l2_tw + 256), p->l2_tw);
+  fft4096_ws<false><<<grid, THREADS, ws4k_smem(false), s>>>(
+      tin, nullptr, out, (int)batch, reinterpret_cast<const float2*>(p->l2_tw + 256), p->l2_tw);
   DPP_LAUNCH_CHECK("fft4096_ws");
+  return DPP_OK;
+}
+
+// the same transform of real u8 rows (x -> (x, 0) fused into the load)
+int fft4096_ws_execute_u8(const FftPlan* p, const uint8_t* in, float2* out, int64_t batch, cudaStream_t s) {
+  using namespace ws4k;
+  if (batch <= 0) return DPP_OK;
+  if (batch > 0x7fffffff / 256) return fail(DPP_EINVAL, "batch %lld too large", (long long)batch);
+  CUtensorMap unused;
+  std::memset(&unused, 0, sizeof(unused));
+  const unsigned grid = (unsigned)(batch < g_ws4k_ctas ? batch : g_ws4k_ctas);
+  fft4096_ws<true><<<grid, THREADS, ws4k_smem(true), s>>>(
+      unused, in, out, (int)batch, reinterpret_cast<const float2*>(p->l2_tw + 256), p->l2_tw);
+  DPP_LAUNCH_CHECK("fft4096_ws<u8>");
   return DPP_OK;
 }
 

@@ -54,11 +54,13 @@ void fft_plan_release(FftPlan* p);
 int fft65536_l2x_init(FftPlan* p);
 int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_colring_init(FftPlan* p);
-int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s);
+int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s,
+                          uint8_t* spec_out = nullptr, float alpha = 0.f);
 int fft16k_l2_init(FftPlan* p);
 int fft16k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft4096_ws_init(FftPlan* p);
 int fft4096_ws_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
+int fft4096_ws_execute_u8(const FftPlan* p, const uint8_t* in, float2* out, int64_t batch, cudaStream_t s);
 int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
 
 }  // namespace dpp

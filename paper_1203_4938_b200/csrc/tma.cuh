@@ -61,4 +61,27 @@ inline int make_tmap_c64_3d(CUtensorMap* map, const void* base, const uint64_t d
   return DPP_OK;
 }
 
+// 3-D view of bytes (u8 planes): dims {d0 (inner), d1, d2}, byte strides {s1, s2}
+inline int make_tmap_u8_3d(CUtensorMap* map, const void* base, const uint64_t dims[3], const uint64_t strides[2],
+                           const uint32_t box[3]) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(DPP_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t st[2] = {strides[0], strides[1]};
+  const cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), d, st, bx, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DPP_ECUDA, "cuTensorMapEncodeTiled (u8 3-D) failed (%d)", (int)r);
+  return DPP_OK;
+}
+
 }  // namespace dpp

@@ -54,6 +54,10 @@ class ExecutionPlan:
     chunk_size: int | None
     device: torch.device
     broadcast: frozenset = frozenset()  # free input stream names handed whole to every chunk
+    # fusion: fft2d instance -> (to_complex instance, spectrum_u8 instance) run as one
+    # fused launch (ops.fft2d_u8_spectrum); the two adapters are then skipped
+    fused: dict = field(default_factory=dict)
+    absorbed: frozenset = frozenset()
 
     @property
     def items_per_element(self) -> Fraction:
@@ -145,14 +149,51 @@ def plan(program, chunk_size: int | None = DEFAULT_CHUNK_SIZE, *, device=None) -
                             f"element, not integral at chunk size {chunk_size}")
         multipliers[iid] = first
     free = free_points(program)
+    fused = _fusions(program, kernels, bindings, free, multipliers)
     result = ExecutionPlan(
         program=program, order=order, multipliers=multipliers, kernels=kernels, bindings=bindings,
         free_inputs=tuple(p for p in free if p.direction is Direction.INPUT),
         free_outputs=tuple(p for p in free if p.direction is Direction.OUTPUT),
-        chunk_size=chunk_size, device=dev, broadcast=frozenset(broadcast))
+        chunk_size=chunk_size, device=dev, broadcast=frozenset(broadcast), fused=fused,
+        absorbed=frozenset(i for pair in fused.values() for i in pair))
     with _cache_lock:
         _cache[key] = result
     return result
+
+
+def _fusions(program, kernels, bindings, free, multipliers) -> dict:
+    """to_complex -> fft2d_RxC -> spectrum_u8 chains whose intermediate edges have
+    no other consumer (and are not free outputs) -> {fft2d iid: (tc iid, spec iid)}.
+    Only shapes with a fused schedule (4096 columns, ring column pass) qualify;
+    DPP_FUSE=0 disables the pass."""
+    import os
+    if os.environ.get("DPP_FUSE") == "0":
+        return {}
+    consumers: dict = {}
+    for a in program.arrows:
+        consumers.setdefault(a.output, []).append(a.input)
+    free_out = {(fp.instance, fp.point) for fp in free if fp.direction is Direction.OUTPUT}
+    kind = {inst.id: kernels[inst.kernel].kind for inst in program.nodes}
+    out = {}
+    for inst in program.nodes:
+        native = kernels[inst.kernel]
+        if not native.kind.startswith("fft2d_") or getattr(native, "cols", None) != 4096 or \
+                native.rows not in (4096, 16384):
+            continue
+        src = bindings.get((inst.id, "x"))
+        if src is None or src[0] != "arrow" or kind.get(src[1]) != "to_complex":
+            continue
+        tc = src[1]
+        if consumers.get((tc, "y"), []) != [(inst.id, "x")] or (tc, "y") in free_out:
+            continue
+        outs = consumers.get((inst.id, "y"), [])
+        if len(outs) != 1 or (inst.id, "y") in free_out or kind.get(outs[0][0]) != "spectrum_u8":
+            continue
+        sp = outs[0][0]
+        if multipliers[tc] != multipliers[inst.id] or multipliers[sp] != multipliers[inst.id]:
+            continue
+        out[inst.id] = (tc, sp)
+    return out
 
 
 def _element_count(p: ExecutionPlan, chunk: Chunk) -> int:
@@ -189,37 +230,70 @@ def _items(p: ExecutionPlan, iid: int, elements: int, chunk_index: int) -> int:
     return int(items)
 
 
+def _run_one(p: ExecutionPlan, iid: int, chunk: Chunk, elements: int, produced: dict, stream) -> None:
+    inst = p.program.instance(iid)
+    node = p.program.kernels[inst.kernel]
+    native = p.kernels[inst.kernel]
+    items = _items(p, iid, elements, chunk.index)
+    inputs = {}
+    for pt in node.io:
+        if not pt.is_input:
+            continue
+        kind = p.bindings[(iid, pt.name)]
+        inputs[pt.name] = chunk.buffers[kind[1]] if kind[0] == "free" else produced[(kind[1], kind[2])]
+    outputs = {pt.name: torch.empty(items * pt.data.width, dtype=torch_dtype(pt.data), device=p.device)
+               for pt in node.io if not pt.is_input}
+    try:
+        if items:
+            native.check_items(items)
+            native.launch(items, inputs, outputs, stream)
+    except KernelRuntimeError as exc:
+        raise EngineRuntimeError(str(exc), instance=iid, work_item=exc.work_item,
+                                 chunk=chunk.index) from exc
+    for name, buf in outputs.items():
+        produced[(iid, name)] = buf
+
+
 def run_chunk(p: ExecutionPlan, chunk: Chunk, stream: torch.cuda.Stream | None = None) -> Chunk:
     """Run every instance over one chunk on ``stream`` (engine.py:176-215)."""
     elements = _element_count(p, chunk)
     produced: dict[tuple[int, str], torch.Tensor] = {}
     for iid in p.order:
-        inst = p.program.instance(iid)
-        node = p.program.kernels[inst.kernel]
-        native = p.kernels[inst.kernel]
-        items = _items(p, iid, elements, chunk.index)
-        inputs = {}
-        for pt in node.io:
-            if not pt.is_input:
-                continue
-            kind = p.bindings[(iid, pt.name)]
-            inputs[pt.name] = chunk.buffers[kind[1]] if kind[0] == "free" else produced[(kind[1], kind[2])]
-        outputs = {pt.name: torch.empty(items * pt.data.width, dtype=torch_dtype(pt.data), device=p.device)
-                   for pt in node.io if not pt.is_input}
-        try:
-            if items:
-                native.check_items(items)
-                native.launch(items, inputs, outputs, stream)
-        except KernelRuntimeError as exc:
-            raise EngineRuntimeError(str(exc), instance=iid, work_item=exc.work_item,
-                                     chunk=chunk.index) from exc
-        for name, buf in outputs.items():
-            produced[(iid, name)] = buf
+        if iid in p.absorbed:
+            continue
+        if iid in p.fused:
+            if not _run_fused(p, iid, chunk, elements, produced, stream):
+                tc, sp = p.fused[iid]
+                for j in (tc, iid, sp):  # no fused schedule after all: the three nodes
+                    _run_one(p, j, chunk, elements, produced, stream)
+            continue
+        _run_one(p, iid, chunk, elements, produced, stream)
     out_buf, out_cnt = {}, {}
     for fp in p.free_outputs:
         out_buf[fp.stream] = produced[(fp.instance, fp.point)]
         out_cnt[fp.stream] = _items(p, fp.instance, elements, chunk.index)
     return Chunk(chunk.index, out_buf, out_cnt)
+
+
+def _run_fused(p: ExecutionPlan, iid: int, chunk: Chunk, elements: int, produced: dict, stream) -> bool:
+    """to_complex -> fft2d -> spectrum_u8 as one fused launch (False: not possible
+    for this chunk; the caller then runs the three instances one by one)."""
+    from . import ops
+    tc, sp = p.fused[iid]
+    native = p.kernels[p.program.instance(iid).kernel]
+    items = _items(p, iid, elements, chunk.index)
+    kind = p.bindings[(tc, "x")]
+    x = chunk.buffers[kind[1]] if kind[0] == "free" else produced[(kind[1], kind[2])]
+    try:
+        native.check_items(items)
+    except KernelRuntimeError as exc:
+        raise EngineRuntimeError(str(exc), instance=iid, work_item=exc.work_item, chunk=chunk.index) from exc
+    y = torch.empty(items, dtype=torch.uint8, device=p.device)
+    alpha = p.kernels[p.program.instance(sp).kernel].alpha
+    if items and not ops.fft2d_u8_spectrum(x, native.rows, native.cols, alpha, y, stream):
+        return False
+    produced[(sp, "y")] = y
+    return True
 
 
 def _checked(p: ExecutionPlan, chunks: Iterable[Chunk]) -> Iterator[tuple[int, Chunk, int]]:

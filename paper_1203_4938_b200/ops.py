@@ -19,7 +19,7 @@ from ._torch import require_cuda, stream_handle
 from .errors import KernelRuntimeError, PlanError
 
 __all__ = ["FftPlanHandle", "fft_plan", "fft_forward", "fft2d_forward", "leaf_dft",
-           "ycbcr", "boxdown", "gradient", "vqnearest", "encode", "decode"]
+           "ycbcr", "boxdown", "gradient", "vqnearest", "encode", "decode", "fft2d_u8_spectrum"]
 
 
 def _check_cuda(t: torch.Tensor, name: str, dtype: torch.dtype | None = None) -> None:
@@ -221,6 +221,31 @@ def u8_to_complex(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     _check_cuda(y, "y")
     _lib.check(_lib.load().dpp_u8_to_complex(x.data_ptr(), y.data_ptr(), x.numel(), stream_handle(stream)),
                "to_complex")
+
+
+def fft2d_u8_spectrum(x: torch.Tensor, rows: int, cols: int, alpha: float, out: torch.Tensor,
+                      stream=None) -> bool:
+    """Fused to_complex -> 2-D FFT -> spectrum_u8 over batches of rows x cols u8
+    images (two passes; the complex intermediate is a scratch tensor).  Returns
+    False (and does nothing) when the shape has no fused schedule."""
+    _check_cuda(x, "x", torch.uint8)
+    _check_cuda(out, "out", torch.uint8)
+    n = rows * cols
+    if x.numel() % n or out.numel() != x.numel():
+        raise PlanError("fused 2-D spectrum: sizes must be whole images and match")
+    batch = x.numel() // n
+    if batch == 0:
+        return True
+    plan = fft_plan(2, rows, cols, batch, x.device)
+    work = torch.empty(2 * x.numel(), dtype=torch.float32, device=x.device)
+    if stream is not None:
+        work.record_stream(stream)
+    rc = _lib.load().dpp_fft2d_u8_spectrum(plan._h, x.data_ptr(), out.data_ptr(), float(alpha), work.data_ptr(),
+                                           batch, stream_handle(stream))
+    if rc == _lib.DPP_ENOTSUP:
+        return False
+    _lib.check(rc, "fft2d_u8_spectrum")
+    return True
 
 
 def spectrum_u8(z: torch.Tensor, y: torch.Tensor, alpha: float, stream=None) -> None:

@@ -69,3 +69,35 @@ def test_chain_device_resident_shared_codebook(cuda):
     out = chain.run_chain(imgs, cb, backend=CudaBackend(outputs="device"))
     assert all(t.is_cuda for t in out.values())
     assert out["mu"].numel() == 2 * 128 * 64
+
+
+def test_fused_chain_equals_three_nodes(cuda):
+    # 4096-column images: the executor fuses to_complex -> fft2d -> spectrum_u8
+    # into two passes (u8 row loads, u8 spectrum stores); the spectra must be
+    # byte-identical to running the three nodes separately
+    import torch
+
+    from paper_1203_4938_b200 import CudaBackend, ops, plan
+    from paper_1203_4938_b200.apps import chain
+    g = torch.Generator(device=cuda).manual_seed(3)
+    imgs = torch.randint(0, 256, (2, 4096, 4096), dtype=torch.uint8, device=cuda, generator=g)
+    prog = chain.chain_program(4096, 4096, 256)
+    p = plan(prog)
+    assert p.fused and len(p.absorbed) == 2
+    fused = torch.empty(imgs.numel(), dtype=torch.uint8, device=cuda)
+    assert ops.fft2d_u8_spectrum(imgs.reshape(-1), 4096, 4096, chain.ALPHA, fused)
+    z = torch.empty((2, 4096, 4096), dtype=torch.complex64, device=cuda)
+    ops.u8_to_complex(imgs.reshape(-1), torch.view_as_real(z).reshape(-1))
+    ops.fft2d_forward(z, 4096, 4096, out=z)
+    ref = torch.empty(imgs.numel(), dtype=torch.uint8, device=cuda)
+    ops.spectrum_u8(torch.view_as_real(z).reshape(-1), ref, chain.ALPHA)
+    assert torch.equal(fused, ref)
+    cbs = torch.randn((2, 256, 16), device=cuda, generator=g)
+    out = chain.run_chain(imgs, cbs, backend=CudaBackend(outputs="device"))
+    rec = torch.empty(2 * (1024 * 1024) * 3, dtype=torch.uint8, device=cuda)
+    cbp = torch.empty(2 * 1024 * 1024, dtype=torch.uint8, device=cuda)
+    crp = torch.empty(2 * 1024 * 1024, dtype=torch.uint8, device=cuda)
+    ops.encode(ref.view(2, 4096, 4096), 1, 4096, 4096, cbs, rec, cbp, crp, batch=2, shared_codebook=False)
+    rec = rec.view(-1, 3)
+    for col, key in enumerate(("mu", "sig", "idx")):  # the whole graph, fused, = encode of the 3-node spectra
+        assert torch.equal(out[key].reshape(-1).to(torch.uint8), rec[:, col]), key
