@@ -142,6 +142,21 @@ def _cpu_chunk(args):
     return time.perf_counter() - t0, count
 
 
+def host_info() -> dict:
+    """What BASELINE.md §3 asks to record with every CPU number."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model,
+            "numpy": np.__version__,
+            "threads_env": {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")}}
+
+
 def cpu_baseline(threads: int, seconds: float = 12.0) -> dict:
     """Reference-algorithm FFT on host cores: per-signal fft() calls, bounded sample."""
     import multiprocessing as mp
@@ -157,7 +172,7 @@ def cpu_baseline(threads: int, seconds: float = 12.0) -> dict:
             done += sum(c for _, c in res)
         wall = time.perf_counter() - t0
     value = done * FLOPS_PER_TRANSFORM / wall / 1e9
-    return {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+    return {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port", "host": host_info(),
             "sample": f"{done} signals of N=2^16 (the step is 4096), reference fft() algorithm "
                       f"(oracle/fft_oracle.py: host bit-reversal, binary32 dft8 leaves, binary64 "
                       f"butterflies), {threads} processes, {wall:.1f} s wall"}
