@@ -178,6 +178,70 @@ def cpu_baseline(threads: int, seconds: float = 12.0) -> dict:
                       f"butterflies), {threads} processes, {wall:.1f} s wall"}
 
 
+def _c4_chunk(args):
+    """Reference compress() steps 1-8 (codebook given, like the GPU node) on one image."""
+    seed, side = args
+    from oracle import imgc_oracle as io
+    rng = np.random.default_rng(seed)
+    g = rng.integers(0, 256, (side, side), dtype=np.uint8)
+    img = np.repeat(g[..., None], 3, 2)
+    cb = rng.standard_normal((256, 16))
+    cb = ((cb - cb.mean(1, keepdims=True)) / cb.std(1, keepdims=True)).astype(np.float32)
+    t0 = time.perf_counter()
+    io.encode(img, cb)
+    return time.perf_counter() - t0, side * side
+
+
+def _c3_chunk(args):
+    seed, count, n = args
+    from oracle import fft_oracle
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((count, n)) + 1j * rng.standard_normal((count, n))).astype(np.complex64)
+    t0 = time.perf_counter()
+    for row in x:
+        fft_oracle.fft(row)
+    return time.perf_counter() - t0, count
+
+
+def secondary_cpu_baselines(threads: int) -> dict:
+    """Bounded host samples of the reference algorithms for C1, C3 and C4 (oracle port)."""
+    import multiprocessing as mp
+    from oracle import fft_oracle
+    out = {}
+    rng = np.random.default_rng(42)
+    x1 = (rng.standard_normal(1024) + 1j * rng.standard_normal(1024)).astype(np.complex64)
+    fft_oracle.fft(x1)
+    lat = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        fft_oracle.fft(x1)
+        lat.append((time.perf_counter() - t0) * 1e3)
+    lat.sort()
+    out["c1"] = {"value": round(lat[len(lat) // 2], 4), "unit": "ms (median)", "cores": 1, "kind": "port",
+                 "sample": "20 calls of fft(x), N=1024 k=3 (the port has no kernel-language compile; the "
+                           "reference's fft() spends ~7 ms of its 8.35 ms there, BASELINE.md §2)"}
+    with mp.get_context("spawn").Pool(threads) as pool:
+        pool.map(_c3_chunk, [(1, 1, 256)] * threads)
+        t0 = time.perf_counter()
+        res = pool.map(_c3_chunk, [(7 + i, 64, 16384) for i in range(threads)])
+        wall = time.perf_counter() - t0
+        rows = sum(c for _, c in res)
+        # the 2-D transform is 2 x 16384 such row transforms (composition, SURVEY §8(d) C3)
+        gflops = rows * 5.0 * 16384 * 14 / wall / 1e9
+        out["c3"] = {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                     "sample": f"{rows} row transforms of 16384 (reference fft() per row; the 2-D result is "
+                               f"the composition over 2 x 16384 rows), {wall:.1f} s wall"}
+        pool.map(_c4_chunk, [(1, 64)] * threads)
+        t0 = time.perf_counter()
+        res = pool.map(_c4_chunk, [(11 + i, 1536) for i in range(threads)])
+        wall = time.perf_counter() - t0
+        px = sum(c for _, c in res)
+        out["c4"] = {"value": round(px / wall / 1e6, 4), "unit": "MPixel/s", "cores": threads, "kind": "port",
+                     "sample": f"{len(res)} gray 1536^2 images through compress() steps 1-8 with a given "
+                               f"256-entry codebook (k-means excluded, as on the GPU), {wall:.1f} s wall"}
+    return out
+
+
 # ---------------------------------------------------------------------------
 
 def run_reference_arm(args) -> None:
@@ -391,6 +455,14 @@ def run_ours(args) -> None:
     if rank == 0:
         cpu = cpu_baseline(len(os.sched_getaffinity(0)), seconds=10.0) if world == 1 and not args.no_cpu \
             else None
+        if cpu is not None:
+            try:
+                sec = secondary_cpu_baselines(len(os.sched_getaffinity(0)))
+                c1["cpu_baseline"] = sec["c1"]
+                fft2d["cpu_baseline"] = sec["c3"]
+                compression["cpu_baseline"] = sec["c4"]
+            except Exception as exc:  # keep the headline line alive
+                compression["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
