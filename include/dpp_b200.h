@@ -98,6 +98,38 @@ int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* 
 
 void dpp_fft_plan_destroy(dpp_fft_plan* plan);
 
+/* Row-sharded 2-D transform (SURVEY §8(b) `dpp_fft2d_c2c_fwd_sharded`, §8(e)
+ * C3) with the all-to-all fused into the column pass: no NCCL on the data
+ * path.  The reference has no 2-D node; the oracle is the row-then-column
+ * composition of apps/fft.py:150-174.  Each of `nranks` processes (one per
+ * GPU) holds rows [rank*n0/P, (rank+1)*n0/P) of every image in a
+ * batch x (n0/P) x n1 row slab and has already run the row pass
+ * (dpp_fft_c2c_forward_batch of a rank-1 n1 plan) on it; after a
+ * dpp_peer_barrier, rank q computes the n0-point FFTs of columns
+ * [q*n1/P, (q+1)*n1/P), reading every rank's slab directly (peer-mapped
+ * pointers, slabs[j] for rank j, NVLink loads).  transpose_back != 0: the
+ * results are stored into every rank's row slab outs[j] (natural row-sharded
+ * layout; outs may equal slabs); else into this rank's batch x n0 x (n1/P)
+ * column slab outs[0].  A second dpp_peer_barrier must follow before any rank
+ * reuses its slabs.  plan: rank 2, n0 x n1, n0 in {4096, 16384}
+ * (DPP_ENOTSUP otherwise); nranks a power of two <= 8 dividing n0/256;
+ * n1 a multiple of 16*nranks. */
+int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slabs, float* const* outs,
+                              int nranks, int rank, int transpose_back, int64_t batch, void* stream);
+
+/* CUDA IPC for the peer-mapped slabs: handle (64 bytes) and byte offset of
+ * `ptr` inside its allocation; open maps a peer allocation's base into this
+ * process (peer access enabled lazily); close unmaps it. */
+int dpp_ipc_get_handle(const void* ptr, void* handle, uint64_t* offset);
+int dpp_ipc_open(const void* handle, void** base);
+int dpp_ipc_close(void* base);
+
+/* Stream-ordered barrier over peer-mapped int32[8] flag arrays (flags[j] =
+ * rank j's, zero-initialised; epoch increases by one per barrier): stores
+ * epoch into slot `rank` of every array (system-scope release) and waits for
+ * every slot of its own (acquire).  Traps after timeout_s instead of hanging. */
+int dpp_peer_barrier(int* const* flags, int nranks, int rank, int epoch, double timeout_s, void* stream);
+
 /* The reference's quadratic oracle naive_dft (apps/fft.py:32-42) on the
  * device: binary64 accumulation, rounded to complex64; `batch` signals of n. */
 int dpp_naive_dft(const float* x, float* y, int64_t n, int64_t batch, void* stream);

@@ -50,6 +50,11 @@ SIGNATURES = {
     "dpp_jit_compile": (_int, [C.c_char_p, C.c_char_p, C.POINTER(_vp), C.c_char_p, _sz]),
     "dpp_jit_launch": (_int, [_vp, C.POINTER(C.c_uint64), _int, _i64, _vp]),
     "dpp_jit_destroy": (None, [_vp]),
+    "dpp_fft2d_columns_sharded": (_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), _int, _int, _int, _i64, _vp]),
+    "dpp_ipc_get_handle": (_int, [_vp, _vp, C.POINTER(C.c_uint64)]),
+    "dpp_ipc_open": (_int, [_vp, C.POINTER(_vp)]),
+    "dpp_ipc_close": (_int, [_vp]),
+    "dpp_peer_barrier": (_int, [C.POINTER(_vp), _int, _int, _int, C.c_double, _vp]),
 }
 
 _lock = threading.Lock()

@@ -139,6 +139,15 @@ int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* 
   return dpp::fft2d_colring_execute(&p, w, batch, s, out, alpha);
 }
 
+int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slabs, float* const* outs, int nranks,
+                              int rank, int transpose_back, int64_t batch, void* stream) {
+  if (!plan || !slabs || !outs) return dpp::fail(DPP_EINVAL, "NULL argument to dpp_fft2d_columns_sharded");
+  if (plan->impl.rank != 2) return dpp::fail(DPP_EINVAL, "the sharded column pass needs a rank-2 plan");
+  return dpp::fft2d_colring_execute_peer(&plan->impl, reinterpret_cast<const float2* const*>(slabs),
+                                         reinterpret_cast<float2* const*>(outs), nranks, rank, transpose_back, batch,
+                                         static_cast<cudaStream_t>(stream));
+}
+
 void dpp_fft_plan_destroy(dpp_fft_plan* plan) {
   if (!plan) return;
   dpp::fft_plan_release(&plan->impl);

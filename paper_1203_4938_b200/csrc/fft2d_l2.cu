@@ -17,6 +17,7 @@
 // transforms (same producer / compute-warp structure, same deadlock argument).
 // In place: P2(u) writes unit u's columns only after every P1(u) has read them.
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -41,7 +42,23 @@ struct Args {
   const float4* tw256; // W256^m as (w, i*w), m < 256
   int units, tiles_per_image, lag, ring;
   float alpha;         // SPEC: spectrum_u8 scale
+  int np, col0, tb;    // PEER: ranks, first column of this rank's block, output to the row slabs
 };
+
+// PEER: one tensor map per rank (row slabs in, row slabs or the local column slab out)
+struct Maps8 {
+  CUtensorMap m[8];
+};
+template <bool PEER>
+struct MapSet {
+  using type = CUtensorMap;
+};
+template <>
+struct MapSet<true> {
+  using type = Maps8;
+};
+__device__ __forceinline__ const CUtensorMap* map_at(const CUtensorMap& m, int) { return &m; }
+__device__ __forceinline__ const CUtensorMap* map_at(const Maps8& m, int j) { return &m.m[j]; }
 
 // P1, B = 16: thread = one (column, a) sequence over b; no exchange
 __device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
@@ -115,9 +132,19 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
 
 // SPEC: the C5 chain's spectrum_u8 node fused into the output: P2 stages
 // u8 = spectrum(X) (a 16 x 256 byte tile per stage) and TMA-stores bytes.
-template <int B, bool DISCARD, bool SPEC = false>
+//
+// PEER (row-sharded C3): the all-to-all is fused into this pass.
+// Rank j holds rows [j R/P, (j+1) R/P) = b in [j B/P, (j+1) B/P) of every
+// image in its own row slab; the P1 box is P sub-boxes, one TMA load from each
+// rank's slab (peer-mapped: NVLink reads), landing at 1024-byte-aligned
+// offsets of the stage so the 128B swizzle is unchanged.  P2 either stores
+// the 256 output rows of its k1 as P sub-boxes into the ranks' row slabs
+// (tb: natural row-sharded output, in place is safe because column block q is
+// touched by rank q only) or one box into the local R x (C/P) column slab.
+template <int B, bool DISCARD, bool SPEC = false, bool PEER = false>
 __global__ void __launch_bounds__(THREADS, 3)
-fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
+fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
+             const __grid_constant__ typename MapSet<PEER>::type tout, const Args a) {
   constexpr int A = TILE / (16 * B);  // a values per P1 item
   constexpr int LOGB = B == 16 ? 4 : 6;
   extern __shared__ __align__(1024) float2 smem[];
@@ -154,9 +181,20 @@ fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
       } else {
         if (u + a.ring < a.units) red_release_add(cnt2 + u, 1);  // lines discarded by the compute warps
         const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image;
-        tma_store_3d(&tout, 16 * ct, g, img * 256,
-                     SPEC ? reinterpret_cast<const void*>(reinterpret_cast<const uint8_t*>(smem + S * TILE) + s * 4096)
-                          : reinterpret_cast<const void*>(smem + s * TILE));
+        if constexpr (PEER) {
+          if (a.tb) {
+            const int kk = 256 / a.np;
+            for (int j = 0; j < a.np; ++j)
+              tma_store_3d(map_at(tout, j), a.col0 + 16 * ct, g, img * kk, smem + s * TILE + j * (TILE / a.np));
+          } else {
+            tma_store_3d(map_at(tout, 0), 16 * ct, g, img * 256, smem + s * TILE);
+          }
+        } else {
+          tma_store_3d(&tout, 16 * ct, g, img * 256,
+                       SPEC ? reinterpret_cast<const void*>(reinterpret_cast<const uint8_t*>(smem + S * TILE) +
+                                                            s * 4096)
+                            : reinterpret_cast<const void*>(smem + s * TILE));
+        }
         bulk_commit();
       }
     };
@@ -193,7 +231,13 @@ fft_cols_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
       mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
       if (pass == 1) {
         const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image;
-        tma_load_3d(buf, &tin, 16 * ct, A * g, img * B, &full[s]);
+        if constexpr (PEER) {
+          const int nb = B / a.np;
+          for (int j = 0; j < a.np; ++j)
+            tma_load_3d(buf + j * (TILE / a.np), map_at(tin, j), a.col0 + 16 * ct, A * g, img * nb, &full[s]);
+        } else {
+          tma_load_3d(buf, &tin, 16 * ct, A * g, img * B, &full[s]);
+        }
       } else {
         fence_proxy_async_global();
         bulk_g2s(buf, a.scratch + (size_t)(u & (a.ring - 1)) * (16 * R) + 4096 * g, TILE * sizeof(float2),
@@ -295,6 +339,8 @@ static int colring_prepare(int* ctas) {
                                       (int)smem));
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   DPP_CUDA_CHECK(
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, colring::fft_cols_l2w<B, true>, colring::THREADS, smem));
@@ -390,6 +436,8 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   a.lag = (int)(units < p->l2_lag ? units : p->l2_lag);
   a.ring = p->l2_ring;
   a.alpha = alpha;
+  a.np = 1;
+  a.col0 = a.tb = 0;
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
   const int64_t items = 2 * (int64_t)B * units;
@@ -412,6 +460,78 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
       colring::fft_cols_l2w<64, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
   }
   DPP_LAUNCH_CHECK("fft_cols_l2w");
+  DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
+  return DPP_OK;
+}
+
+// Row-sharded 2-D column pass with the exchange fused in (PEER kernel above).
+// slabs[j]: rank j's batch x (R/np) x C row slab (already row-transformed;
+// device pointers valid in this process — peer-mapped for j != rank).
+// tb: outs[j] = rank j's row slab of the result (may equal slabs[j]);
+// otherwise outs[0] = this rank's batch x R x (C/np) column slab.
+int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, float2* const* outs, int np, int rank,
+                               int tb, int64_t batch, cudaStream_t s) {
+  const int64_t R = p->n0, C = p->n1;
+  const int B = (int)(R / 256);
+  if (!p->col_ring) return fail(DPP_ENOTSUP, "row-sharded column pass needs the column ring (n0 = 4096 or 16384)");
+  if (np < 1 || np > 8 || (np & (np - 1)) || B % np)
+    return fail(DPP_EINVAL, "rank count %d must be a power of two <= 8 dividing %d", np, B);
+  if (rank < 0 || rank >= np) return fail(DPP_EINVAL, "rank %d outside 0..%d", rank, np - 1);
+  if (C % (16 * np)) return fail(DPP_EINVAL, "%lld columns do not split into 16-column tiles over %d ranks",
+                                 (long long)C, np);
+  if (batch < 0 || batch > p->batch) return fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld",
+                                                 (long long)batch, (long long)p->batch);
+  for (int j = 0; j < np; ++j)
+    if (!slabs[j] || (tb ? !outs[j] : !outs[0])) return fail(DPP_EINVAL, "NULL slab pointer");
+  const int64_t w = C / np;
+  const int64_t units = batch * (w / 16);
+  if (units == 0) return DPP_OK;
+  const int nb = B / np, kk = 256 / np;
+  colring::Maps8 tin, tout;
+  std::memset(&tin, 0, sizeof(tin));
+  std::memset(&tout, 0, sizeof(tout));
+  for (int j = 0; j < np; ++j) {
+    const uint64_t dims[3] = {(uint64_t)C, 256, (uint64_t)nb * batch};
+    const uint64_t strides[2] = {(uint64_t)C * 8, (uint64_t)C * 8 * 256};
+    const uint32_t box[3] = {16, (uint32_t)(colring::TILE / (16 * B)), (uint32_t)nb};
+    if (int rc = make_tmap_c64_3d(&tin.m[j], slabs[j], dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  }
+  if (tb) {
+    for (int j = 0; j < np; ++j) {
+      const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)kk * batch};
+      const uint64_t strides[2] = {(uint64_t)C * 8, (uint64_t)C * 8 * B};
+      const uint32_t box[3] = {16, 1, (uint32_t)kk};
+      if (int rc = make_tmap_c64_3d(&tout.m[j], outs[j], dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+    }
+  } else {
+    const uint64_t dims[3] = {(uint64_t)w, (uint64_t)B, (uint64_t)(256 * batch)};
+    const uint64_t strides[2] = {(uint64_t)w * 8, (uint64_t)w * 8 * B};
+    const uint32_t box[3] = {16, 1, 256};
+    if (int rc = make_tmap_c64_3d(&tout.m[0], outs[0], dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  }
+  colring::Args a;
+  a.scratch = p->l2_scratch;
+  a.ctrl = p->l2_ctrl;
+  a.tw256 = p->l2_tw;
+  a.twr = reinterpret_cast<const float2*>(p->l2_tw + 256);
+  a.units = (int)units;
+  a.tiles_per_image = (int)(w / 16);
+  a.lag = (int)(units < p->l2_lag ? units : p->l2_lag);
+  a.ring = p->l2_ring;
+  a.alpha = 0.f;
+  a.np = np;
+  a.col0 = (int)(rank * w);
+  a.tb = tb ? 1 : 0;
+  DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
+  DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
+  const int64_t items = 2 * (int64_t)B * units;
+  const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
+  const size_t smem = colring_smem(false);
+  if (B == 16)
+    colring::fft_cols_l2w<16, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  else
+    colring::fft_cols_l2w<64, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  DPP_LAUNCH_CHECK("fft_cols_l2w<peer>");
   DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
   return DPP_OK;
 }

@@ -56,6 +56,8 @@ int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_
 int fft2d_colring_init(FftPlan* p);
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s,
                           uint8_t* spec_out = nullptr, float alpha = 0.f);
+int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, float2* const* outs, int np, int rank,
+                               int tb, int64_t batch, cudaStream_t s);
 int fft16k_l2_init(FftPlan* p);
 int fft16k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft4096_ws_init(FftPlan* p);

@@ -2,7 +2,14 @@
 
 * ``shard_range``: contiguous batch / row / image slabs per rank (C2, C4, C5 —
   independent units, no data-path collective).
-* ``fft2d_row_sharded`` (C3): a 2-D transform whose rows are
+* ``PeerShardedFft2d`` (C3, the product path): the same
+  row-sharded transform with the all-to-all fused into the column pass — every
+  rank maps every other rank's row slab (CUDA IPC) and the column kernel reads
+  its column block straight out of the peers' HBM over NVLink (TMA loads from
+  peer pointers) and, for natural-order output, TMA-stores the results straight
+  back into the peers' slabs.  No NCCL and no staging copies on the data path;
+  two stream-ordered flag barriers per call.
+* ``fft2d_row_sharded`` (C3, the NCCL baseline): a 2-D transform whose rows are
   split contiguously over P ranks.  Row FFTs run locally; ONE all-to-all
   turns each rank's row slab into a column slab (the send buffer is packed
   so that the received buffer is already the n0 x (n1/P) column slab in
@@ -22,7 +29,8 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_range", "fft2d_row_sharded", "pack_column_blocks", "unpack_column_blocks"]
+__all__ = ["shard_range", "fft2d_row_sharded", "pack_column_blocks", "unpack_column_blocks",
+           "PeerShardedFft2d"]
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -102,3 +110,113 @@ def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group) -> None:
         as_real(recv).copy_(got)
         return
     dist.all_to_all_single(as_real(recv), as_real(send), group=group)
+
+
+class PeerShardedFft2d:
+    """Row-sharded 2-D FFT, exchange fused into the column pass (C-ABI
+    ``dpp_fft2d_columns_sharded``, include/dpp_b200.h; SURVEY §8(b)
+    ``dpp_fft2d_c2c_fwd_sharded``).
+
+    Collective: every rank of ``group`` constructs it with the same arguments
+    (one process per GPU).  Each rank owns ``slab``, a (batch, n0/P, n1)
+    complex64 row slab, and a flag array; their CUDA IPC handles are
+    exchanged once (``all_gather_object``) and opened, so a call moves data
+    only inside the kernels.  ``barrier="host"`` replaces the device flag
+    barrier by stream sync + ``dist.barrier`` (for debugging)."""
+
+    def __init__(self, n0: int, n1: int, batch: int = 1, group=None, device=None,
+                 barrier: str = "device", timeout_s: float = 30.0):
+        import ctypes as C
+        from . import _lib, ops
+        self._C, self._lib = C, _lib.load()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if barrier not in ("device", "host"):
+            raise ValueError(f"barrier must be 'device' or 'host', got {barrier!r}")
+        if n0 % self.world or n1 % (16 * self.world):
+            raise ValueError(f"{n0} x {n1} does not shard over {self.world} ranks")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n0, self.n1, self.batch, self.device = n0, n1, batch, dev
+        self.barrier_mode, self.timeout_s = barrier, timeout_s
+        self.rows = n0 // self.world
+        self.slab = torch.empty((batch, self.rows, n1), dtype=torch.complex64, device=dev)
+        self.cols = torch.empty((batch, n0, n1 // self.world), dtype=torch.complex64, device=dev)
+        self.flags = torch.zeros(8, dtype=torch.int32, device=dev)
+        self._plan2d = ops.fft_plan(2, n0, n1, batch, dev)
+        self._plan_rows = ops.fft_plan(1, n1, 1, batch * self.rows, dev)
+        self._epoch = 0
+        self._opened: list[int] = []
+        self._slabs = self._exchange(self.slab)
+        self._flag_ptrs = self._exchange(self.flags)
+        P = self._C.c_void_p * self.world
+        self._slab_arr = P(*self._slabs)
+        self._flag_arr = P(*self._flag_ptrs)
+        self._col_arr = P(self.cols.data_ptr(), *([0] * (self.world - 1)))
+
+    def _exchange(self, t: torch.Tensor) -> list[int]:
+        """Pointers, valid in this process, to every rank's copy of ``t``."""
+        C, lib = self._C, self._lib
+        if self.world == 1:
+            return [t.data_ptr()]
+        from ._lib import check
+        handle = C.create_string_buffer(64)
+        off = C.c_uint64()
+        check(lib.dpp_ipc_get_handle(t.data_ptr(), handle, C.byref(off)), "ipc handle")
+        got: list = [None] * self.world
+        dist.all_gather_object(got, (handle.raw, off.value), group=self.group)
+        ptrs = []
+        for j, (h, o) in enumerate(got):
+            if j == self.rank:
+                ptrs.append(t.data_ptr())
+                continue
+            base = C.c_void_p()
+            check(lib.dpp_ipc_open(C.create_string_buffer(h, 64), C.byref(base)), f"ipc open (rank {j})")
+            self._opened.append(base.value)
+            ptrs.append(base.value + o)
+        return ptrs
+
+    def _barrier(self, stream) -> None:
+        from ._lib import check
+        from .ops import stream_handle
+        if self.barrier_mode == "host":
+            (stream or torch.cuda.current_stream(self.device)).synchronize()
+            if self.world > 1:
+                dist.barrier(group=self.group)
+            return
+        self._epoch += 1
+        check(self._lib.dpp_peer_barrier(self._flag_arr, self.world, self.rank, self._epoch, self.timeout_s,
+                                         stream_handle(stream)), "peer barrier")
+
+    def __call__(self, local_rows: torch.Tensor | None = None, transpose_back: bool = True,
+                 stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Forward 2-D FFT of the row-sharded batch.  ``local_rows`` (this
+        rank's (batch, n0/P, n1) rows; None: ``slab`` already holds them) is
+        row-transformed into ``slab``.  Returns ``slab`` (transpose_back: this
+        rank's rows of the result) or ``cols`` (this rank's (batch, n0, n1/P)
+        column block) — buffers owned by this object, overwritten by the next
+        call."""
+        from ._lib import check
+        from .ops import stream_handle
+        src = self.slab if local_rows is None else local_rows
+        if src.dtype != torch.complex64 or src.numel() != self.slab.numel() or not src.is_contiguous():
+            raise ValueError(f"local rows must be contiguous complex64 of {tuple(self.slab.shape)}")
+        self._plan_rows.execute(src, self.slab, self.batch * self.rows, stream)
+        self._barrier(stream)
+        outs = self._slab_arr if transpose_back else self._col_arr
+        check(self._lib.dpp_fft2d_columns_sharded(self._plan2d._h, self._slab_arr, outs, self.world, self.rank,
+                                                   1 if transpose_back else 0, self.batch, stream_handle(stream)),
+              "sharded column pass")
+        self._barrier(stream)
+        return self.slab if transpose_back else self.cols
+
+    def close(self) -> None:
+        for base in self._opened:
+            self._lib.dpp_ipc_close(base)
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
