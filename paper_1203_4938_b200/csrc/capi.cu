@@ -50,6 +50,14 @@ void fft_plan_release(FftPlan* p) {
     delete p->rows;
     p->rows = nullptr;
   }
+  if (p->cols) {
+    fft_plan_release(p->cols);
+    delete p->cols;
+    p->cols = nullptr;
+  }
+  if (p->big_tw) cudaFree(p->big_tw);
+  if (p->big_scratch) cudaFree(p->big_scratch);
+  p->big_tw = p->big_scratch = nullptr;
 }
 
 }  // namespace dpp

@@ -1233,7 +1233,7 @@ int fft1d_plan_init(FftPlan* p) {
              (p->mode == 3 || p->mode == 9) ? (std::string(", ") + std::to_string(p->max_clusters) + " clusters").c_str() : "");
     return DPP_OK;
   }
-  return fail(DPP_ENOTSUP, "1-D transform size 2^%d is above the 2^17 single-pass limit", lg);
+  return fft_large_init(p);
 }
 
 int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s) {
@@ -1247,6 +1247,8 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
     }
   } else if (p->kind == FftPlan::L2X) {
     return fft65536_l2x_execute(p, in, out, batch, s);
+  } else if (p->kind == FftPlan::LARGE) {
+    return fft_large_execute(p, in, out, batch, s);
   } else if (p->kind == FftPlan::CLUSTER) {
     if (p->ws4k) return fft4096_ws_execute(p, in, out, batch, s);
     if (p->ring16k) {

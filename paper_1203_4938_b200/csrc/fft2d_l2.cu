@@ -43,7 +43,28 @@ struct Args {
   int units, tiles_per_image, lag, ring;
   float alpha;         // SPEC: spectrum_u8 scale
   int np, col0, tb;    // PEER: ranks, first column of this rank's block, output to the row slabs
+  const float2* twlo;  // TW: W_N^m for m < 16384 ...
+  const float2* twhi;  //     ... and W_N^(16384 h): W_N^m = twlo[m & 16383] * twhi[m >> 14]
 };
+
+// TW (1-D transforms above 2^17, csrc/fft_large.cu): the four-step twiddle
+// W_N^{r k1} of the column-length (row r) x row-length (column k1) split,
+// applied to the loaded values before the column FFT
+__device__ __forceinline__ float2 tw_big(const Args& a, uint32_t m) {
+  return cmul(__ldg(a.twlo + (m & 16383u)), __ldg(a.twhi + (m >> 14)));
+}
+template <bool TW>
+__device__ __forceinline__ void p1_twiddle(float2 (&v)[16], const Args& a, uint32_t m0, uint32_t step) {
+  if constexpr (TW) {
+    float2 w = tw_big(a, m0);
+    const float2 st = tw_big(a, step);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      v[j] = cmul(v[j], w);
+      w = cmul(w, st);
+    }
+  }
+}
 
 // PEER: one tensor map per rank (row slabs in, row slabs or the local column slab out)
 struct Maps8 {
@@ -61,13 +82,18 @@ __device__ __forceinline__ const CUtensorMap* map_at(const CUtensorMap& m, int) 
 __device__ __forceinline__ const CUtensorMap* map_at(const Maps8& m, int j) { return &m.m[j]; }
 
 // P1, B = 16: thread = one (column, a) sequence over b; no exchange
+template <bool TW = false>
 __device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
-                                       const Args& a, uint64_t keep_pol) {
+                                       const Args& a, uint64_t keep_pol, int colbase = 0) {
   const int col = lane & 15, alo = 2 * warp + (lane >> 4);
+  const int ar = 16 * g + alo;
 #pragma unroll
   for (int bb = 0; bb < 16; ++bb) v[bb] = lds64(b + 8u * swz(16 * bb + alo, col));
+  {
+    const uint32_t kc = (uint32_t)(colbase + col);  // rows 256 bb + ar
+    p1_twiddle<TW>(v, a, (uint32_t)ar * kc, 256u * kc);
+  }
   dft16c(v);  // v[k1]
-  const int ar = 16 * g + alo;
   const float2 wa = __ldg(a.twr + ar);  // W_R^a
   float2 w = wa;
 #pragma unroll
@@ -87,11 +113,16 @@ __device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, in
 // = 16 distinct bank pairs.
 __device__ __forceinline__ int gbeta(int m0) { return (m0 << 2) | ((m0 >> 2) & 1); }
 
+template <bool TW = false>
 __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
-                                       const Args& a, uint64_t keep_pol) {
+                                       const Args& a, uint64_t keep_pol, int colbase = 0) {
   const int alo = warp >> 1, col = 8 * (warp & 1) + (lane & 7), b0 = lane >> 3;
 #pragma unroll
   for (int b1 = 0; b1 < 16; ++b1) v[b1] = lds64(b + 8u * swz(16 * b1 + 4 * b0 + alo, col));
+  {
+    const uint32_t kc = (uint32_t)(colbase + col);  // rows 256 (4 b1 + b0) + 4 g + alo
+    p1_twiddle<TW>(v, a, (uint32_t)(256 * b0 + 4 * g + alo) * kc, 1024u * kc);
+  }
   dft16c(v);  // v[m0]
   {
     const float2 wb = __ldg(a.twr + 256 * b0);  // W64^b0 = W_R^{256 b0}
@@ -141,7 +172,7 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
 // the 256 output rows of its k1 as P sub-boxes into the ranks' row slabs
 // (tb: natural row-sharded output, in place is safe because column block q is
 // touched by rank q only) or one box into the local R x (C/P) column slab.
-template <int B, bool DISCARD, bool SPEC = false, bool PEER = false>
+template <int B, bool DISCARD, bool SPEC = false, bool PEER = false, bool TW = false>
 __global__ void __launch_bounds__(THREADS, 3)
 fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
              const __grid_constant__ typename MapSet<PEER>::type tout, const Args a) {
@@ -279,10 +310,11 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
     const uint32_t b = sbase + (uint32_t)s * (TILE * 8);
     float2* slot = a.scratch + (size_t)(u & (a.ring - 1)) * (16 * R);
     if (pass == 1) {
+      const int colbase = TW ? 16 * (u - (u / a.tiles_per_image) * a.tiles_per_image) : 0;
       if constexpr (B == 16)
-        p1_b16(v, b, warp, lane, g, slot, a, keep_pol);
+        p1_b16<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
       else
-        p1_b64(v, b, warp, lane, g, slot, a, keep_pol);
+        p1_b64<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
     } else {
       if (DISCARD) discard_l2(slot + 4096 * g + 16 * (tid & 255));
       const uint32_t bA = b + offA;
@@ -340,6 +372,8 @@ static int colring_prepare(int* ctas) {
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   DPP_CUDA_CHECK(
@@ -403,7 +437,8 @@ int fft2d_colring_init(FftPlan* p) {
 
 // spec_out != nullptr: fused spectrum_u8 — the column pass writes u8 spectra there
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s, uint8_t* spec_out,
-                          float alpha) {
+                          float alpha, float2* dst, const float2* twlo, const float2* twhi) {
+  if (!dst) dst = data;
   const int64_t R = p->n0, C = p->n1;
   const int B = (int)(R / 256);
   const int64_t units = batch * (C / 16);
@@ -424,7 +459,7 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
     const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch)};
     const uint64_t strides[2] = {(uint64_t)C * 8, (uint64_t)C * 8 * B};
     const uint32_t box[3] = {16, 1, 256};
-    if (int rc = make_tmap_c64_3d(&tout, data, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+    if (int rc = make_tmap_c64_3d(&tout, dst, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
   }
   colring::Args a;
   a.scratch = p->l2_scratch;
@@ -438,12 +473,19 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   a.alpha = alpha;
   a.np = 1;
   a.col0 = a.tb = 0;
+  a.twlo = twlo;
+  a.twhi = twhi;
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
   const int64_t items = 2 * (int64_t)B * units;
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
   const size_t smem = colring_smem(spec_out != nullptr);
-  if (spec_out) {
+  if (twlo) {
+    if (B == 16)
+      colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    else
+      colring::fft_cols_l2w<64, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  } else if (spec_out) {
     if (B == 16)
       colring::fft_cols_l2w<16, true, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
     else
@@ -519,6 +561,7 @@ int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, flo
   a.lag = (int)(units < p->l2_lag ? units : p->l2_lag);
   a.ring = p->l2_ring;
   a.alpha = 0.f;
+  a.twlo = a.twhi = nullptr;
   a.np = np;
   a.col0 = (int)(rank * w);
   a.tb = tb ? 1 : 0;

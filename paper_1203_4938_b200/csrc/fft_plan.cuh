@@ -9,7 +9,7 @@ struct dpp_fft_plan;  // public opaque name (include/dpp_b200.h)
 namespace dpp {
 
 struct FftPlan {
-  enum Kind { SMALL = 1, CLUSTER = 2, L2X = 3 };
+  enum Kind { SMALL = 1, CLUSTER = 2, L2X = 3, LARGE = 4 };
   int rank = 1;
   int64_t n0 = 0, n1 = 0, batch = 0;  // rank 1: n0 points; rank 2: n0 rows x n1 cols
   int device = 0;
@@ -42,6 +42,11 @@ struct FftPlan {
   int ring16k = 0;
   // rank 1, n = 4096: warp-specialised single-CTA kernel (fft4k.cu)
   int ws4k = 0;
+  // rank 1, n > 2^17 (fft_large.cu): transpose, row pass (rows), twiddled column ring (cols)
+  FftPlan* cols = nullptr;
+  float2* big_tw = nullptr;       // W_N^m, m < 16384, then W_N^(16384 h)
+  float2* big_scratch = nullptr;  // in-place calls: big_chunk transforms at a time
+  int64_t big_chunk = 0;
   char desc[256] = {0};
 };
 
@@ -55,7 +60,10 @@ int fft65536_l2x_init(FftPlan* p);
 int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_colring_init(FftPlan* p);
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s,
-                          uint8_t* spec_out = nullptr, float alpha = 0.f);
+                          uint8_t* spec_out = nullptr, float alpha = 0.f, float2* dst = nullptr,
+                          const float2* twlo = nullptr, const float2* twhi = nullptr);
+int fft_large_init(FftPlan* p);
+int fft_large_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, float2* const* outs, int np, int rank,
                                int tb, int64_t batch, cudaStream_t s);
 int fft16k_l2_init(FftPlan* p);

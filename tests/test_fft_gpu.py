@@ -323,3 +323,31 @@ def test_2d_column_pass_variants(cuda, env):
                        timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-5
+
+
+@pytest.mark.parametrize("m,batch", [(18, 4), (19, 2), (20, 2), (22, 1), (25, 1)])
+def test_sizes_above_2e17_vs_oracle(cuda, m, batch):
+    """n > 2^17: transpose + row pass + twiddled column ring (csrc/fft_large.cu);
+    2^25 takes the 16384-row column ring."""
+    n = 1 << m
+    x = complex_signals(300 + m, (batch, n))
+    got = _fft(x, n, cuda)
+    errs = [rel_l2(g, r) for g, r in zip(got, fo.fft_rows(x))]
+    assert max(errs) <= tol(n), (n, max(errs))
+
+
+def test_large_in_place_chunks_match_out_of_place(cuda):
+    """In-place calls stage big_chunk transforms through the plan's scratch
+    (32 at 2^20); 40 transforms cross a chunk boundary."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    n, batch = 1 << 20, 40
+    x = torch.from_numpy(complex_signals(5, (batch, n))).to(cuda)
+    ref = ops.fft_forward(x, n)
+    y = x.clone()
+    ops.fft_forward(y, n, out=y)
+    assert torch.equal(y, ref)
+    got = ref[[0, 39]].cpu().numpy()
+    want = fo.fft_rows(x[[0, 39]].cpu().numpy())
+    assert max(rel_l2(g, r) for g, r in zip(got, want)) <= tol(n)
