@@ -386,22 +386,32 @@ def run_ours(args) -> None:
             def step2d():
                 ops.fft2d_forward(x2, n2d, n2d, out=x2)
         else:
+            import torch.distributed as dist
+            sh, peer_err = None, None
             try:
                 from paper_1203_4938_b200.distributed import PeerShardedFft2d
-                sh = PeerShardedFft2d(n2d, n2d, 1)
+                sh = PeerShardedFft2d(n2d, n2d, 1, timeout_s=10.0)
+            except Exception as exc:  # no IPC / peer access
+                peer_err = exc
+            agree = torch.tensor([0 if sh is None else 1], dtype=torch.int32, device=dev)
+            dist.all_reduce(agree, op=dist.ReduceOp.MIN)  # every rank takes the same path
+            if int(agree.item()) == 1:
                 sh.slab.copy_(torch.randn((1, rows, n2d), dtype=torch.complex64, device=dev, generator=gen))
 
                 def step2d():
                     sh(None, transpose_back=True)
                 a2a_passes = 2  # peer loads of the column block + peer stores of the results
                 exchange = "row-sharded, exchange fused into the column pass (peer HBM over NVLink), row-slab output"
-            except Exception as exc:  # no IPC / peer access: the NCCL composition
+            else:  # the NCCL composition
+                if sh is not None:
+                    sh.close()
                 from paper_1203_4938_b200.distributed import fft2d_row_sharded
                 x2 = torch.randn((rows, n2d), dtype=torch.complex64, device=dev, generator=gen)
 
                 def step2d():
                     fft2d_row_sharded(x2, n2d, transpose_back=False)
-                exchange = f"row-sharded, NCCL all-to-all, column-slab output (peer path: {type(exc).__name__})"
+                why = type(peer_err).__name__ if peer_err is not None else "another rank"
+                exchange = f"row-sharded, NCCL all-to-all, column-slab output (peer path unavailable: {why})"
 
         for _ in range(2):
             step2d()
