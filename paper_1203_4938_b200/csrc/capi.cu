@@ -2,13 +2,20 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 
 #include "common.cuh"
 #include "fft_plan.cuh"
 
+// The plan owns mutable device state (L2 exchange rings, their counters, the
+// large-size scratch) that consecutive executions reuse in stream order: each
+// execution waits for the previous one's completion event and records its
+// own.  `mu` makes that wait/launch/record sequence atomic across host
+// threads, so one plan can be shared by threads and streams.
 struct dpp_fft_plan {
   dpp::FftPlan impl;
+  std::mutex mu;
 };
 
 namespace dpp {
@@ -109,6 +116,7 @@ int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* 
   auto s = static_cast<cudaStream_t>(stream);
   const auto* src = reinterpret_cast<const float2*>(in);
   auto* dst = reinterpret_cast<float2*>(out);
+  std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
   return plan->impl.rank == 1 ? dpp::fft1d_execute(&plan->impl, src, dst, batch, s)
                               : dpp::fft2d_execute(&plan->impl, src, dst, batch, s);
 }
@@ -125,6 +133,7 @@ int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, vo
   if (batch < 0 || batch > plan->impl.batch)
     return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch,
                      (long long)plan->impl.batch);
+  std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
   return dpp::fft2d_columns_execute(&plan->impl, reinterpret_cast<float2*>(data), batch,
                                     static_cast<cudaStream_t>(stream));
 }
@@ -143,6 +152,7 @@ int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* 
   if (!in || !out || !work) return dpp::fail(DPP_EINVAL, "NULL data pointer");
   auto s = static_cast<cudaStream_t>(stream);
   auto* w = reinterpret_cast<float2*>(work);
+  std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
   if (int rc = dpp::fft4096_ws_execute_u8(p.rows, in, w, batch * p.n0, s)) return rc;
   return dpp::fft2d_colring_execute(&p, w, batch, s, out, alpha);
 }
@@ -151,6 +161,7 @@ int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slab
                               int rank, int transpose_back, int64_t batch, void* stream) {
   if (!plan || !slabs || !outs) return dpp::fail(DPP_EINVAL, "NULL argument to dpp_fft2d_columns_sharded");
   if (plan->impl.rank != 2) return dpp::fail(DPP_EINVAL, "the sharded column pass needs a rank-2 plan");
+  std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
   return dpp::fft2d_colring_execute_peer(&plan->impl, reinterpret_cast<const float2* const*>(slabs),
                                          reinterpret_cast<float2* const*>(outs), nranks, rank, transpose_back, batch,
                                          static_cast<cudaStream_t>(stream));

@@ -351,3 +351,40 @@ def test_large_in_place_chunks_match_out_of_place(cuda):
     got = ref[[0, 39]].cpu().numpy()
     want = fo.fft_rows(x[[0, 39]].cpu().numpy())
     assert max(rel_l2(g, r) for g, r in zip(got, want)) <= tol(n)
+
+
+@pytest.mark.parametrize("n", [4096, 16384, 65536, 1 << 18])
+def test_one_plan_shared_by_threads_and_streams(cuda, n):
+    """Plans own their exchange rings; the plan lock serialises the
+    wait/launch/record sequence so threads on separate streams can share one
+    plan (the engine's pool threads do)."""
+    import threading
+
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    batch, nthreads = 16, 6
+    xs = [torch.from_numpy(complex_signals(40 + i, (batch, n))).to(cuda) for i in range(nthreads)]
+    ref = [ops.fft_forward(x, n) for x in xs]
+    torch.cuda.synchronize()
+    outs = [torch.empty_like(x) for x in xs]
+    streams = [torch.cuda.Stream(cuda) for _ in range(nthreads)]
+    errors = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                for _ in range(5):
+                    ops.fft_forward(xs[i], n, out=outs[i], stream=streams[i])
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(nthreads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for o, r in zip(outs, ref):
+        assert torch.equal(o, r)
