@@ -218,6 +218,31 @@ int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_
 int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const double* uniforms,
                int max_iter, float* centroids_out, double* trace, int* iterations, void* stream);
 
+/* The same trainer over points sharded across ranks (one process per GPU,
+ * SURVEY §8(f) row 2 multi-GPU): each rank wraps its contiguous slice of the
+ * training blocks in a shard; the driver (kmeans.py, kmeans_sharded) does one
+ * small all-reduce per k-means++ step and one per Lloyd iteration.
+ *   seed:   d2 = min(d2, |p - centroid|^2) (first != 0: initialise);
+ *           *total (host) = the shard's d2 sum in block order.
+ *   pick:   the point whose inclusive d2 prefix first exceeds `target`
+ *           (searchsorted 'right', imgc.py:245), or local_index when >= 0;
+ *           copied to centroid_out (device, 16 doubles); *picked = its index.
+ *   assign: nearest centroid (first minimum) per point; acc (device,
+ *           k*16 + k + 2 doubles) = [coordinate sums][counts][changed][SSE].
+ *   far:    *packed (device int64) = max over the shard of
+ *           (f32 bits of the distance to the assigned centroid) << 32 |
+ *           (0xffffffff - global index), base = the shard's first index.
+ *   set_assign: the reseeded point joins `cluster`. */
+typedef struct dpp_kmeans_shard dpp_kmeans_shard;
+int dpp_kmeans_shard_create(dpp_kmeans_shard** shard, const double* pts, int64_t n, int k, void* stream);
+int dpp_kmeans_shard_seed(dpp_kmeans_shard* shard, const double* centroid, int first, double* total);
+int dpp_kmeans_shard_pick(dpp_kmeans_shard* shard, double target, int64_t local_index, double* centroid_out,
+                          int64_t* picked);
+int dpp_kmeans_shard_assign(dpp_kmeans_shard* shard, const double* cents, double* acc);
+int dpp_kmeans_shard_far(dpp_kmeans_shard* shard, const double* cents, int64_t base, int64_t* packed);
+int dpp_kmeans_shard_set_assign(dpp_kmeans_shard* shard, int64_t local_index, int cluster);
+void dpp_kmeans_shard_destroy(dpp_kmeans_shard* shard);
+
 /* C5 chain adapters (node bodies in apps/chain.py):
  *   to_complex:  y[i] = ((float)x[i], 0)          n u8 -> n complex64 (n % 4 == 0)
  *   spectrum_u8: y[i] = (u8)clamp(floor(alpha*log(1+|z[i]|)), 0, 255)   (n even) */

@@ -54,6 +54,13 @@ SIGNATURES = {
     "dpp_ipc_get_handle": (_int, [_vp, _vp, C.POINTER(C.c_uint64)]),
     "dpp_ipc_open": (_int, [_vp, C.POINTER(_vp)]),
     "dpp_ipc_close": (_int, [_vp]),
+    "dpp_kmeans_shard_create": (_int, [C.POINTER(_vp), _vp, _i64, _int, _vp]),
+    "dpp_kmeans_shard_seed": (_int, [_vp, _vp, _int, C.POINTER(C.c_double)]),
+    "dpp_kmeans_shard_pick": (_int, [_vp, C.c_double, _i64, _vp, C.POINTER(_i64)]),
+    "dpp_kmeans_shard_assign": (_int, [_vp, _vp, _vp]),
+    "dpp_kmeans_shard_far": (_int, [_vp, _vp, _i64, _vp]),
+    "dpp_kmeans_shard_set_assign": (_int, [_vp, _i64, _int]),
+    "dpp_kmeans_shard_destroy": (None, [_vp]),
     "dpp_peer_barrier": (_int, [C.POINTER(_vp), _int, _int, _int, C.c_double, _vp]),
 }
 

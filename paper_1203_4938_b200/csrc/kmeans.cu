@@ -89,6 +89,51 @@ __global__ void kpp_pick(const double* __restrict__ d2, int64_t n, const double*
   (void)total_s;
 }
 
+// shard-local pick: the point whose inclusive prefix of d2 first exceeds
+// `target` (the global target minus the totals of the ranks before this one)
+__global__ void kpp_pick_target(const double* __restrict__ d2, int64_t n, const double* __restrict__ block_sums,
+                                int nblocks, int block, double target, const double* __restrict__ pts,
+                                double* __restrict__ centroid, int64_t* __restrict__ pick_out) {
+  __shared__ int64_t pick_s;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    int b = 0;
+    for (; b < nblocks - 1; ++b) {
+      if (acc + block_sums[b] > target) break;
+      acc += block_sums[b];
+    }
+    const int64_t lo = (int64_t)b * block, hi = lo + block < n ? lo + block : n;
+    int64_t pick = hi - 1;
+    for (int64_t i = lo; i < hi; ++i) {
+      acc += d2[i];
+      if (acc > target) { pick = i; break; }
+    }
+    pick_s = pick;
+    *pick_out = pick;
+  }
+  __syncthreads();
+  if (threadIdx.x < KD) centroid[threadIdx.x] = pts[pick_s * KD + threadIdx.x];
+}
+
+// sequential (block-order) total of the block sums, as kpp_pick forms it
+__global__ void kpp_total(const double* __restrict__ block_sums, int nblocks, double* __restrict__ total) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (int b = 0; b < nblocks; ++b) t += block_sums[b];
+  *total = t;
+}
+
+// shard accumulator for the all-reduce: [k*16 sums][k counts][changed][sse] in binary64
+__global__ void pack_acc(const double* __restrict__ sums, const unsigned long long* __restrict__ counts,
+                         const unsigned long long* __restrict__ changed, const double* __restrict__ sse, int k,
+                         double* __restrict__ acc) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * KD) acc[e] = sums[e];
+  else if (e < k * KD + k) acc[e] = (double)counts[e - k * KD];
+  else if (e == k * KD + k) acc[e] = (double)*changed;
+  else if (e == k * KD + k + 1) acc[e] = *sse;
+}
+
 // nearest centroid (first minimum), counts changes vs previous assignment,
 // accumulates per-cluster sums/counts in shared memory then globally
 __global__ void lloyd_assign(const double* __restrict__ pts, int64_t n, const double* __restrict__ cents, int k,
@@ -139,20 +184,175 @@ __global__ void lloyd_means(double* __restrict__ cents, const double* __restrict
   if (e < k * KD && counts[e / KD]) cents[e] = sums[e] / (double)counts[e / KD];
 }
 
-// farthest point from its assigned centroid (for empty-cluster reseeding)
+// farthest point from its assigned centroid (for empty-cluster reseeding);
+// `base` = global index of the shard's first point
 __global__ void far_point(const double* __restrict__ pts, int64_t n, const double* __restrict__ cents,
-                          const int32_t* __restrict__ assign, unsigned long long* __restrict__ best) {
+                          const int32_t* __restrict__ assign, unsigned long long* __restrict__ best,
+                          int64_t base = 0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double d = dist2(pts + i * KD, cents + (int64_t)assign[i] * KD);
   // pack (distance as f32 bits, inverted index): atomicMax picks the largest
   // distance and, among equal ones, the lowest index (np.argmax)
-  atomicMax(best, ((unsigned long long)__float_as_uint((float)d) << 32) | (0xffffffffu - (uint32_t)i));
+  atomicMax(best, ((unsigned long long)__float_as_uint((float)d) << 32) | (0xffffffffu - (uint32_t)(base + i)));
 }
+
+// one shard of a row-sharded k-means (multi-GPU): the
+// device buffers of the single-GPU trainer for this rank's points; the
+// driver (paper_1203_4938_b200/kmeans.py, kmeans_sharded) combines shards
+// with one all-reduce per seeding step / Lloyd iteration
+struct KmShard {
+  const double* pts = nullptr;
+  int64_t n = 0;
+  int k = 0, nb = 0;
+  cudaStream_t s = nullptr;
+  double *d2 = nullptr, *bsum = nullptr, *sums = nullptr, *sse = nullptr, *total = nullptr;
+  int32_t* assign = nullptr;
+  unsigned long long *counts = nullptr, *changed = nullptr, *far = nullptr;
+  int64_t* pick = nullptr;
+  void release() {
+    for (void* ptr : {(void*)d2, (void*)bsum, (void*)sums, (void*)sse, (void*)total, (void*)assign, (void*)counts,
+                      (void*)changed, (void*)far, (void*)pick})
+      if (ptr) cudaFree(ptr);
+  }
+};
 
 }  // namespace dpp
 
+struct dpp_kmeans_shard {
+  dpp::KmShard impl;
+};
+
 extern "C" {
+
+int dpp_kmeans_shard_create(dpp_kmeans_shard** shard, const double* pts, int64_t n, int k, void* stream) {
+  using namespace dpp;
+  if (!shard) return fail(DPP_EINVAL, "NULL shard pointer");
+  *shard = nullptr;
+  if (n < 0 || n > 0x7fffffffLL) return fail(DPP_EINVAL, "shard of %lld points", (long long)n);
+  if (k < 1 || k > 256) return fail(DPP_EINVAL, "codebook size must be in 1..256");
+  auto* h = new dpp_kmeans_shard();
+  KmShard& m = h->impl;
+  m.pts = pts;
+  m.n = n;
+  m.k = k;
+  m.nb = (int)((n + 255) / 256);
+  m.s = static_cast<cudaStream_t>(stream);
+  const size_t nn = (size_t)(n > 0 ? n : 1), nbb = (size_t)(m.nb > 0 ? m.nb : 1);
+  bool ok = cudaMalloc(&m.d2, nn * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&m.bsum, nbb * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&m.sums, (size_t)k * KD * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&m.sse, sizeof(double)) == cudaSuccess && cudaMalloc(&m.total, sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&m.assign, nn * sizeof(int32_t)) == cudaSuccess &&
+            cudaMalloc(&m.counts, k * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMalloc(&m.changed, sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMalloc(&m.far, sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMalloc(&m.pick, sizeof(int64_t)) == cudaSuccess;
+  if (!ok || cudaMemsetAsync(m.assign, 0xff, nn * sizeof(int32_t), m.s) != cudaSuccess) {
+    m.release();
+    delete h;
+    return fail(DPP_ECUDA, "k-means shard allocation failed");
+  }
+  *shard = h;
+  return DPP_OK;
+}
+
+// k-means++ step on the shard: d2 = min(d2, |p - centroid|^2) (first: init);
+// *total (host) = the shard's sum of d2 in block order
+int dpp_kmeans_shard_seed(dpp_kmeans_shard* shard, const double* centroid, int first, double* total) {
+  using namespace dpp;
+  if (!shard || !centroid || !total) return fail(DPP_EINVAL, "NULL argument to dpp_kmeans_shard_seed");
+  KmShard& m = shard->impl;
+  if (m.n == 0) {
+    *total = 0.0;
+    return DPP_OK;
+  }
+  kpp_update<<<m.nb, 256, 0, m.s>>>(m.pts, m.n, centroid, m.d2, m.bsum, first);
+  kpp_total<<<1, 32, 0, m.s>>>(m.bsum, m.nb, m.total);
+  DPP_LAUNCH_CHECK("k-means++ shard update");
+  DPP_CUDA_CHECK(cudaMemcpyAsync(total, m.total, sizeof(double), cudaMemcpyDeviceToHost, m.s));
+  DPP_CUDA_CHECK(cudaStreamSynchronize(m.s));
+  return DPP_OK;
+}
+
+// the shard's pick for a local target (local_index < 0), or the given local
+// index (degenerate all-zero d2: uniform pick); copies the point to
+// centroid_out (device, 16 doubles) and returns the local index
+int dpp_kmeans_shard_pick(dpp_kmeans_shard* shard, double target, int64_t local_index, double* centroid_out,
+                          int64_t* picked) {
+  using namespace dpp;
+  if (!shard || !centroid_out || !picked) return fail(DPP_EINVAL, "NULL argument to dpp_kmeans_shard_pick");
+  KmShard& m = shard->impl;
+  if (m.n == 0) return fail(DPP_EINVAL, "pick from an empty shard");
+  if (local_index >= 0) {
+    if (local_index >= m.n) return fail(DPP_EINVAL, "local index %lld outside the shard", (long long)local_index);
+    DPP_CUDA_CHECK(cudaMemcpyAsync(centroid_out, m.pts + local_index * KD, KD * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, m.s));
+    *picked = local_index;
+    return DPP_OK;
+  }
+  kpp_pick_target<<<1, 32, 0, m.s>>>(m.d2, m.n, m.bsum, m.nb, 256, target, m.pts, centroid_out, m.pick);
+  DPP_LAUNCH_CHECK("k-means++ shard pick");
+  DPP_CUDA_CHECK(cudaMemcpyAsync(picked, m.pick, sizeof(int64_t), cudaMemcpyDeviceToHost, m.s));
+  DPP_CUDA_CHECK(cudaStreamSynchronize(m.s));
+  return DPP_OK;
+}
+
+// Lloyd assignment on the shard: acc (device, k*16 + k + 2 doubles) =
+// [per-cluster coordinate sums][counts][assignments changed][sum of squared distances]
+int dpp_kmeans_shard_assign(dpp_kmeans_shard* shard, const double* cents, double* acc) {
+  using namespace dpp;
+  if (!shard || !cents || !acc) return fail(DPP_EINVAL, "NULL argument to dpp_kmeans_shard_assign");
+  KmShard& m = shard->impl;
+  const int k = m.k;
+  const int tot = k * KD + k + 2;
+  if (m.n == 0) {
+    DPP_CUDA_CHECK(cudaMemsetAsync(acc, 0, tot * sizeof(double), m.s));
+    return DPP_OK;
+  }
+  const size_t shm = (size_t)k * KD * 2 * sizeof(double) + k * sizeof(unsigned int);
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  DPP_CUDA_CHECK(cudaMemsetAsync(m.sums, 0, (size_t)k * KD * sizeof(double), m.s));
+  DPP_CUDA_CHECK(cudaMemsetAsync(m.counts, 0, k * sizeof(unsigned long long), m.s));
+  DPP_CUDA_CHECK(cudaMemsetAsync(m.changed, 0, sizeof(unsigned long long), m.s));
+  DPP_CUDA_CHECK(cudaMemsetAsync(m.sse, 0, sizeof(double), m.s));
+  lloyd_assign<<<m.nb, 256, shm, m.s>>>(m.pts, m.n, cents, k, m.assign, m.sums, m.counts, m.changed, m.sse);
+  pack_acc<<<(tot + 255) / 256, 256, 0, m.s>>>(m.sums, m.counts, m.changed, m.sse, k, acc);
+  DPP_LAUNCH_CHECK("lloyd shard assign");
+  return DPP_OK;
+}
+
+// farthest point of the shard from its assigned centroid, packed as in
+// far_point with global indices (base = the shard's first global index);
+// *packed (device int64) receives the shard maximum (0 for an empty shard)
+int dpp_kmeans_shard_far(dpp_kmeans_shard* shard, const double* cents, int64_t base, int64_t* packed) {
+  using namespace dpp;
+  if (!shard || !cents || !packed) return fail(DPP_EINVAL, "NULL argument to dpp_kmeans_shard_far");
+  KmShard& m = shard->impl;
+  DPP_CUDA_CHECK(cudaMemsetAsync(packed, 0, sizeof(int64_t), m.s));
+  if (m.n == 0) return DPP_OK;
+  far_point<<<m.nb, 256, 0, m.s>>>(m.pts, m.n, cents, m.assign, reinterpret_cast<unsigned long long*>(packed), base);
+  DPP_LAUNCH_CHECK("far point");
+  return DPP_OK;
+}
+
+// an empty cluster reseeded at a point of this shard: the point joins it
+int dpp_kmeans_shard_set_assign(dpp_kmeans_shard* shard, int64_t local_index, int cluster) {
+  using namespace dpp;
+  if (!shard || local_index < 0 || local_index >= shard->impl.n)
+    return fail(DPP_EINVAL, "bad dpp_kmeans_shard_set_assign arguments");
+  KmShard& m = shard->impl;
+  int32_t c = cluster;
+  DPP_CUDA_CHECK(cudaMemcpyAsync(m.assign + local_index, &c, sizeof(int32_t), cudaMemcpyHostToDevice, m.s));
+  DPP_CUDA_CHECK(cudaStreamSynchronize(m.s));
+  return DPP_OK;
+}
+
+void dpp_kmeans_shard_destroy(dpp_kmeans_shard* shard) {
+  if (!shard) return;
+  shard->impl.release();
+  delete shard;
+}
 
 int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const double* uniforms, int max_iter,
                float* centroids_out, double* trace, int* iterations, void* stream) {
