@@ -18,6 +18,23 @@ struct dpp_fft_plan {
   std::mutex mu;
 };
 
+namespace {
+// Executions may come from threads that never touched the runtime (no current
+// context: the driver-API tensor-map encode would fail with
+// CUDA_ERROR_INVALID_CONTEXT): make the plan's device current for the call
+// and restore the caller's device afterwards.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
 namespace dpp {
 
 static thread_local char g_last_error[1024] = "";
@@ -117,6 +134,7 @@ int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* 
   const auto* src = reinterpret_cast<const float2*>(in);
   auto* dst = reinterpret_cast<float2*>(out);
   std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
+  DeviceScope dev_scope(plan->impl.device);
   return plan->impl.rank == 1 ? dpp::fft1d_execute(&plan->impl, src, dst, batch, s)
                               : dpp::fft2d_execute(&plan->impl, src, dst, batch, s);
 }
@@ -134,6 +152,7 @@ int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, vo
     return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch,
                      (long long)plan->impl.batch);
   std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
+  DeviceScope dev_scope(plan->impl.device);
   return dpp::fft2d_columns_execute(&plan->impl, reinterpret_cast<float2*>(data), batch,
                                     static_cast<cudaStream_t>(stream));
 }
@@ -153,6 +172,7 @@ int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* 
   auto s = static_cast<cudaStream_t>(stream);
   auto* w = reinterpret_cast<float2*>(work);
   std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
+  DeviceScope dev_scope(plan->impl.device);
   if (int rc = dpp::fft4096_ws_execute_u8(p.rows, in, w, batch * p.n0, s)) return rc;
   return dpp::fft2d_colring_execute(&p, w, batch, s, out, alpha);
 }
@@ -162,6 +182,7 @@ int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slab
   if (!plan || !slabs || !outs) return dpp::fail(DPP_EINVAL, "NULL argument to dpp_fft2d_columns_sharded");
   if (plan->impl.rank != 2) return dpp::fail(DPP_EINVAL, "the sharded column pass needs a rank-2 plan");
   std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
+  DeviceScope dev_scope(plan->impl.device);
   return dpp::fft2d_colring_execute_peer(&plan->impl, reinterpret_cast<const float2* const*>(slabs),
                                          reinterpret_cast<float2* const*>(outs), nranks, rank, transpose_back, batch,
                                          static_cast<cudaStream_t>(stream));
