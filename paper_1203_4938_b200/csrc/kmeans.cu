@@ -364,20 +364,34 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   if (n > 0x7fffffffLL) return fail(DPP_EINVAL, "too many training blocks");
   const int T = 256;
   const int nb = (int)((n + T - 1) / T);
-  double *d2, *bsum, *cents, *sums, *sse;
-  int32_t* assign;
-  unsigned long long *counts, *changed, *far;
-  int64_t* pick;
-  DPP_CUDA_CHECK(cudaMallocAsync(&d2, n * sizeof(double), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&bsum, nb * sizeof(double), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&cents, (size_t)k * KD * sizeof(double), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&sums, (size_t)k * KD * sizeof(double), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&sse, sizeof(double), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&assign, n * sizeof(int32_t), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&counts, k * sizeof(unsigned long long), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&changed, sizeof(unsigned long long), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&far, sizeof(unsigned long long), s));
-  DPP_CUDA_CHECK(cudaMallocAsync(&pick, sizeof(int64_t), s));
+  double *d2 = nullptr, *bsum = nullptr, *cents = nullptr, *sums = nullptr, *sse = nullptr;
+  int32_t* assign = nullptr;
+  unsigned long long *counts = nullptr, *changed = nullptr, *far = nullptr;
+  int64_t* pick = nullptr;
+  // every exit path (errors included) returns the scratch to the pool
+  struct Release {
+    std::vector<void*> ptrs;
+    cudaStream_t s;
+    ~Release() {
+      for (void* ptr : ptrs)
+        if (ptr) cudaFreeAsync(ptr, s);
+    }
+  } release{{}, s};
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, s);
+    release.ptrs.push_back(*ptr);
+    return e;
+  };
+  DPP_CUDA_CHECK(alloc(&d2, n * sizeof(double)));
+  DPP_CUDA_CHECK(alloc(&bsum, nb * sizeof(double)));
+  DPP_CUDA_CHECK(alloc(&cents, (size_t)k * KD * sizeof(double)));
+  DPP_CUDA_CHECK(alloc(&sums, (size_t)k * KD * sizeof(double)));
+  DPP_CUDA_CHECK(alloc(&sse, sizeof(double)));
+  DPP_CUDA_CHECK(alloc(&assign, n * sizeof(int32_t)));
+  DPP_CUDA_CHECK(alloc(&counts, k * sizeof(unsigned long long)));
+  DPP_CUDA_CHECK(alloc(&changed, sizeof(unsigned long long)));
+  DPP_CUDA_CHECK(alloc(&far, sizeof(unsigned long long)));
+  DPP_CUDA_CHECK(alloc(&pick, sizeof(int64_t)));
 
   // k-means++ seeding
   DPP_CUDA_CHECK(cudaMemcpyAsync(cents, pts + first_pick * KD, KD * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -439,9 +453,6 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   for (size_t e = 0; e < hc.size(); ++e) hf[e] = (float)hc[e];
   DPP_CUDA_CHECK(cudaMemcpyAsync(centroids_out, hf.data(), hf.size() * sizeof(float), cudaMemcpyHostToDevice, s));
   DPP_CUDA_CHECK(cudaStreamSynchronize(s));
-  for (void* ptr : {(void*)d2, (void*)bsum, (void*)cents, (void*)sums, (void*)sse, (void*)assign, (void*)counts,
-                    (void*)changed, (void*)far, (void*)pick})
-    cudaFreeAsync(ptr, s);
   return DPP_OK;
 }
 
