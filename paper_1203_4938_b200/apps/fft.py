@@ -19,6 +19,8 @@ document also runs on the reference engine (slowly) and names its meaning.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -285,7 +287,7 @@ def fft_batch(signals, n: int | None = None, backend: CudaBackend | None = None,
     return _unstream(out, shape, isinstance(out, DeviceStream))
 
 
-_PIPE_CHUNK_BYTES = 128 << 20
+_PIPE_CHUNK_BYTES = int(os.environ.get("DPP_PIPE_CHUNK_MB", "128")) << 20
 _pipes: dict = {}
 
 
