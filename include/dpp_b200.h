@@ -133,6 +133,23 @@ int dpp_ipc_close(void* base);
  * every slot of its own (acquire).  Traps after timeout_s instead of hanging. */
 int dpp_peer_barrier(int* const* flags, int nranks, int rank, int epoch, double timeout_s, void* stream);
 
+/* The whole row-sharded transform in one call (SURVEY §8(b)
+ * `dpp_fft2d_c2c_fwd_sharded`; the peer group replaces the NCCL communicator
+ * of that sketch: no collective library on the data path).  A group holds
+ * every rank's peer-mapped row slab (batch x n0/P x n1 complex64) and flag
+ * array (int32[8], zeroed) — slabs[rank]/flags[rank] are this rank's own —
+ * and the barrier epoch.  The call: row pass of rows_in (NULL: the slab
+ * already holds the rows) into slabs[rank], barrier, fused column/exchange
+ * pass, barrier.  transpose_back != 0: the result is this rank's rows in
+ * slabs[rank] (`out` unused); else this rank's batch x n0 x (n1/P) column
+ * slab in `out`.  All ranks call it with the same plan shape and batch. */
+typedef struct dpp_peer_group dpp_peer_group;
+int dpp_peer_group_create(dpp_peer_group** group, int nranks, int rank, float* const* slabs, int* const* flags,
+                          double timeout_s);
+void dpp_peer_group_destroy(dpp_peer_group* group);
+int dpp_fft2d_c2c_fwd_sharded(const dpp_fft_plan* plan, dpp_peer_group* group, const float* rows_in, float* out,
+                              int transpose_back, int64_t batch, void* stream);
+
 /* The reference's quadratic oracle naive_dft (apps/fft.py:32-42) on the
  * device: binary64 accumulation, rounded to complex64; `batch` signals of n. */
 int dpp_naive_dft(const float* x, float* y, int64_t n, int64_t batch, void* stream);

@@ -61,6 +61,9 @@ SIGNATURES = {
     "dpp_kmeans_shard_far": (_int, [_vp, _vp, _i64, _vp]),
     "dpp_kmeans_shard_set_assign": (_int, [_vp, _i64, _int]),
     "dpp_kmeans_shard_destroy": (None, [_vp]),
+    "dpp_peer_group_create": (_int, [C.POINTER(_vp), _int, _int, C.POINTER(_vp), C.POINTER(_vp), C.c_double]),
+    "dpp_peer_group_destroy": (None, [_vp]),
+    "dpp_fft2d_c2c_fwd_sharded": (_int, [_vp, _vp, _vp, _vp, _int, _i64, _vp]),
     "dpp_peer_barrier": (_int, [C.POINTER(_vp), _int, _int, _int, C.c_double, _vp]),
 }
 

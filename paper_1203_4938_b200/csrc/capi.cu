@@ -188,6 +188,76 @@ int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slab
                                          static_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------------------
+// SURVEY §8(b) `dpp_fft2d_c2c_fwd_sharded`: the whole row-sharded transform in
+// one call over a peer group (the mapped slabs and flag arrays of every rank)
+
+struct dpp_peer_group {
+  int nranks = 0, rank = 0;
+  float* slabs[8] = {nullptr};
+  int* flags[8] = {nullptr};
+  double timeout_s = 30.0;
+  int epoch = 0;
+  std::mutex mu;
+};
+
+int dpp_peer_group_create(dpp_peer_group** group, int nranks, int rank, float* const* slabs, int* const* flags,
+                          double timeout_s) {
+  if (!group) return dpp::fail(DPP_EINVAL, "NULL group pointer");
+  *group = nullptr;
+  if (nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks || !slabs || !flags)
+    return dpp::fail(DPP_EINVAL, "bad peer group (%d ranks, rank %d)", nranks, rank);
+  auto* g = new (std::nothrow) dpp_peer_group();
+  if (!g) return dpp::fail(DPP_EINVAL, "out of host memory");
+  g->nranks = nranks;
+  g->rank = rank;
+  g->timeout_s = timeout_s > 0 ? timeout_s : 30.0;
+  for (int j = 0; j < nranks; ++j) {
+    if (!slabs[j] || !flags[j]) {
+      delete g;
+      return dpp::fail(DPP_EINVAL, "NULL slab or flag pointer for rank %d", j);
+    }
+    g->slabs[j] = slabs[j];
+    g->flags[j] = flags[j];
+  }
+  *group = g;
+  return DPP_OK;
+}
+
+void dpp_peer_group_destroy(dpp_peer_group* group) { delete group; }
+
+int dpp_fft2d_c2c_fwd_sharded(const dpp_fft_plan* plan, dpp_peer_group* group, const float* rows_in, float* out,
+                              int transpose_back, int64_t batch, void* stream) {
+  if (!plan || !group) return dpp::fail(DPP_EINVAL, "NULL plan or peer group");
+  const dpp::FftPlan& p = plan->impl;
+  if (p.rank != 2 || !p.rows) return dpp::fail(DPP_EINVAL, "the sharded transform needs a rank-2 plan");
+  if (batch < 0 || batch > p.batch)
+    return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch, (long long)p.batch);
+  if (!transpose_back && !out) return dpp::fail(DPP_EINVAL, "column-slab output needs `out`");
+  if (batch == 0) return DPP_OK;
+  const int P = group->nranks;
+  if (p.n0 % P) return dpp::fail(DPP_EINVAL, "%lld rows do not split over %d ranks", (long long)p.n0, P);
+  auto s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
+  std::lock_guard<std::mutex> gg(group->mu);
+  DeviceScope dev_scope(p.device);
+  float2* slab = reinterpret_cast<float2*>(group->slabs[group->rank]);
+  const float2* src = rows_in ? reinterpret_cast<const float2*>(rows_in) : slab;
+  // 1. row pass of this rank's rows into its (peer-visible) slab
+  if (int rc = dpp::fft1d_execute(p.rows, src, slab, batch * (p.n0 / P), s)) return rc;
+  // 2. every slab is row-transformed
+  if (int rc = dpp_peer_barrier(group->flags, P, group->rank, ++group->epoch, group->timeout_s, stream)) return rc;
+  // 3. column pass with the exchange fused in
+  float* col_out[8] = {reinterpret_cast<float*>(out)};
+  if (int rc = dpp::fft2d_colring_execute_peer(&p, reinterpret_cast<const float2* const*>(group->slabs),
+                                               reinterpret_cast<float2* const*>(transpose_back ? group->slabs
+                                                                                               : col_out),
+                                               P, group->rank, transpose_back, batch, s))
+    return rc;
+  // 4. no rank reuses its slab while peers still read or write it
+  return dpp_peer_barrier(group->flags, P, group->rank, ++group->epoch, group->timeout_s, stream);
+}
+
 void dpp_fft_plan_destroy(dpp_fft_plan* plan) {
   if (!plan) return;
   dpp::fft_plan_release(&plan->impl);

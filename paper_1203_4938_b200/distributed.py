@@ -153,6 +153,10 @@ class PeerShardedFft2d:
         self._slab_arr = P(*self._slabs)
         self._flag_arr = P(*self._flag_ptrs)
         self._col_arr = P(self.cols.data_ptr(), *([0] * (self.world - 1)))
+        self._group = C.c_void_p()
+        from ._lib import check
+        check(self._lib.dpp_peer_group_create(C.byref(self._group), self.world, self.rank, self._slab_arr,
+                                              self._flag_arr, float(timeout_s)), "peer group")
 
     def _exchange(self, t: torch.Tensor) -> list[int]:
         """Pointers, valid in this process, to every rank's copy of ``t``."""
@@ -201,6 +205,12 @@ class PeerShardedFft2d:
         src = self.slab if local_rows is None else local_rows
         if src.dtype != torch.complex64 or src.numel() != self.slab.numel() or not src.is_contiguous():
             raise ValueError(f"local rows must be contiguous complex64 of {tuple(self.slab.shape)}")
+        if self.barrier_mode == "device":
+            # one C-ABI call: rows, barrier, fused column/exchange pass, barrier
+            check(self._lib.dpp_fft2d_c2c_fwd_sharded(self._plan2d._h, self._group, src.data_ptr(),
+                                                       self.cols.data_ptr(), 1 if transpose_back else 0,
+                                                       self.batch, stream_handle(stream)), "sharded 2-D FFT")
+            return self.slab if transpose_back else self.cols
         self._plan_rows.execute(src, self.slab, self.batch * self.rows, stream)
         self._barrier(stream)
         outs = self._slab_arr if transpose_back else self._col_arr
@@ -211,6 +221,10 @@ class PeerShardedFft2d:
         return self.slab if transpose_back else self.cols
 
     def close(self) -> None:
+        g = getattr(self, "_group", None)
+        if g is not None and g.value:
+            self._lib.dpp_peer_group_destroy(g)
+            self._group = None
         for base in self._opened:
             self._lib.dpp_ipc_close(base)
         self._opened = []
