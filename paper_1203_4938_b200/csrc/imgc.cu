@@ -391,7 +391,16 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
 namespace tc {
 constexpr int M = 128;      // blocks per tile (TMEM lanes)
 constexpr int NCB = 256;    // centroids (padded; TMEM columns)
-constexpr int THREADS = 128;
+// DPP_TC_SPLIT=1 (measured slower: 0.667 vs 0.54 ms per 8192^2 frame, the
+// helpers idle through the binary64 statistics and 3 CTAs/SM overlap less):
+// 256 threads per CTA — warps 4-7 take the second half of
+// every 128-column score pass (the epilogue is the kernel's largest cost),
+// 3 CTAs per SM (24 warps) instead of 4 x 128 threads (16 warps)
+#ifndef DPP_TC_SPLIT
+#define DPP_TC_SPLIT 0
+#endif
+constexpr int THREADS = DPP_TC_SPLIT ? 256 : 128;
+constexpr int CTAS_PER_SM = DPP_TC_SPLIT ? 3 : 4;
 // K-major canonical layout, no swizzle: 8-row groups of 8 K-quarters (4 tf32)
 __device__ __forceinline__ uint32_t off(int row, int k) {
   return (uint32_t)((row >> 3) * 1024 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
@@ -437,7 +446,12 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }  // namespace tc
 
 template <int CH>
-__global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs a, int64_t batch, float delta_scale,
+#if DPP_TC_SPLIT
+#define DPP_TC_BOUNDS __launch_bounds__(tc::THREADS, tc::CTAS_PER_SM)
+#else
+#define DPP_TC_BOUNDS __launch_bounds__(tc::THREADS)
+#endif
+__global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch, float delta_scale,
                                                                unsigned long long* ambiguous) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   uint8_t* sA = tsm;
@@ -448,7 +462,11 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
+  __shared__ float h_m1[tc::M], h_m2[tc::M];  // DPP_TC_SPLIT: the helper half's best / runner-up ...
+  __shared__ int h_i1[tc::M];                 // ... and best index per block
   const int tid = threadIdx.x, warp = tid >> 5;
+  const bool primary = !DPP_TC_SPLIT || tid < tc::M;  // one block (A row, TMEM lane) per primary thread
+  const int row = DPP_TC_SPLIT ? (tid & (tc::M - 1)) : tid;
   // Each CTA owns a contiguous range of the flat (image, tile) space, so the
   // grid is one balanced wave for any batch; the codebook (B operand, norms,
   // band) is restaged only when the range crosses into the next image.
@@ -517,7 +535,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t taddr = tmem + ((uint32_t)((DPP_TC_SPLIT ? (warp & 3) : warp) * 32) << 16);  // warp w reads lanes 32 (w % 4)..
   // band half-width: 1.5e-3 at |c| <= 4 (the normalised-block scale), growing
   // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
   auto band = [&]() {
@@ -538,8 +556,8 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
       delta2 = band();
     }
     const int64_t t = ft - img * ntiles;
-    const int64_t k = t * tc::M + tid;
-    const bool active = k < nblocks;
+    const int64_t k = t * tc::M + row;
+    const bool active = primary && k < nblocks;
     float nb[16];
     double mean = 0.0, sd = 0.0;
     if (active) {
@@ -551,6 +569,7 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
     // A row: n_hi (K 0..15) and the exact remainder n_lo (K 16..31)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      if (!primary) break;
       float4 hi, lo;
       float* h = &hi.x;
       float* l = &lo.x;
@@ -559,8 +578,8 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
         h[e] = __uint_as_float(__float_as_uint(nb[4 * q + e]) & 0xFFFFE000u);
         l[e] = __fsub_rn(nb[4 * q + e], h[e]);
       }
-      *reinterpret_cast<float4*>(sA + tc::off(tid, 4 * q)) = hi;
-      *reinterpret_cast<float4*>(sA + tc::off(tid, 16 + 4 * q)) = lo;
+      *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
+      *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
     }
     // two MMA passes of 128 centroids each through the same 128 TMEM columns;
     // pass 1 keeps the best and runner-up approximate score
@@ -584,8 +603,10 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
       mbar_wait(&bar, phase);
       phase ^= 1;
       tc::fence_after();
+      constexpr int CHUNKS = DPP_TC_SPLIT ? tc::NH / 64 : tc::NH / 32;
 #pragma unroll 1
-      for (int ch = 0; ch < tc::NH / 32; ++ch) {
+      for (int cq = 0; cq < CHUNKS; ++cq) {
+        const int ch = (DPP_TC_SPLIT && !primary) ? CHUNKS + cq : cq;
         uint32_t r[32];
         tc::ld32(taddr + ch * 32, r);
         const int j0 = h * tc::NH + ch * 32;
@@ -603,6 +624,27 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
             m1 = p ? s : m1;
           }
         }
+      }
+    }
+    if (DPP_TC_SPLIT) {
+      // the two halves of each pass: best of both, runner-up = the better of
+      // the other half's best and the two runners-up (exact ties give m2 == m1:
+      // ambiguous, settled by the exact re-check)
+      if (!primary) {
+        h_m1[row] = m1;
+        h_m2[row] = m2;
+        h_i1[row] = i1;
+      }
+      __syncthreads();
+      if (primary) {
+        const float bm1 = h_m1[row], bm2 = h_m2[row];
+        const int bi1 = h_i1[row];
+        const float nm2 = fminf(fmaxf(m1, bm1), fminf(m2, bm2));
+        if (bm1 < m1) {
+          m1 = bm1;
+          i1 = bi1;
+        }
+        m2 = nm2;
       }
     }
     bool zero = active;
@@ -696,7 +738,7 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
   }
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
   const int64_t all_tiles = ntiles * batch;
-  const int64_t resident = 4 * (int64_t)sm_count;  // 4 CTAs per SM (SMEM, TMEM columns)
+  const int64_t resident = tc::CTAS_PER_SM * (int64_t)sm_count;  // SMEM, TMEM columns, registers
   dim3 grid((unsigned)(all_tiles < resident ? all_tiles : resident));
   const size_t smem = tc::SMEM;
   switch (channels) {
