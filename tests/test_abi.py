@@ -4,6 +4,8 @@ from __future__ import annotations
 
 import ctypes
 import re
+
+import pytest
 from pathlib import Path
 
 from paper_1203_4938_b200 import _lib
@@ -79,3 +81,30 @@ def test_bit_exact_kernels_contain_no_fused_binary32_multiply_add():
 def test_library_is_sm100a():
     blob = _lib.LIB_PATH.read_bytes()
     assert b"sm_100a" in blob
+
+
+@pytest.mark.gpu
+def test_plain_c_consumer(tmp_path):
+    """tests/c/abi_smoke.c: the C ABI from a C program (gcc, cudart, the
+    in-tree library) — no Python or torch between the caller and the kernels."""
+    import subprocess
+    root = Path(__file__).resolve().parents[1]
+    lib_dir = root / "paper_1203_4938_b200"
+    exe = tmp_path / "abi_smoke"
+    cuda = Path("/usr/local/cuda")
+    subprocess.run(["gcc", "-O1", "-o", str(exe), str(root / "tests" / "c" / "abi_smoke.c"),
+                    f"-I{root / 'include'}", f"-I{cuda / 'include'}", f"-L{lib_dir}", "-ldpp_b200",
+                    f"-L{cuda / 'lib64'}", "-lcudart", "-lm", f"-Wl,-rpath,{lib_dir}",
+                    f"-Wl,-rpath,{cuda / 'lib64'}"], check=True)
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stderr
+    assert "abi smoke ok" in res.stdout
+
+
+def test_header_is_plain_c(tmp_path):
+    """The header and the C consumer compile as C11 (no C++ or torch types)."""
+    import subprocess
+    root = Path(__file__).resolve().parents[1]
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-c", "-o", str(tmp_path / "abi_smoke.o"),
+                    str(root / "tests" / "c" / "abi_smoke.c"), f"-I{root / 'include'}",
+                    "-I/usr/local/cuda/include"], check=True)
