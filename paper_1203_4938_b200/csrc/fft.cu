@@ -1211,6 +1211,17 @@ int fft1d_plan_init(FftPlan* p) {
         return DPP_OK;
       }
     }
+    if (n == 131072) {
+      const char* e = getenv("DPP_FFT_L2");
+      if (!e || atoi(e) != 0) {
+        if (int rc2 = fft128k_l2_init(p)) return rc2;
+        p->ring128k = 1;
+        snprintf(p->desc, sizeof(p->desc),
+                 "two-pass 256x512 four-step, L2-resident exchange (ring %d, lag %d), warp-wide 512-point P2",
+                 p->l2_ring, p->l2_lag);
+        return DPP_OK;
+      }
+    }
     if (n == 8192 || n == 16384 || n == 32768) {
       const char* e = getenv("DPP_FFT_L2");
       if (!e || atoi(e) != 0) {
@@ -1251,6 +1262,7 @@ int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch
     return fft_large_execute(p, in, out, batch, s);
   } else if (p->kind == FftPlan::CLUSTER) {
     if (p->ws4k) return fft4096_ws_execute(p, in, out, batch, s);
+    if (p->ring128k) return fft128k_l2_execute(p, in, out, batch, s);
     if (p->ring16k) {
       const int64_t tpu = 65536 / p->n0;  // transforms per ring unit
       const int64_t main = batch - batch % tpu;

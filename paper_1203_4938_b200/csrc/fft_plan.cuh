@@ -42,6 +42,8 @@ struct FftPlan {
   int ring16k = 0;
   // rank 1, n = 4096: warp-specialised single-CTA kernel (fft4k.cu)
   int ws4k = 0;
+  // rank 1, n = 2^17: L2-ring kernel, one transform per unit (fft128k_l2.cu)
+  int ring128k = 0;
   // rank 1, n > 2^17 (fft_large.cu): transpose, row pass (rows), twiddled column ring (cols)
   FftPlan* cols = nullptr;
   float2* big_tw = nullptr;       // W_N^m, m < 16384, then W_N^(16384 h)
@@ -68,6 +70,8 @@ int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, flo
                                int tb, int64_t batch, cudaStream_t s);
 int fft16k_l2_init(FftPlan* p);
 int fft16k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
+int fft128k_l2_init(FftPlan* p);
+int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft4096_ws_init(FftPlan* p);
 int fft4096_ws_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft4096_ws_execute_u8(const FftPlan* p, const uint8_t* in, float2* out, int64_t batch, cudaStream_t s);
