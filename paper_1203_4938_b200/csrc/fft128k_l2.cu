@@ -17,6 +17,12 @@
 //       staged 64B-swizzled and written by two 2-D TMA stores (8 x 256).
 // Two named barriers per P2 item: the stage is reused for the exchange and
 // the output only after every warp has its inputs / finished its exchange.
+//
+// n = 2^18 = 512 x 512 (LOGN = 18, 64 items per pass): P1 is the same
+// warp-wide 512-point FFT down 8 columns of the [a][b] view (two 2-D TMA
+// boxes of 8 x 256, 64B-swizzled), twiddle W_n^{b k1}, stored straight from
+// registers into the P2 block layout above; P2 is the 2^17 P2 with 512 output
+// columns.
 #include <cmath>
 #include <vector>
 
@@ -30,13 +36,10 @@ namespace ring128k {
 
 using namespace ring;
 
-constexpr int N = 131072;
 constexpr int CW = 8;
 constexpr int THREADS = (CW + 1) * 32;
 constexpr int TILE = 4096;
 constexpr int S = 2;
-constexpr int ITEMS = 32;
-constexpr int LOGI = 5;
 
 struct Args {
   float2* scratch;
@@ -48,8 +51,50 @@ struct Args {
 
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
+// One 512-point FFT per warp: on entry lane b0 holds v[b1] = x[32 b1 + b0];
+// on exit lane (m0 = lane >> 1, m2 = lane & 1) holds v[m1] = X[m0 + 16 m1 +
+// 256 m2].  rx: this warp's 4 KB exchange region; pwb -> W_512^lane, pw32 -> W_32.
+__device__ __forceinline__ void fft512_warp(float2 (&v)[16], uint32_t rx, int lane, const float2* pwb,
+                                            const float2* pw32) {
+  dft16c(v);  // v[m0]
+  {
+    const float2 wb = __ldg(pwb);
+    float2 w = wb;
+#pragma unroll
+    for (int m0 = 1; m0 < 16; ++m0) {
+      v[m0] = cmul(v[m0], w);
+      w = cmul(w, wb);
+    }
+  }
+#pragma unroll
+  for (int m0 = 0; m0 < 16; ++m0) sts64(rx + 8u * (32 * m0 + (lane ^ (2 * (m0 & 7)))), v[m0]);
+  __syncwarp();
+  const int m0r = lane >> 1, l0 = lane & 1;
+#pragma unroll
+  for (int l1 = 0; l1 < 16; ++l1) v[l1] = lds64(rx + 8u * (32 * m0r + ((2 * l1 + l0) ^ (2 * (m0r & 7)))));
+  dft16c(v);  // v[m1] = F_l0[m1]
+  if (l0) {
+    const float2 w32 = __ldg(pw32);
+    float2 w = w32;
+#pragma unroll
+    for (int m1 = 1; m1 < 16; ++m1) {
+      v[m1] = cmul(v[m1], w);
+      w = cmul(w, w32);
+    }
+  }
+#pragma unroll
+  for (int m1 = 0; m1 < 16; ++m1) {
+    const float px = __shfl_xor_sync(0xffffffffu, v[m1].x, 1);
+    const float py = __shfl_xor_sync(0xffffffffu, v[m1].y, 1);
+    v[m1] = l0 ? make_float2(px - v[m1].x, py - v[m1].y) : make_float2(v[m1].x + px, v[m1].y + py);
+  }
+}
+
+template <int LOGN>
 __global__ void __launch_bounds__(THREADS, 3)
-fft128k_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
+fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
+  constexpr int N = 1 << LOGN;
+  constexpr int LOGI = LOGN == 17 ? 5 : 6, ITEMS = 1 << LOGI;  // items per pass
   extern __shared__ __align__(1024) float2 smem[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t done[S];
@@ -119,7 +164,12 @@ fft128k_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUt
       float2* buf = smem + s * TILE;
       mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
       if (pass == 1) {
-        tma_load_2d_hint(buf, &tin, 16 * g, 256 * u, &full[s], stream_pol);
+        if constexpr (LOGN == 17) {
+          tma_load_2d_hint(buf, &tin, 16 * g, 256 * u, &full[s], stream_pol);
+        } else {
+          tma_load_2d_hint(buf, &tin, 8 * g, 512 * u, &full[s], stream_pol);
+          tma_load_2d_hint(buf + TILE / 2, &tin, 8 * g, 512 * u + 256, &full[s], stream_pol);
+        }
       } else {
         fence_proxy_async_global();
         bulk_g2s(buf, a.scratch + (size_t)(u & (a.ring - 1)) * N + 4096 * g, TILE * sizeof(float2), &full[s]);
@@ -148,7 +198,7 @@ fft128k_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUt
     const int g = tick & (ITEMS - 1);
     const uint32_t b = sbase + (uint32_t)s * (TILE * 8);
     float2* slot = a.scratch + (size_t)(u & (a.ring - 1)) * N;
-    if (pass == 1) {
+    if (pass == 1 && LOGN == 17) {
       // P1 (the 2^16 kernel's mapping): column col = 2w + (lane & 1), row part idx = lane >> 1
       const int col = 2 * warp + (lane & 1);
       const int idx = lane >> 1;
@@ -190,50 +240,45 @@ fft128k_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUt
       float2* dst = slot + 4096 * (idx >> 3) + 8 * bb + ((idx & 7) ^ ((bb >> 1) & 7));
 #pragma unroll
       for (int c1 = 0; c1 < 16; ++c1) st_l2_hint(dst + 8192 * c1, v[c1], keep_pol);
+    } else if (pass == 1) {
+      // P1, n = 2^18: warp w owns column b = 8 g + w of the 512 x 8 tile
+      // (two 256-row halves, 64B-swizzled), lane b0 holds a = 32 a1 + b0
+      const int bb = 8 * g + warp;
+#pragma unroll
+      for (int a1 = 0; a1 < 16; ++a1) {
+        const int r = 32 * (a1 & 7) + lane;  // row inside half a1 >> 3
+        v[a1] = lds64(b + 16384u * (uint32_t)(a1 >> 3) + 64u * (uint32_t)r +
+                      16u * (uint32_t)((warp >> 1) ^ ((r >> 1) & 3)) + 8u * (uint32_t)(warp & 1));
+      }
+      bar_compute();  // every warp holds its column: the stage is free for the exchange
+      fft512_warp(v, b + 8u * 512 * (uint32_t)warp, lane, a.twn + (N / 512) * lane, a.twn + N / 32);
+      // lane (m0, m2) holds k1 = m0 + 16 m1 + 256 m2; twiddle W_n^{b k1}
+      const int m0r = lane >> 1, l0 = lane & 1;
+      const int k1b = m0r + 256 * l0;
+      float2 w = __ldg(a.twn + bb * k1b);
+      const float2 step = __ldg(a.twn + 16 * bb);
+      v[0] = cmul(v[0], w);
+#pragma unroll
+      for (int m1 = 1; m1 < 16; ++m1) {
+        w = cmul(w, step);
+        v[m1] = cmul(v[m1], w);
+      }
+      // k1 >> 3 = (m0 >> 3) + 2 m1 + 32 m2, k1 & 7 = m0 & 7
+      float2* dst = slot + 4096 * ((m0r >> 3) + 32 * l0) + 8 * bb + ((m0r & 7) ^ ((bb >> 1) & 7));
+#pragma unroll
+      for (int m1 = 0; m1 < 16; ++m1) st_l2_hint(dst + 8192 * m1, v[m1], keep_pol);
     } else {
       // P2: warp = k1 % 8, lane b0 holds b = 32 b1 + b0
-      const int b0 = lane;
       discard_l2(slot + 4096 * g + 16 * (tid & 255));
-      const uint32_t rd = b + 8u * (uint32_t)(8 * b0 + (warp ^ ((b0 >> 1) & 7)));
+      const uint32_t rd = b + 8u * (uint32_t)(8 * lane + (warp ^ ((lane >> 1) & 7)));
 #pragma unroll
       for (int b1 = 0; b1 < 16; ++b1) v[b1] = lds64(rd + 8u * 256 * b1);
       bar_compute();  // every warp holds its sequence: the stage is free for the exchange
-      dft16c(v);      // v[m0]
-      {
-        const float2 wb = __ldg(a.twn + 256 * b0);  // W_512^b0
-        float2 w = wb;
-#pragma unroll
-        for (int m0 = 1; m0 < 16; ++m0) {
-          v[m0] = cmul(v[m0], w);
-          w = cmul(w, wb);
-        }
-      }
-      const uint32_t rx = b + 8u * 512 * (uint32_t)warp;  // this warp's 4 KB exchange region
-#pragma unroll
-      for (int m0 = 0; m0 < 16; ++m0) sts64(rx + 8u * (32 * m0 + (b0 ^ (2 * (m0 & 7)))), v[m0]);
-      __syncwarp();
-      const int m0r = lane >> 1, l0 = lane & 1;
-#pragma unroll
-      for (int l1 = 0; l1 < 16; ++l1) v[l1] = lds64(rx + 8u * (32 * m0r + ((2 * l1 + l0) ^ (2 * (m0r & 7)))));
-      dft16c(v);  // v[m1] = F_l0[m1]
-      if (l0) {
-        const float2 w32 = __ldg(a.twn + 4096);  // W_32
-        float2 w = w32;
-#pragma unroll
-        for (int m1 = 1; m1 < 16; ++m1) {
-          v[m1] = cmul(v[m1], w);
-          w = cmul(w, w32);
-        }
-      }
-#pragma unroll
-      for (int m1 = 0; m1 < 16; ++m1) {
-        const float px = __shfl_xor_sync(0xffffffffu, v[m1].x, 1);
-        const float py = __shfl_xor_sync(0xffffffffu, v[m1].y, 1);
-        v[m1] = l0 ? make_float2(px - v[m1].x, py - v[m1].y) : make_float2(v[m1].x + px, v[m1].y + py);
-      }
+      fft512_warp(v, b + 8u * 512 * (uint32_t)warp, lane, a.twn + (N / 512) * lane, a.twn + N / 32);
       bar_compute();  // every exchange read is done: the stage takes the output tile
-      // X[k1 + 256 k2], k2 = m0r + 16 m1 + 256 l0: row r = m0r + 16 m1 of half l0,
-      // column warp, 64B-swizzled (16-byte chunk ^= (r >> 1) & 3)
+      // X[k1 + R k2] (R = n / 512 columns), k2 = m0 + 16 m1 + 256 m2: row
+      // r = m0 + 16 m1 of half m2, column warp, 64B-swizzled (chunk ^= (r >> 1) & 3)
+      const int m0r = lane >> 1, l0 = lane & 1;
       const uint32_t ob = b + 16384u * (uint32_t)l0 + 8u * (uint32_t)(warp & 1);
 #pragma unroll
       for (int m1 = 0; m1 < 16; ++m1) {
@@ -249,24 +294,28 @@ fft128k_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUt
 
 }  // namespace ring128k
 
-static int g_r128_ctas = 0;
+static int g_r512_ctas[2] = {0, 0};
 
+// n = 2^17 (256 x 512) and 2^18 (512 x 512)
 int fft128k_l2_init(FftPlan* p) {
   using namespace ring128k;
-  if (p->n0 != N) return fail(DPP_EINVAL, "fft128k ring is for n = 2^17");
+  const int64_t N = p->n0;
+  if (N != (1 << 17) && N != (1 << 18)) return fail(DPP_EINVAL, "the 512-point ring is for n = 2^17 and 2^18");
+  const int slot = N == (1 << 17) ? 0 : 1;
   const size_t smem = (size_t)S * TILE * sizeof(float2);
-  if (!g_r128_ctas) {
-    DPP_CUDA_CHECK(cudaFuncSetAttribute(fft128k_l2w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (!g_r512_ctas[slot]) {
+    const void* fn = slot == 0 ? (const void*)fft_ring512_l2w<17> : (const void*)fft_ring512_l2w<18>;
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, dev = 0, sms = 0;
-    DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft128k_l2w, THREADS, smem));
+    DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, smem));
     DPP_CUDA_CHECK(cudaGetDevice(&dev));
     DPP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (per_sm < 1) return fail(DPP_ECUDA, "fft128k_l2w does not fit on an SM");
-    g_r128_ctas = per_sm * sms;
+    if (per_sm < 1) return fail(DPP_ECUDA, "fft_ring512_l2w does not fit on an SM");
+    g_r512_ctas[slot] = per_sm * sms;
   }
-  // a unit is one 1 MB transform: half the 2^16 kernel's lag and ring slots
-  p->l2_lag = 24;
-  p->l2_ring = 64;
+  // units are whole transforms (1 or 2 MB): the 2^16 kernel's 24 MB lag and 64 MB ring
+  p->l2_lag = slot == 0 ? 24 : 12;
+  p->l2_ring = slot == 0 ? 64 : 32;
   if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
   if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e) > 0 ? atoi(e) : p->l2_ring;
   if (p->l2_ring <= p->l2_lag) p->l2_ring = p->l2_lag + 1;
@@ -299,11 +348,21 @@ int fft128k_l2_init(FftPlan* p) {
 int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s) {
   using namespace ring128k;
   if (batch <= 0) return DPP_OK;
-  if (batch > 0x7fffffff / (2 * ITEMS)) return fail(DPP_EINVAL, "batch %lld too large", (long long)batch);
+  const bool big = p->n0 == (1 << 18);
+  const int items = big ? 64 : 32;
+  if (batch > 0x7fffffff / (2 * items)) return fail(DPP_EINVAL, "batch %lld too large", (long long)batch);
   CUtensorMap tin, tout;
-  if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 256, 512, 256, 16, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
-  // output as rows k2 (512 per transform) x 256 columns k1, boxes of 8 columns x 256 rows
-  if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 512, 256, 256, 8, CU_TENSOR_MAP_SWIZZLE_64B)) return rc;
+  if (big) {
+    // input as 512 rows a x 512 columns b, boxes of 8 columns x 256 rows (64B swizzle)
+    if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 512, 512, 256, 8, CU_TENSOR_MAP_SWIZZLE_64B)) return rc;
+  } else {
+    if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 256, 512, 256, 16, CU_TENSOR_MAP_SWIZZLE_128B))
+      return rc;
+  }
+  // output as rows k2 (512 per transform) x n/512 columns k1, boxes of 8 columns x 256 rows
+  if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 512, (uint64_t)(p->n0 / 512), 256, 8,
+                             CU_TENSOR_MAP_SWIZZLE_64B))
+    return rc;
   Args a;
   a.scratch = p->l2_scratch;
   a.ctrl = p->l2_ctrl;
@@ -314,10 +373,15 @@ int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
   a.ring = p->l2_ring;
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)batch) * sizeof(int), s));
-  const int64_t items = 2 * ITEMS * batch;
-  const unsigned grid = (unsigned)(items < g_r128_ctas ? items : g_r128_ctas);
-  fft128k_l2w<<<grid, THREADS, (size_t)S * TILE * sizeof(float2), s>>>(tin, tout, a);
-  DPP_LAUNCH_CHECK("fft128k_l2w");
+  const int64_t total = 2 * (int64_t)items * batch;
+  const int ctas = g_r512_ctas[big ? 1 : 0];
+  const unsigned grid = (unsigned)(total < ctas ? total : ctas);
+  const size_t smem = (size_t)S * TILE * sizeof(float2);
+  if (big)
+    fft_ring512_l2w<18><<<grid, THREADS, smem, s>>>(tin, tout, a);
+  else
+    fft_ring512_l2w<17><<<grid, THREADS, smem, s>>>(tin, tout, a);
+  DPP_LAUNCH_CHECK("fft_ring512_l2w");
   DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
   return DPP_OK;
 }
