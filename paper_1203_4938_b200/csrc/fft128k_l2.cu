@@ -314,7 +314,7 @@ int fft128k_l2_init(FftPlan* p) {
     g_r512_ctas[slot] = per_sm * sms;
   }
   // units are whole transforms (1 or 2 MB): the 2^16 kernel's 24 MB lag and 64 MB ring
-  p->l2_lag = slot == 0 ? 24 : 12;
+  p->l2_lag = slot == 0 ? 24 : 16;
   p->l2_ring = slot == 0 ? 64 : 32;
   if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
   if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e) > 0 ? atoi(e) : p->l2_ring;
