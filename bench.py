@@ -47,8 +47,8 @@ def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": d["hbm_gbs"], "source": "measured"}
-    return {"hbm_gbs": 6650.0, "source": "fallback"}
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d.get("bf16_tflops", 1590.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
 
 
 class ClockSampler:
@@ -366,7 +366,15 @@ def run_ours(args) -> None:
                              "reference (configs[3])",
                    "roofline": {"bound": "fp32", "hbm_frac": round(comp_bytes / (c_ms / 1e3) / 1e9
                                                                     / pk["hbm_gbs"], 5),
-                                "vq_flop_per_block": 12288}}
+                                "vq_flop_per_block": 12288,
+                                # the exact search's fp32 work per second (it runs as TF32 MMAs + a
+                                # CUDA-core re-check of the ambiguous blocks)
+                                "vq_effective_tflops": round(12288 * nb / (c_ms / 1e3) / 1e12, 1),
+                                # 3xTF32 scores: 3 MMAs x 2 x 256 centroids x 16 K per block
+                                "tf32_mma_tflops": round(24576 * nb / (c_ms / 1e3) / 1e12, 1),
+                                "tf32_peak_tflops": round(pk["bf16_tflops"] / 2, 1),
+                                "tf32_frac": round(24576 * nb / (c_ms / 1e3) / 1e12 / (pk["bf16_tflops"] / 2), 4),
+                                "peak_source": pk["source"] + " (tf32 = bf16 dense / 2)"}}
 
     del x, y
 
