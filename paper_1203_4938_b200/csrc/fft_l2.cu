@@ -340,7 +340,10 @@ struct Args {
 #ifndef DPP_L2_PF
 #define DPP_L2_PF 0  // L2 prefetch distance in item-times (measured: no gain, profiles/r1_fft_l2.md)
 #endif
-template <int S, int MINB, bool DISCARD, int PF = DPP_L2_PF>
+// LDG2: P2 reads its block straight from L2 into registers (ld.global.cg)
+// instead of a bulk copy into the stage: 16 B/point less shared-memory
+// traffic, the L2 latency exposed to the compute warps instead
+template <int S, int MINB, bool DISCARD, int PF = DPP_L2_PF, bool LDG2 = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
   extern __shared__ __align__(1024) float2 smem[];
@@ -428,6 +431,10 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
       bulk_wait_read0();  // the stage's previous output tile has left shared memory
       s_tick[s] = tick;
       float2* buf = smem + s * TILE;
+      if (LDG2 && pass == 2) {
+        mbar_arrive1(&full[s]);  // the compute warps load the block themselves
+        continue;
+      }
       mbar_arrive_expect_tx(&full[s], TILE * sizeof(float2));
       if (pass == 1) {
         tma_load_2d_hint(buf, &tin, 16 * g, t * 256, &full[s], stream_pol);
@@ -474,12 +481,22 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
     const int g = tick & 15;
     const uint32_t b = sbase + (uint32_t)s * (TILE * 8);
     float2* slot = a.scratch + (size_t)(t & (a.ring - 1)) * l2x::N;
-    // the P2 block is in shared memory: drop its scratch lines (no HBM write-back)
-    if (DISCARD && pass == 2) l2x::discard_l2(slot + 4096 * g + 16 * (tid & 255));
     const uint32_t bA = b + offA;
+    if (LDG2 && pass == 2) {
+      const float2* pa = slot + 4096 * g + (offA >> 3);  // the block has the tile's layout
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
+      for (int j = 0; j < 16; ++j) v[j] = ld_l2(pa + 256 * j);
+    } else {
+      // the P2 block is in shared memory: drop its scratch lines (no HBM write-back)
+      if (DISCARD && pass == 2) l2x::discard_l2(slot + 4096 * g + 16 * (tid & 255));
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = lds64(bA + 2048 * j);
+    }
     dft16c(v);
+    if (LDG2 && DISCARD && pass == 2) {
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // every warp's loads have returned
+      l2x::discard_l2(slot + 4096 * g + 16 * (tid & 255));
+    }
     float2 wk = w1;
 #pragma unroll
     for (int k = 1; k < 16; ++k) {
@@ -586,6 +603,7 @@ static int l2p_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
 #define DPP_L2W_MINB 3  // and CTAs per SM
 #endif
 static int g_l2w_cfg = 0;  // 0: S=2 x 3 CTAs/SM, 1: S=3 x 2 CTAs/SM
+static int g_l2w_ldg2 = 0;  // DPP_L2_P2LDG=1: P2 blocks loaded by the compute warps (A/B variant)
 static int g_l2w_ctas = 0;
 
 template <int S, int MINB, bool D>
@@ -599,8 +617,13 @@ static size_t l2w_smem(int S) { return (size_t)S * l2x::l2w::TILE * sizeof(float
 
 static int l2w_prepare() {
   if (const char* e = getenv("DPP_FFT_L2_CFG")) g_l2w_cfg = atoi(e) == 1 ? 1 : 0;
+  if (const char* e = getenv("DPP_L2_P2LDG")) g_l2w_ldg2 = atoi(e) != 0;
   const int S = g_l2w_cfg ? 3 : DPP_L2W_S;
   const size_t smem = l2w_smem(S);
+  {
+    auto k2 = l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, true, DPP_L2_PF, true>;
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l2w_smem(DPP_L2W_S)));
+  }
   int rc = g_l2w_cfg ? (l2w_prepare_one<3, 2, true>(smem) || l2w_prepare_one<3, 2, false>(smem))
                      : (l2w_prepare_one<DPP_L2W_S, DPP_L2W_MINB, true>(smem) || l2w_prepare_one<DPP_L2W_S, DPP_L2W_MINB, false>(smem));
   if (rc) return DPP_ECUDA;
@@ -638,6 +661,9 @@ static int l2w_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
   if (g_l2w_cfg) {
     if (g_discard) l2x::l2w::fft65536_l2w<3, 2, true><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
     else l2x::l2w::fft65536_l2w<3, 2, false><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
+  } else if (g_l2w_ldg2) {
+    l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, true, DPP_L2_PF, true><<<grid, l2x::l2w::THREADS, smem, s>>>(
+        tin, tout, a);
   } else {
     if (g_discard) l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, true><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
     else l2x::l2w::fft65536_l2w<DPP_L2W_S, DPP_L2W_MINB, false><<<grid, l2x::l2w::THREADS, smem, s>>>(tin, tout, a);
