@@ -23,6 +23,14 @@
 // boxes of 8 x 256, 64B-swizzled), twiddle W_n^{b k1}, stored straight from
 // registers into the P2 block layout above; P2 is the 2^17 P2 with 512 output
 // columns.
+//
+// n = 2^19 = 512 x 1024 (LOGN = 19, 128 items per pass): P1 as for 2^18 on
+// rows of 1024; P2 blocks are 4 columns k1 x 1024 rows b (element (b, c) at
+// 4 b + (c ^ ((b >> 2) & 3))), and each 1024-point sequence is split over a
+// warp pair by one decimation-in-frequency step: warp e of the pair FFTs
+// (x[j] + x[j+512]) (e = 0) or (x[j] - x[j+512]) W_1024^j (e = 1) with the
+// 512-point warp FFT, giving X[2 k' + e] — no exchange between the two warps.
+// Output tile 1024 rows x 4 columns, 32B-swizzled, four 2-D TMA stores (4 x 256).
 #include <cmath>
 #include <vector>
 
@@ -94,7 +102,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(THREADS, 3)
 fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
   constexpr int N = 1 << LOGN;
-  constexpr int LOGI = LOGN == 17 ? 5 : 6, ITEMS = 1 << LOGI;  // items per pass
+  constexpr int LOGI = LOGN == 17 ? 5 : (LOGN == 18 ? 6 : 7), ITEMS = 1 << LOGI;  // items per pass
   extern __shared__ __align__(1024) float2 smem[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t done[S];
@@ -127,8 +135,14 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
       } else {
         if (u + a.ring < a.units) red_release_add(cnt2 + u, 1);
         const int g2 = s_tick[s] & (ITEMS - 1);
-        tma_store_2d_hint(&tout, 8 * g2, 512 * u, smem + s * TILE, stream_pol);
-        tma_store_2d_hint(&tout, 8 * g2, 512 * u + 256, smem + s * TILE + TILE / 2, stream_pol);
+        if constexpr (LOGN == 19) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            tma_store_2d_hint(&tout, 4 * g2, 1024 * u + 256 * h, smem + s * TILE + h * (TILE / 4), stream_pol);
+        } else {
+          tma_store_2d_hint(&tout, 8 * g2, 512 * u, smem + s * TILE, stream_pol);
+          tma_store_2d_hint(&tout, 8 * g2, 512 * u + 256, smem + s * TILE + TILE / 2, stream_pol);
+        }
         bulk_commit();
       }
     };
@@ -263,12 +277,50 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
         w = cmul(w, step);
         v[m1] = cmul(v[m1], w);
       }
-      // k1 >> 3 = (m0 >> 3) + 2 m1 + 32 m2, k1 & 7 = m0 & 7
-      float2* dst = slot + 4096 * ((m0r >> 3) + 32 * l0) + 8 * bb + ((m0r & 7) ^ ((bb >> 1) & 7));
+      if constexpr (LOGN == 18) {
+        // k1 >> 3 = (m0 >> 3) + 2 m1 + 32 m2, k1 & 7 = m0 & 7
+        float2* dst = slot + 4096 * ((m0r >> 3) + 32 * l0) + 8 * bb + ((m0r & 7) ^ ((bb >> 1) & 7));
 #pragma unroll
-      for (int m1 = 0; m1 < 16; ++m1) st_l2_hint(dst + 8192 * m1, v[m1], keep_pol);
+        for (int m1 = 0; m1 < 16; ++m1) st_l2_hint(dst + 8192 * m1, v[m1], keep_pol);
+      } else {
+        // 4-column blocks: k1 >> 2 = (m0 >> 2) + 4 m1 + 64 m2, k1 & 3 = m0 & 3
+        float2* dst = slot + 4096 * ((m0r >> 2) + 64 * l0) + 4 * bb + ((m0r & 3) ^ ((bb >> 2) & 3));
+#pragma unroll
+        for (int m1 = 0; m1 < 16; ++m1) st_l2_hint(dst + 16384 * m1, v[m1], keep_pol);
+      }
+    } else if (LOGN == 19) {
+      // P2, n = 2^19: warp pair p = k1 % 4 of the block, warp e = w & 1 of the pair
+      discard_l2(slot + 4096 * g + 16 * (tid & 255));
+      const int p = warp >> 1, e = warp & 1;
+      const uint32_t rd = b + 8u * (uint32_t)(4 * lane + (p ^ ((lane >> 2) & 3)));
+      float2 wj = __ldg(a.twn + (N / 1024) * lane);  // W_1024^{lane}, then x W_32 per b1
+      const float2 w32s = __ldg(a.twn + N / 32);
+#pragma unroll
+      for (int b1 = 0; b1 < 16; ++b1) {
+        const float2 lo = lds64(rd + 8u * 128 * b1), hi = lds64(rd + 8u * 128 * b1 + 16384u);
+        if (e) {
+          v[b1] = cmul(make_float2(lo.x - hi.x, lo.y - hi.y), wj);
+          wj = cmul(wj, w32s);
+        } else {
+          v[b1] = make_float2(lo.x + hi.x, lo.y + hi.y);
+        }
+      }
+      bar_compute();  // every warp holds its half-sequence: the stage is free for the exchange
+      fft512_warp(v, b + 8u * 512 * (uint32_t)warp, lane, a.twn + (N / 512) * lane, a.twn + N / 32);
+      bar_compute();  // every exchange read is done: the stage takes the output tile
+      // X[k1 + 512 k2], k2 = 2 (m0 + 16 m1 + 256 m2) + e: quarter k2 >> 8, row
+      // r = k2 & 255, column p, 32B-swizzled (chunk ^= (r >> 2) & 1)
+      const int m0r = lane >> 1, l0 = lane & 1;
+#pragma unroll
+      for (int m1 = 0; m1 < 16; ++m1) {
+        const int k2 = 2 * (m0r + 16 * m1 + 256 * l0) + e;
+        const int r = k2 & 255;
+        sts64(b + 8192u * (uint32_t)(k2 >> 8) + 32u * (uint32_t)r + 16u * (uint32_t)((p >> 1) ^ ((r >> 2) & 1)) +
+                  8u * (uint32_t)(p & 1),
+              v[m1]);
+      }
     } else {
-      // P2: warp = k1 % 8, lane b0 holds b = 32 b1 + b0
+      // P2 (2^17, 2^18): warp = k1 % 8, lane b0 holds b = 32 b1 + b0
       discard_l2(slot + 4096 * g + 16 * (tid & 255));
       const uint32_t rd = b + 8u * (uint32_t)(8 * lane + (warp ^ ((lane >> 1) & 7)));
 #pragma unroll
@@ -294,17 +346,19 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
 
 }  // namespace ring128k
 
-static int g_r512_ctas[2] = {0, 0};
+static int g_r512_ctas[3] = {0, 0, 0};
 
 // n = 2^17 (256 x 512) and 2^18 (512 x 512)
 int fft128k_l2_init(FftPlan* p) {
   using namespace ring128k;
   const int64_t N = p->n0;
-  if (N != (1 << 17) && N != (1 << 18)) return fail(DPP_EINVAL, "the 512-point ring is for n = 2^17 and 2^18");
-  const int slot = N == (1 << 17) ? 0 : 1;
+  if (N != (1 << 17) && N != (1 << 18) && N != (1 << 19))
+    return fail(DPP_EINVAL, "the 512-point ring is for n = 2^17 .. 2^19");
+  const int slot = N == (1 << 17) ? 0 : (N == (1 << 18) ? 1 : 2);
   const size_t smem = (size_t)S * TILE * sizeof(float2);
   if (!g_r512_ctas[slot]) {
-    const void* fn = slot == 0 ? (const void*)fft_ring512_l2w<17> : (const void*)fft_ring512_l2w<18>;
+    const void* fn = slot == 0 ? (const void*)fft_ring512_l2w<17>
+                               : (slot == 1 ? (const void*)fft_ring512_l2w<18> : (const void*)fft_ring512_l2w<19>);
     DPP_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, dev = 0, sms = 0;
     DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, smem));
@@ -314,8 +368,8 @@ int fft128k_l2_init(FftPlan* p) {
     g_r512_ctas[slot] = per_sm * sms;
   }
   // units are whole transforms (1 or 2 MB): the 2^16 kernel's 24 MB lag and 64 MB ring
-  p->l2_lag = slot == 0 ? 24 : 16;
-  p->l2_ring = slot == 0 ? 64 : 32;
+  p->l2_lag = slot == 0 ? 24 : (slot == 1 ? 16 : 8);
+  p->l2_ring = slot == 0 ? 64 : (slot == 1 ? 32 : 16);
   if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
   if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e) > 0 ? atoi(e) : p->l2_ring;
   if (p->l2_ring <= p->l2_lag) p->l2_ring = p->l2_lag + 1;
@@ -348,21 +402,29 @@ int fft128k_l2_init(FftPlan* p) {
 int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s) {
   using namespace ring128k;
   if (batch <= 0) return DPP_OK;
-  const bool big = p->n0 == (1 << 18);
-  const int items = big ? 64 : 32;
+  const int lg = p->n0 == (1 << 17) ? 17 : (p->n0 == (1 << 18) ? 18 : 19);
+  const int items = lg == 17 ? 32 : (lg == 18 ? 64 : 128);
   if (batch > 0x7fffffff / (2 * items)) return fail(DPP_EINVAL, "batch %lld too large", (long long)batch);
   CUtensorMap tin, tout;
-  if (big) {
-    // input as 512 rows a x 512 columns b, boxes of 8 columns x 256 rows (64B swizzle)
-    if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 512, 512, 256, 8, CU_TENSOR_MAP_SWIZZLE_64B)) return rc;
+  if (lg >= 18) {
+    // input as 512 rows a x n/512 columns b, boxes of 8 columns x 256 rows (64B swizzle)
+    if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 512, (uint64_t)(p->n0 / 512), 256, 8,
+                               CU_TENSOR_MAP_SWIZZLE_64B))
+      return rc;
   } else {
     if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 256, 512, 256, 16, CU_TENSOR_MAP_SWIZZLE_128B))
       return rc;
   }
-  // output as rows k2 (512 per transform) x n/512 columns k1, boxes of 8 columns x 256 rows
-  if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 512, (uint64_t)(p->n0 / 512), 256, 8,
-                             CU_TENSOR_MAP_SWIZZLE_64B))
-    return rc;
+  if (lg == 19) {
+    // output as rows k2 (1024 per transform) x 512 columns k1, boxes of 4 columns x 256 rows
+    if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 1024, 512, 256, 4, CU_TENSOR_MAP_SWIZZLE_32B))
+      return rc;
+  } else {
+    // output as rows k2 (512 per transform) x n/512 columns k1, boxes of 8 columns x 256 rows
+    if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 512, (uint64_t)(p->n0 / 512), 256, 8,
+                               CU_TENSOR_MAP_SWIZZLE_64B))
+      return rc;
+  }
   Args a;
   a.scratch = p->l2_scratch;
   a.ctrl = p->l2_ctrl;
@@ -374,10 +436,12 @@ int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)batch) * sizeof(int), s));
   const int64_t total = 2 * (int64_t)items * batch;
-  const int ctas = g_r512_ctas[big ? 1 : 0];
+  const int ctas = g_r512_ctas[lg - 17];
   const unsigned grid = (unsigned)(total < ctas ? total : ctas);
   const size_t smem = (size_t)S * TILE * sizeof(float2);
-  if (big)
+  if (lg == 19)
+    fft_ring512_l2w<19><<<grid, THREADS, smem, s>>>(tin, tout, a);
+  else if (lg == 18)
     fft_ring512_l2w<18><<<grid, THREADS, smem, s>>>(tin, tout, a);
   else
     fft_ring512_l2w<17><<<grid, THREADS, smem, s>>>(tin, tout, a);
