@@ -1244,15 +1244,16 @@ int fft1d_plan_init(FftPlan* p) {
              (p->mode == 3 || p->mode == 9) ? (std::string(", ") + std::to_string(p->max_clusters) + " clusters").c_str() : "");
     return DPP_OK;
   }
-  if (n == 262144 || n == 524288) {
+  if (n == 262144 || n == 524288 || n == 1048576) {
     const char* e = getenv("DPP_FFT_L2");
     if (!e || atoi(e) != 0) {
       p->kind = FftPlan::CLUSTER;
       if (int rc = fft128k_l2_init(p)) return rc;
       p->ring128k = 1;
       snprintf(p->desc, sizeof(p->desc),
-               "two-pass 512x%lld four-step, L2-resident exchange (ring %d, lag %d), warp-wide 512-point passes",
-               (long long)(n / 512), p->l2_ring, p->l2_lag);
+               "two-pass %lldx%lld four-step, L2-resident exchange (ring %d, lag %d), warp-wide 512-point FFTs",
+               (long long)(n <= 524288 ? 512 : 1024), (long long)(n <= 524288 ? n / 512 : 1024), p->l2_ring,
+               p->l2_lag);
       return DPP_OK;
     }
   }

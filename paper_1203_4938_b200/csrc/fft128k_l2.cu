@@ -31,6 +31,11 @@
 // (x[j] + x[j+512]) (e = 0) or (x[j] - x[j+512]) W_1024^j (e = 1) with the
 // 512-point warp FFT, giving X[2 k' + e] — no exchange between the two warps.
 // Output tile 1024 rows x 4 columns, 32B-swizzled, four 2-D TMA stores (4 x 256).
+//
+// n = 2^20 = 1024 x 1024 (LOGN = 20, 256 items per pass): P1 loads 4 columns
+// x 1024 rows (four 32B-swizzled boxes) and runs the same warp-pair
+// decimation-in-frequency 1024-point FFT down each column, twiddle
+// W_n^{b k1}, stores into the 4-column P2 blocks; P2 is the 2^19 P2.
 #include <cmath>
 #include <vector>
 
@@ -102,7 +107,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(THREADS, 3)
 fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, const Args a) {
   constexpr int N = 1 << LOGN;
-  constexpr int LOGI = LOGN == 17 ? 5 : (LOGN == 18 ? 6 : 7), ITEMS = 1 << LOGI;  // items per pass
+  constexpr int LOGI = LOGN == 17 ? 5 : (LOGN == 18 ? 6 : (LOGN == 19 ? 7 : 8)), ITEMS = 1 << LOGI;  // per pass
   extern __shared__ __align__(1024) float2 smem[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t done[S];
@@ -135,7 +140,7 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
       } else {
         if (u + a.ring < a.units) red_release_add(cnt2 + u, 1);
         const int g2 = s_tick[s] & (ITEMS - 1);
-        if constexpr (LOGN == 19) {
+        if constexpr (LOGN >= 19) {
 #pragma unroll
           for (int h = 0; h < 4; ++h)
             tma_store_2d_hint(&tout, 4 * g2, 1024 * u + 256 * h, smem + s * TILE + h * (TILE / 4), stream_pol);
@@ -180,6 +185,10 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
       if (pass == 1) {
         if constexpr (LOGN == 17) {
           tma_load_2d_hint(buf, &tin, 16 * g, 256 * u, &full[s], stream_pol);
+        } else if constexpr (LOGN == 20) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            tma_load_2d_hint(buf + h * (TILE / 4), &tin, 4 * g, 1024 * u + 256 * h, &full[s], stream_pol);
         } else {
           tma_load_2d_hint(buf, &tin, 8 * g, 512 * u, &full[s], stream_pol);
           tma_load_2d_hint(buf + TILE / 2, &tin, 8 * g, 512 * u + 256, &full[s], stream_pol);
@@ -254,6 +263,44 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
       float2* dst = slot + 4096 * (idx >> 3) + 8 * bb + ((idx & 7) ^ ((bb >> 1) & 7));
 #pragma unroll
       for (int c1 = 0; c1 < 16; ++c1) st_l2_hint(dst + 8192 * c1, v[c1], keep_pol);
+    } else if (pass == 1 && LOGN == 20) {
+      // P1, n = 2^20: warp pair p owns column b = 4 g + p of the 1024 x 4 tile
+      // (four 256-row quarters, 32B-swizzled); warp e of the pair takes the
+      // DIF half: a = 32 a1 + lane paired with a + 512
+      const int p = warp >> 1, e = warp & 1;
+      const int bb = 4 * g + p;
+      float2 wj = __ldg(a.twn + (N / 1024) * lane);  // W_1024^{lane}, then x W_32 per a1
+      const float2 w32s = __ldg(a.twn + N / 32);
+#pragma unroll
+      for (int a1 = 0; a1 < 16; ++a1) {
+        const int r = 32 * (a1 & 7) + lane;  // row inside quarter a1 >> 3 (and + 2 for a + 512)
+        const uint32_t ad = b + 8192u * (uint32_t)(a1 >> 3) + 32u * (uint32_t)r +
+                            16u * (uint32_t)((p >> 1) ^ ((r >> 2) & 1)) + 8u * (uint32_t)(p & 1);
+        const float2 lo = lds64(ad), hi = lds64(ad + 16384u);
+        if (e) {
+          v[a1] = cmul(make_float2(lo.x - hi.x, lo.y - hi.y), wj);
+          wj = cmul(wj, w32s);
+        } else {
+          v[a1] = make_float2(lo.x + hi.x, lo.y + hi.y);
+        }
+      }
+      bar_compute();  // every warp holds its half-column: the stage is free for the exchange
+      fft512_warp(v, b + 8u * 512 * (uint32_t)warp, lane, a.twn + (N / 512) * lane, a.twn + N / 32);
+      // lane (m0, m2) of warp e holds k1 = 2 (m0 + 16 m1 + 256 m2) + e; twiddle W_n^{b k1}
+      const int m0r = lane >> 1, l0 = lane & 1;
+      const int kb = 2 * m0r + e;  // < 32
+      float2 w = __ldg(a.twn + bb * (kb + 512 * l0));
+      const float2 step = __ldg(a.twn + 32 * bb);
+      v[0] = cmul(v[0], w);
+#pragma unroll
+      for (int m1 = 1; m1 < 16; ++m1) {
+        w = cmul(w, step);
+        v[m1] = cmul(v[m1], w);
+      }
+      // 4-column blocks: k1 >> 2 = (kb >> 2) + 8 m1 + 128 m2, k1 & 3 = kb & 3
+      float2* dst = slot + 4096 * ((kb >> 2) + 128 * l0) + 4 * bb + ((kb & 3) ^ ((bb >> 2) & 3));
+#pragma unroll
+      for (int m1 = 0; m1 < 16; ++m1) st_l2_hint(dst + 32768 * m1, v[m1], keep_pol);
     } else if (pass == 1) {
       // P1, n = 2^18: warp w owns column b = 8 g + w of the 512 x 8 tile
       // (two 256-row halves, 64B-swizzled), lane b0 holds a = 32 a1 + b0
@@ -288,8 +335,8 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
 #pragma unroll
         for (int m1 = 0; m1 < 16; ++m1) st_l2_hint(dst + 16384 * m1, v[m1], keep_pol);
       }
-    } else if (LOGN == 19) {
-      // P2, n = 2^19: warp pair p = k1 % 4 of the block, warp e = w & 1 of the pair
+    } else if (LOGN >= 19) {
+      // P2, n = 2^19, 2^20: warp pair p = k1 % 4 of the block, warp e = w & 1 of the pair
       discard_l2(slot + 4096 * g + 16 * (tid & 255));
       const int p = warp >> 1, e = warp & 1;
       const uint32_t rd = b + 8u * (uint32_t)(4 * lane + (p ^ ((lane >> 2) & 3)));
@@ -308,7 +355,7 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
       bar_compute();  // every warp holds its half-sequence: the stage is free for the exchange
       fft512_warp(v, b + 8u * 512 * (uint32_t)warp, lane, a.twn + (N / 512) * lane, a.twn + N / 32);
       bar_compute();  // every exchange read is done: the stage takes the output tile
-      // X[k1 + 512 k2], k2 = 2 (m0 + 16 m1 + 256 m2) + e: quarter k2 >> 8, row
+      // X[k1 + (n/1024) k2], k2 = 2 (m0 + 16 m1 + 256 m2) + e: quarter k2 >> 8, row
       // r = k2 & 255, column p, 32B-swizzled (chunk ^= (r >> 2) & 1)
       const int m0r = lane >> 1, l0 = lane & 1;
 #pragma unroll
@@ -346,19 +393,20 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
 
 }  // namespace ring128k
 
-static int g_r512_ctas[3] = {0, 0, 0};
+static int g_r512_ctas[4] = {0, 0, 0, 0};
 
 // n = 2^17 (256 x 512) and 2^18 (512 x 512)
 int fft128k_l2_init(FftPlan* p) {
   using namespace ring128k;
   const int64_t N = p->n0;
-  if (N != (1 << 17) && N != (1 << 18) && N != (1 << 19))
-    return fail(DPP_EINVAL, "the 512-point ring is for n = 2^17 .. 2^19");
-  const int slot = N == (1 << 17) ? 0 : (N == (1 << 18) ? 1 : 2);
+  if (N < (1 << 17) || N > (1 << 20) || (N & (N - 1)))
+    return fail(DPP_EINVAL, "the 512-point ring is for n = 2^17 .. 2^20");
+  const int slot = N == (1 << 17) ? 0 : (N == (1 << 18) ? 1 : (N == (1 << 19) ? 2 : 3));
   const size_t smem = (size_t)S * TILE * sizeof(float2);
   if (!g_r512_ctas[slot]) {
-    const void* fn = slot == 0 ? (const void*)fft_ring512_l2w<17>
-                               : (slot == 1 ? (const void*)fft_ring512_l2w<18> : (const void*)fft_ring512_l2w<19>);
+    const void* fns[4] = {(const void*)fft_ring512_l2w<17>, (const void*)fft_ring512_l2w<18>,
+                          (const void*)fft_ring512_l2w<19>, (const void*)fft_ring512_l2w<20>};
+    const void* fn = fns[slot];
     DPP_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, dev = 0, sms = 0;
     DPP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, smem));
@@ -368,8 +416,9 @@ int fft128k_l2_init(FftPlan* p) {
     g_r512_ctas[slot] = per_sm * sms;
   }
   // units are whole transforms (1 or 2 MB): the 2^16 kernel's 24 MB lag and 64 MB ring
-  p->l2_lag = slot == 0 ? 24 : (slot == 1 ? 16 : 8);
-  p->l2_ring = slot == 0 ? 64 : (slot == 1 ? 32 : 16);
+  const int lags[4] = {24, 16, 8, 4}, rings[4] = {64, 32, 16, 8};
+  p->l2_lag = lags[slot];
+  p->l2_ring = rings[slot];
   if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
   if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e) > 0 ? atoi(e) : p->l2_ring;
   if (p->l2_ring <= p->l2_lag) p->l2_ring = p->l2_lag + 1;
@@ -402,11 +451,14 @@ int fft128k_l2_init(FftPlan* p) {
 int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s) {
   using namespace ring128k;
   if (batch <= 0) return DPP_OK;
-  const int lg = p->n0 == (1 << 17) ? 17 : (p->n0 == (1 << 18) ? 18 : 19);
-  const int items = lg == 17 ? 32 : (lg == 18 ? 64 : 128);
+  const int lg = p->n0 == (1 << 17) ? 17 : (p->n0 == (1 << 18) ? 18 : (p->n0 == (1 << 19) ? 19 : 20));
+  const int items = 32 << (lg - 17);
   if (batch > 0x7fffffff / (2 * items)) return fail(DPP_EINVAL, "batch %lld too large", (long long)batch);
   CUtensorMap tin, tout;
-  if (lg >= 18) {
+  if (lg == 20) {
+    // input as 1024 rows a x 1024 columns b, boxes of 4 columns x 256 rows (32B swizzle)
+    if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 1024, 1024, 256, 4, CU_TENSOR_MAP_SWIZZLE_32B)) return rc;
+  } else if (lg >= 18) {
     // input as 512 rows a x n/512 columns b, boxes of 8 columns x 256 rows (64B swizzle)
     if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 512, (uint64_t)(p->n0 / 512), 256, 8,
                                CU_TENSOR_MAP_SWIZZLE_64B))
@@ -415,9 +467,10 @@ int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
     if (int rc = make_tmap_c64(&tin, in, (uint64_t)batch * 256, 512, 256, 16, CU_TENSOR_MAP_SWIZZLE_128B))
       return rc;
   }
-  if (lg == 19) {
-    // output as rows k2 (1024 per transform) x 512 columns k1, boxes of 4 columns x 256 rows
-    if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 1024, 512, 256, 4, CU_TENSOR_MAP_SWIZZLE_32B))
+  if (lg >= 19) {
+    // output as rows k2 (1024 per transform) x n/1024 columns k1, boxes of 4 columns x 256 rows
+    if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 1024, (uint64_t)(p->n0 / 1024), 256, 4,
+                               CU_TENSOR_MAP_SWIZZLE_32B))
       return rc;
   } else {
     // output as rows k2 (512 per transform) x n/512 columns k1, boxes of 8 columns x 256 rows
@@ -439,7 +492,9 @@ int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
   const int ctas = g_r512_ctas[lg - 17];
   const unsigned grid = (unsigned)(total < ctas ? total : ctas);
   const size_t smem = (size_t)S * TILE * sizeof(float2);
-  if (lg == 19)
+  if (lg == 20)
+    fft_ring512_l2w<20><<<grid, THREADS, smem, s>>>(tin, tout, a);
+  else if (lg == 19)
     fft_ring512_l2w<19><<<grid, THREADS, smem, s>>>(tin, tout, a);
   else if (lg == 18)
     fft_ring512_l2w<18><<<grid, THREADS, smem, s>>>(tin, tout, a);

@@ -244,14 +244,14 @@ def test_2e16_kernel_variants(cuda, env):
     _run_variant(env, 65536)
 
 
-@pytest.mark.parametrize("n", [8192, 16384, 32768, 131072, 262144, 524288])
+@pytest.mark.parametrize("n", [8192, 16384, 32768, 131072, 262144, 524288, 1048576])
 @pytest.mark.parametrize("env", [{}, {"DPP_FFT_L2_RING": "4", "DPP_FFT_L2_LAG": "2"}, {"DPP_FFT_L2": "0"}],
                          ids=["default", "ring4-lag2", "cluster"])
 def test_2e13_to_2e15_kernel_variants(cuda, env, n):
     # n = 256 B: the L2-ring kernel runs units of 256/B transforms (37 is
     # ragged for all three) and the cluster kernel the remainder; 2^17 runs
-    # 2^18 and 2^19 one transform per unit (csrc/fft128k_l2.cu); DPP_FFT_L2=0 is
-    # cluster-only (the three-pass path for 2^18, 2^19)
+    # 2^18 .. 2^20 one transform per unit (csrc/fft128k_l2.cu); DPP_FFT_L2=0 is
+    # cluster-only (the three-pass path above 2^17)
     _run_variant(env, n)
 
 
