@@ -389,3 +389,22 @@ def test_one_plan_shared_by_threads_and_streams(cuda, n):
     assert not errors, errors
     for o, r in zip(outs, ref):
         assert torch.equal(o, r)
+
+
+@pytest.mark.parametrize("m", [16, 17, 18, 19, 20])
+def test_ring_kernels_single_transform_and_smaller_batches(cuda, m):
+    """batch 1 (lag clamped to 1) and a plan reused for fewer transforms than
+    it was created for: the ring schedule must drain for any count."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    n = 1 << m
+    x = torch.from_numpy(complex_signals(60 + m, (3, n))).to(cuda)
+    plan = ops.fft_plan(1, n, 1, 3, cuda)
+    y = torch.empty_like(x)
+    for b in (3, 1, 2):
+        plan.execute(x, y, b)
+        torch.cuda.synchronize()
+        got = y[:b].cpu().numpy()
+        want = fo.fft_rows(x[:b].cpu().numpy())
+        assert max(rel_l2(g, r) for g, r in zip(got, want)) <= tol(n), (m, b)
