@@ -20,6 +20,7 @@ document also runs on the reference engine (slowly) and names its meaning.
 from __future__ import annotations
 
 import os
+import threading
 
 from dataclasses import dataclass, replace
 
@@ -289,6 +290,7 @@ def fft_batch(signals, n: int | None = None, backend: CudaBackend | None = None,
 
 _PIPE_CHUNK_BYTES = int(os.environ.get("DPP_PIPE_CHUNK_MB", "128")) << 20
 _pipes: dict = {}
+_pipes_lock = threading.Lock()
 
 
 def _fft_host_pipelined(signals, n: int, out, dev):
@@ -297,22 +299,32 @@ def _fft_host_pipelined(signals, n: int, out, dev):
     H2D of chunk c+1, the transform of chunk c and the D2H of chunk c-1 run
     concurrently (PCIe is full duplex), so the host round trip the paper names
     as the GPU bottleneck costs max(H2D, D2H) instead of
-    their sum.  Three rotating device slots; transforms run in place."""
+    their sum.  Three rotating device slots; transforms run in place.  A
+    pipeline (streams + slots) is shared per (device, chunk, n) and owned by
+    one caller at a time."""
     import torch
 
-    from .. import ops
     rows = signals.numel() // n
     src = signals.reshape(rows, n)
     dst = out.reshape(rows, n)
     per = max(1, min(rows, _PIPE_CHUNK_BYTES // (8 * n)))
     key = (dev.index, per, n)
-    st = _pipes.get(key)
-    if st is None:
-        st = {"h2d": torch.cuda.Stream(dev), "fft": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
-              "bufs": [torch.empty((per, n), dtype=torch.complex64, device=dev) for _ in range(3)],
-              "loaded": [torch.cuda.Event() for _ in range(3)], "done": [torch.cuda.Event() for _ in range(3)],
-              "free": [None, None, None]}
-        _pipes[key] = st
+    with _pipes_lock:
+        st = _pipes.get(key)
+        if st is None:
+            st = {"h2d": torch.cuda.Stream(dev), "fft": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                  "bufs": [torch.empty((per, n), dtype=torch.complex64, device=dev) for _ in range(3)],
+                  "loaded": [torch.cuda.Event() for _ in range(3)], "done": [torch.cuda.Event() for _ in range(3)],
+                  "free": [None, None, None], "lock": threading.Lock()}
+            _pipes[key] = st
+    with st["lock"]:  # one caller at a time owns the pipeline's streams and slots
+        return _run_pipe(st, src, dst, rows, per, n, dev, out)
+
+
+def _run_pipe(st, src, dst, rows, per, n, dev, out):
+    import torch
+
+    from .. import ops
     caller = torch.cuda.current_stream(dev)
     st["h2d"].wait_stream(caller)
     for c, r0 in enumerate(range(0, rows, per)):
