@@ -141,9 +141,10 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
         if (u + a.ring < a.units) red_release_add(cnt2 + u, 1);
         const int g2 = s_tick[s] & (ITEMS - 1);
         if constexpr (LOGN >= 19) {
+          // four 256-row tiles: output rows k2 = 2 k'' + e, tile (e, k'' >> 8)
 #pragma unroll
-          for (int h = 0; h < 4; ++h)
-            tma_store_2d_hint(&tout, 4 * g2, 1024 * u + 256 * h, smem + s * TILE + h * (TILE / 4), stream_pol);
+          for (int t4 = 0; t4 < 4; ++t4)
+            tma_store_3d(&tout, 4 * g2, t4 >> 1, 512 * u + 256 * (t4 & 1), smem + s * TILE + t4 * (TILE / 4));
         } else {
           tma_store_2d_hint(&tout, 8 * g2, 512 * u, smem + s * TILE, stream_pol);
           tma_store_2d_hint(&tout, 8 * g2, 512 * u + 256, smem + s * TILE + TILE / 2, stream_pol);
@@ -355,16 +356,16 @@ fft_ring512_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__
       bar_compute();  // every warp holds its half-sequence: the stage is free for the exchange
       fft512_warp(v, b + 8u * 512 * (uint32_t)warp, lane, a.twn + (N / 512) * lane, a.twn + N / 32);
       bar_compute();  // every exchange read is done: the stage takes the output tile
-      // X[k1 + (n/1024) k2], k2 = 2 (m0 + 16 m1 + 256 m2) + e: quarter k2 >> 8, row
-      // r = k2 & 255, column p, 32B-swizzled (chunk ^= (r >> 2) & 1)
+      // X[k1 + (n/1024) k2], k2 = 2 k' + e, k' = m0 + 16 m1 + 256 m2: this warp's
+      // outputs are the parity-e rows — tile (e, m2), row r = m0 + 16 m1, column p,
+      // 32B-swizzled (chunk ^= (r >> 2) & 1); a 3-D TMA store puts row r of tile
+      // (e, h) at k2 = 2 (256 h + r) + e
       const int m0r = lane >> 1, l0 = lane & 1;
+      const uint32_t ob = b + 8192u * (uint32_t)(2 * e + l0) + 8u * (uint32_t)(p & 1);
 #pragma unroll
       for (int m1 = 0; m1 < 16; ++m1) {
-        const int k2 = 2 * (m0r + 16 * m1 + 256 * l0) + e;
-        const int r = k2 & 255;
-        sts64(b + 8192u * (uint32_t)(k2 >> 8) + 32u * (uint32_t)r + 16u * (uint32_t)((p >> 1) ^ ((r >> 2) & 1)) +
-                  8u * (uint32_t)(p & 1),
-              v[m1]);
+        const int r = m0r + 16 * m1;
+        sts64(ob + 32u * (uint32_t)r + 16u * (uint32_t)((p >> 1) ^ ((r >> 2) & 1)), v[m1]);
       }
     } else {
       // P2 (2^17, 2^18): warp = k1 % 8, lane b0 holds b = 32 b1 + b0
@@ -468,10 +469,13 @@ int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
       return rc;
   }
   if (lg >= 19) {
-    // output as rows k2 (1024 per transform) x n/1024 columns k1, boxes of 4 columns x 256 rows
-    if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 1024, (uint64_t)(p->n0 / 1024), 256, 4,
-                               CU_TENSOR_MAP_SWIZZLE_32B))
-      return rc;
+    // output rows k2 = 2 k'' + e (1024 per transform) x n/1024 columns k1 as a 3-D view
+    // {k1, e, k''}; boxes of 4 columns x 1 parity x 256 rows
+    const uint64_t cols = (uint64_t)(p->n0 / 1024);
+    const uint64_t dims[3] = {cols, 2, (uint64_t)batch * 512};
+    const uint64_t strides[2] = {cols * 8, cols * 16};
+    const uint32_t box[3] = {4, 1, 256};
+    if (int rc = make_tmap_c64_3d(&tout, out, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_32B)) return rc;
   } else {
     // output as rows k2 (512 per transform) x n/512 columns k1, boxes of 8 columns x 256 rows
     if (int rc = make_tmap_c64(&tout, out, (uint64_t)batch * 512, (uint64_t)(p->n0 / 512), 256, 8,
