@@ -23,9 +23,15 @@ def torch_dtype(dt: DataType) -> torch.dtype:
     return _TORCH_DTYPES[dt.base]
 
 
+_CUDA_OK: bool | None = None
+
+
 def require_cuda(device=None) -> torch.device:
-    if not torch.cuda.is_available():
-        raise NativeLibraryError("no CUDA device: the B200 nodes have no CPU fallback")
+    global _CUDA_OK
+    if not _CUDA_OK:  # a positive answer is cached (the per-call NVML query showed in C1 latency)
+        _CUDA_OK = torch.cuda.is_available()
+        if not _CUDA_OK:
+            raise NativeLibraryError("no CUDA device: the B200 nodes have no CPU fallback")
     dev = torch.device("cuda" if device is None else device)
     if dev.type != "cuda":
         raise NativeLibraryError(f"device {dev} is not a CUDA device")

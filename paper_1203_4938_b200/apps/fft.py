@@ -19,6 +19,7 @@ document also runs on the reference engine (slowly) and names its meaning.
 
 from __future__ import annotations
 
+import functools
 import os
 import threading
 
@@ -27,7 +28,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from ..client import CudaBackend, run
-from ..model import Instance, Node, Program
+from ..model import Instance, Node, Program, frozen_program
 from ..types import DataType, Direction, IOPoint
 from ..wire import DeviceStream, StreamFile
 
@@ -151,9 +152,16 @@ def fft_kernel(n: int) -> Node:
     return Node(f"fft{n}", body, (IOPoint("x", dt, Direction.INPUT), IOPoint("y", dt, Direction.OUTPUT)))
 
 
-def fft_program(n: int) -> Program:
+@functools.lru_cache(maxsize=64)
+def _fft_program_cached(n: int) -> Program:
     node = fft_kernel(n)
-    return Program({node.name: node}, (Instance(0, node.name),), ())
+    return frozen_program(Program({node.name: node}, (Instance(0, node.name),), ()))
+
+
+def fft_program(n: int) -> Program:
+    """One-instance program with the fft{n} node (built once per n and shared;
+    its id is computed once)."""
+    return _fft_program_cached(n)
 
 
 def fft2d_kernel(rows: int, cols: int) -> Node:
