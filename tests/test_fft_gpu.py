@@ -408,3 +408,18 @@ def test_ring_kernels_single_transform_and_smaller_batches(cuda, m):
         got = y[:b].cpu().numpy()
         want = fo.fft_rows(x[:b].cpu().numpy())
         assert max(rel_l2(g, r) for g, r in zip(got, want)) <= tol(n), (m, b)
+
+
+def test_empty_batches_are_no_ops(cuda):
+    """Zero transforms through every kernel family and through the graph API
+    (the reference engine returns empty streams for empty inputs)."""
+    import torch
+
+    from paper_1203_4938_b200 import DataType, StreamFile, ops, run
+    from paper_1203_4938_b200.apps.fft import fft_program
+    for n in (1024, 4096, 65536, 1 << 17, 1 << 21):
+        x = torch.zeros((0, n), dtype=torch.complex64, device=cuda)
+        assert ops.fft_forward(x, n).shape == (0, n)
+    assert ops.fft2d_forward(torch.zeros((0, 4096, 64), dtype=torch.complex64, device=cuda), 4096, 64).numel() == 0
+    out = run(None, fft_program(1024), {"0.x": StreamFile(DataType("float", 2), np.zeros(0, np.float32))})
+    assert out["0.y"].values.size == 0
