@@ -199,14 +199,20 @@ int fft2d_plan_init(FftPlan* p) {
   int width = 0, rc = DPP_ENOTSUP;
   int64_t l1 = 0;
   int cl = 1;
+  const bool ring_only = n0 == 32768;  // no cluster column kernel: the column ring only
   switch (n0) {
 #define PREP(L, A, B, C, W) \
   case L: width = W; l1 = A; cl = C; rc = prepare_columns<A, B, C, W>(); break;
     DPP_COLUMN_TABLE(PREP)
 #undef PREP
   }
+  if (ring_only) {
+    width = 16;
+    l1 = 128;
+    rc = DPP_OK;
+  }
   if (rc == DPP_ENOTSUP)
-    return fail(DPP_ENOTSUP, "2-D column length %lld not supported (256..16384)", (long long)n0);
+    return fail(DPP_ENOTSUP, "2-D column length %lld not supported (256..32768)", (long long)n0);
   if (rc) return rc;
   // A/B switch: 256-byte column tiles for 4096-row images (DPP_FFT_COLW=32)
   const char* ew = getenv("DPP_FFT_COLW");
@@ -233,6 +239,8 @@ int fft2d_plan_init(FftPlan* p) {
   if (rc) return rc;
   rc = fft2d_colring_init(p);
   if (rc != DPP_OK && rc != DPP_ENOTSUP) return rc;
+  if (ring_only && !p->col_ring)
+    return fail(DPP_ENOTSUP, "2-D column length 32768 needs the column ring (row length a multiple of 16)");
   char rows[200];
   snprintf(rows, sizeof(rows), "%s", p->rows->desc);
   if (p->col_ring)

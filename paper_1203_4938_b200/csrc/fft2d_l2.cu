@@ -161,6 +161,81 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
   }
 }
 
+// P1 for B = 32 and 128: L = B / 16 lanes per (column, a) sequence, the
+// B = 64 pattern above with general L (b = L b1 + b0, k1 = m0 + 16 m1, lane j
+// owns m0 = Q j + ii, Q = 16 / L; exchange slot beta = gL(m0) ^ b0 with
+// gL(m0) = L m0 | ((m0 / Q) & (L/2 - 1)), as in csrc/fft16k_l2.cu).
+template <int L>
+__device__ __forceinline__ int gbetaL(int m0) {
+  constexpr int Q = 16 / L;
+  return L * m0 | ((m0 / Q) & (L / 2 - 1));
+}
+template <int L>
+__device__ __forceinline__ void dftLc(float2* v) {
+  if constexpr (L == 2) {
+    const float2 t = v[0];
+    v[0] = make_float2(t.x + v[1].x, t.y + v[1].y);
+    v[1] = make_float2(t.x - v[1].x, t.y - v[1].y);
+  } else if constexpr (L == 4) {
+    dft4c(v[0], v[1], v[2], v[3]);
+  } else {
+    float2 t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = v[q];
+    dft8(t);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = t[q];
+  }
+}
+template <int L>
+__device__ __forceinline__ void p1_bL(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
+                                      const Args& a, uint64_t keep_pol) {
+  constexpr int A = 16 / L, Q = 16 / L;  // a values per item (A * L = 16), m0 values per lane
+  // 256 threads = 16 columns x A a-values x L lanes
+  constexpr int SPW = 32 / L;  // sequences per warp
+  const int b0 = lane / SPW;
+  const int rest = warp * SPW + lane % SPW;  // 0 .. 256 / L - 1: (a, column) of the sequence
+  const int col = rest & 15, alo = (rest >> 4) & (A - 1);
+#pragma unroll
+  for (int b1 = 0; b1 < 16; ++b1) v[b1] = lds64(b + 8u * swz(16 * b1 + A * b0 + alo, col));
+  dft16c(v);  // v[m0]
+  {
+    const float2 wb = __ldg(a.twr + 256 * b0);  // W_B^b0 = W_R^{256 b0}
+    float2 w = wb;
+#pragma unroll
+    for (int m0 = 1; m0 < 16; ++m0) {
+      v[m0] = cmul(v[m0], w);
+      w = cmul(w, wb);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int m0 = 0; m0 < 16; ++m0) sts64(b + 8u * swz(A * (gbetaL<L>(m0) ^ b0) + alo, col), v[m0]);
+  __syncwarp();
+  const int j = b0;  // after the exchange this lane owns m0 = Q j + ii
+#pragma unroll
+  for (int ii = 0; ii < Q; ++ii)
+#pragma unroll
+    for (int c = 0; c < L; ++c) v[L * ii + c] = lds64(b + 8u * swz(A * (gbetaL<L>(Q * j + ii) ^ c) + alo, col));
+#pragma unroll
+  for (int ii = 0; ii < Q; ++ii) dftLc<L>(v + L * ii);  // v[L ii + m1]
+  // W_R^{a k1}, a = A g + alo, k1 = Q j + ii + 16 m1
+  const int ar = A * g + alo;
+  const float2 s1 = __ldg(a.twr + ar), s16 = __ldg(a.twr + 16 * ar);
+  float2 wi = __ldg(a.twr + Q * ar * j);
+  float2* base = slot + swz(ar, col);
+#pragma unroll
+  for (int ii = 0; ii < Q; ++ii) {
+    float2 w = wi;
+#pragma unroll
+    for (int m1 = 0; m1 < L; ++m1) {
+      st_l2_hint(base + 4096 * (Q * j + ii + 16 * m1), cmul(v[L * ii + m1], w), keep_pol);
+      w = cmul(w, s16);
+    }
+    wi = cmul(wi, s1);
+  }
+}
+
 // SPEC: the C5 chain's spectrum_u8 node fused into the output: P2 stages
 // u8 = spectrum(X) (a 16 x 256 byte tile per stage) and TMA-stores bytes.
 //
@@ -177,7 +252,7 @@ __global__ void __launch_bounds__(THREADS, 3)
 fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
              const __grid_constant__ typename MapSet<PEER>::type tout, const Args a) {
   constexpr int A = TILE / (16 * B);  // a values per P1 item
-  constexpr int LOGB = B == 16 ? 4 : 6;
+  constexpr int LOGB = B == 16 ? 4 : (B == 32 ? 5 : (B == 64 ? 6 : 7));
   extern __shared__ __align__(1024) float2 smem[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t done[S];
@@ -314,7 +389,10 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
       if constexpr (B == 16)
         p1_b16<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
       else
-        p1_b64<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
+        if constexpr (B == 64)
+          p1_b64<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
+        else
+          p1_bL<B / 16>(v, b, warp, lane, g, slot, a, keep_pol);
     } else {
       if (DISCARD) discard_l2(slot + 4096 * g + 16 * (tid & 255));
       const uint32_t bA = b + offA;
@@ -369,12 +447,14 @@ static int colring_prepare(int* ctas) {
                                       (int)smem));
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if constexpr (B == 16 || B == 64) {  // the fused spectrum and the four-step twiddle (4096 / 16384 rows)
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
   int per_sm = 0, dev = 0, sms = 0;
   DPP_CUDA_CHECK(
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, colring::fft_cols_l2w<B, true>, colring::THREADS, smem));
@@ -390,7 +470,7 @@ static int colring_prepare(int* ctas) {
 // has no ring schedule.
 int fft2d_colring_init(FftPlan* p) {
   const int64_t R = p->n0;
-  if (!(R == 4096 || R == 16384) || p->n1 % 16) return DPP_ENOTSUP;
+  if (!(R == 4096 || R == 8192 || R == 16384 || R == 32768) || p->n1 % 16) return DPP_ENOTSUP;
   if (const char* e = getenv("DPP_FFT_COLRING"))
     if (atoi(e) == 0) return DPP_ENOTSUP;
   if (g_col_discard < 0) {
@@ -398,7 +478,10 @@ int fft2d_colring_init(FftPlan* p) {
     g_col_discard = e ? atoi(e) != 0 : 1;
   }
   const int B = (int)(R / 256);
-  int rc = B == 16 ? colring_prepare<16>(&p->col_ring_ctas) : colring_prepare<64>(&p->col_ring_ctas);
+  int rc = B == 16 ? colring_prepare<16>(&p->col_ring_ctas)
+                   : B == 32 ? colring_prepare<32>(&p->col_ring_ctas)
+                             : B == 64 ? colring_prepare<64>(&p->col_ring_ctas)
+                                       : colring_prepare<128>(&p->col_ring_ctas);
   if (rc) return rc;
   p->l2_lag = 768 / B;
   if (const char* e = getenv("DPP_FFT_COL_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
@@ -480,6 +563,8 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   const int64_t items = 2 * (int64_t)B * units;
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
   const size_t smem = colring_smem(spec_out != nullptr);
+  if ((twlo || spec_out) && B != 16 && B != 64)
+    return fail(DPP_ENOTSUP, "fused spectrum / twiddled column pass needs 4096 or 16384 rows");
   if (twlo) {
     if (B == 16)
       colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
@@ -490,16 +575,21 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
       colring::fft_cols_l2w<16, true, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
     else
       colring::fft_cols_l2w<64, true, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
-  } else if (B == 16) {
-    if (g_col_discard)
-      colring::fft_cols_l2w<16, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
-    else
-      colring::fft_cols_l2w<16, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
   } else {
-    if (g_col_discard)
-      colring::fft_cols_l2w<64, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
-    else
-      colring::fft_cols_l2w<64, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+#define COLRING_PLAIN(BB)                                                                  \
+  case BB:                                                                                 \
+    if (g_col_discard)                                                                     \
+      colring::fft_cols_l2w<BB, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);  \
+    else                                                                                   \
+      colring::fft_cols_l2w<BB, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); \
+    break;
+    switch (B) {
+      COLRING_PLAIN(16)
+      COLRING_PLAIN(32)
+      COLRING_PLAIN(64)
+      COLRING_PLAIN(128)
+    }
+#undef COLRING_PLAIN
   }
   DPP_LAUNCH_CHECK("fft_cols_l2w");
   DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
@@ -570,10 +660,12 @@ int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, flo
   const int64_t items = 2 * (int64_t)B * units;
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
   const size_t smem = colring_smem(false);
-  if (B == 16)
-    colring::fft_cols_l2w<16, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
-  else
-    colring::fft_cols_l2w<64, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  switch (B) {
+    case 16: colring::fft_cols_l2w<16, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+    case 32: colring::fft_cols_l2w<32, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+    case 64: colring::fft_cols_l2w<64, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+    default: colring::fft_cols_l2w<128, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  }
   DPP_LAUNCH_CHECK("fft_cols_l2w<peer>");
   DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
   return DPP_OK;

@@ -121,7 +121,7 @@ def test_large_batch_checksum_against_sampled_oracle(cuda):
 
 
 @pytest.mark.parametrize("shape", [(256, 32), (512, 64), (1024, 256), (2048, 16), (4096, 64),
-                                   (8192, 8), (16384, 8)])
+                                   (8192, 8), (8192, 32), (16384, 8), (32768, 16)])
 def test_2d_vs_composed_oracle(cuda, shape):
     import torch
 
@@ -295,7 +295,11 @@ sys.path.insert(0, {tests!r})
 from conftest import complex_signals, rel_l2
 from paper_1203_4938_b200 import ops
 worst = 0.0
-for (r, c, b) in ((4096, 64, 5), (16384, 32, 3)):
+import os
+shapes = [(4096, 64, 5), (8192, 32, 3), (16384, 32, 3)]
+if os.environ.get("DPP_FFT_COLRING") != "0":
+    shapes.append((32768, 16, 2))  # the column ring is the only column pass for 32768 rows
+for (r, c, b) in shapes:
     x = complex_signals(r + c, (b, r, c))
     xt = torch.from_numpy(x).cuda()
     got = ops.fft2d_forward(xt, r, c).cpu().numpy()
@@ -311,7 +315,7 @@ print(worst)
                                  {"DPP_FFT_COLRING": "0"}],
                          ids=["ring4-lag2", "no-discard", "cluster-columns"])
 def test_2d_column_pass_variants(cuda, env):
-    # the L2-ring column pass (4096- and 16384-row images) with a 4-slot ring
+    # the L2-ring column pass (4096- to 32768-row images) with a 4-slot ring
     # (every slot reused, both waits fire), without L2 discards, and the
     # cluster column kernel it replaced; in place == out of place, numpy fft2
     import os

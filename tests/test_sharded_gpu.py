@@ -132,3 +132,14 @@ def test_rejects_unsupported_shapes():
     with pytest.raises((PlanError, ValueError)):
         from paper_1203_4938_b200.distributed import PeerShardedFft2d
         PeerShardedFft2d(4096, 24, 1)
+
+
+@pytest.mark.parametrize("n0,n1", [(8192, 64), (32768, 32)])
+def test_single_rank_other_column_lengths(n0, n1):
+    """The PEER column pass for the 32- and 128-row-group rings (8192, 32768 rows)."""
+    from paper_1203_4938_b200.distributed import PeerShardedFft2d
+    full = _input(n0, n1, 1)
+    sh = PeerShardedFft2d(n0, n1, 1)
+    for back in (True, False):
+        out = sh(torch.from_numpy(full).cuda(), transpose_back=back).cpu().numpy()
+        assert np.array_equal(out, _single_gpu(full))
