@@ -61,7 +61,7 @@ typedef struct dpp_fft_plan dpp_fft_plan;
 
 /* Create a forward, unnormalised complex-to-complex plan.
  *   rank 1: `batch` contiguous transforms of n0 points (n1 ignored).
- *   rank 2: `batch` contiguous n0 x n1 row-major 2-D transforms.
+ *   rank 2: `batch` contiguous n0 x n1 row-major 2-D transforms (n0 256..32768).
  * Sizes must be powers of two >= 2 (same rule as FftPlan, fft.py:133-139);
  * rank 1 up to 2^30 (above 2^20: three passes, and in-place calls stage
  * through a plan-owned scratch of <= 256 MB or one transform, allocated on
@@ -114,7 +114,7 @@ void dpp_fft_plan_destroy(dpp_fft_plan* plan);
  * results are stored into every rank's row slab outs[j] (natural row-sharded
  * layout; outs may equal slabs); else into this rank's batch x n0 x (n1/P)
  * column slab outs[0].  A second dpp_peer_barrier must follow before any rank
- * reuses its slabs.  plan: rank 2, n0 x n1, n0 in {4096, 16384}
+ * reuses its slabs.  plan: rank 2, n0 x n1, n0 in {4096, 8192, 16384, 32768}
  * (DPP_ENOTSUP otherwise); nranks a power of two <= 8 dividing n0/256;
  * n1 a multiple of 16*nranks. */
 int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slabs, float* const* outs,
