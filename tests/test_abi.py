@@ -22,6 +22,25 @@ def test_header_and_binding_agree():
     assert declared_symbols() == set(_lib.SIGNATURES)
 
 
+def declared_arity() -> dict[str, int]:
+    """Parameter count of every prototype in the header."""
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    out = {}
+    for name, params in re.findall(r"\b(dpp_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", text, flags=re.S):
+        params = params.strip()
+        out[name] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_binding_arity_matches_the_header():
+    """ctypes argtypes have exactly as many entries as the C prototypes
+    (a missing or extra argument would shift every pointer after it)."""
+    arity = declared_arity()
+    assert set(arity) == set(_lib.SIGNATURES)
+    for name, (_, argtypes) in _lib.SIGNATURES.items():
+        assert len(argtypes) == arity[name], (name, len(argtypes), arity[name])
+
+
 def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in declared_symbols():
