@@ -244,7 +244,18 @@ def match_fft(node):
     m = re.match(re.escape(NATIVE_TAG) + r" fft2d rows=(\d+) cols=(\d+)\n", node.body)
     if m:
         r, c = int(m.group(1)), int(m.group(2))
-        return Fft2dNode(r, c) if node.body == fft2d_kernel(r, c).body else None
+        if node.body != fft2d_kernel(r, c).body:
+            return None
+        # shapes without a native 2-D schedule (column length < 256, or rows
+        # narrower than a column tile) run the node's own naive-DFT body
+        # through the JIT: the document's meaning, on the GPU, just O(N^2)
+        from . import ops
+        from .errors import PlanError
+        try:
+            ops.fft_plan(2, r, c, 1)
+        except PlanError:
+            return None
+        return Fft2dNode(r, c)
     return None
 
 

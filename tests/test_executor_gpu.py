@@ -158,3 +158,16 @@ def test_chunked_host_streams_pipeline(cuda):
     sf = StreamFile(DataType("float", 16), y)
     a = run(CudaBackend(chunk_size=1000, max_in_flight=3), leaf_program(3), {"0.x": sf})["0.y"].values
     assert np.array_equal(a, fo.leaf_eval(3, y).ravel())
+
+
+def test_fft2d_node_without_a_native_schedule_runs_its_body(cuda):
+    """fft2d_8x16 (column length < 256): the node's naive-DFT body through the
+    JIT on the GPU — the document's meaning (tests/golden/docs_golden.npz)."""
+    from paper_1203_4938_b200 import DataType, StreamFile, run
+    from paper_1203_4938_b200.apps.fft import fft2d_program
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((2, 8, 16)) + 1j * rng.standard_normal((2, 8, 16))).astype(np.complex64)
+    sf = StreamFile(DataType("float", 2), x.view(np.float32).reshape(-1))
+    y = run(None, fft2d_program(8, 16), {"0.x": sf})["0.y"].values.view(np.complex64).reshape(2, 8, 16)
+    ref = np.fft.fft2(x.astype(np.complex128))
+    assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-5
