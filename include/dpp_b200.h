@@ -114,7 +114,7 @@ void dpp_fft_plan_destroy(dpp_fft_plan* plan);
  * results are stored into every rank's row slab outs[j] (natural row-sharded
  * layout; outs may equal slabs); else into this rank's batch x n0 x (n1/P)
  * column slab outs[0].  A second dpp_peer_barrier must follow before any rank
- * reuses its slabs.  plan: rank 2, n0 x n1, n0 in {4096, 8192, 16384, 32768}
+ * reuses its slabs.  plan: rank 2, n0 x n1, n0 in 1024 .. 32768
  * (DPP_ENOTSUP otherwise); nranks a power of two <= 8 dividing n0/256;
  * n1 a multiple of 16*nranks. */
 int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slabs, float* const* outs,

@@ -161,6 +161,47 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
   }
 }
 
+// P1 for B = 4 and 8 (1024- and 2048-row images): S = 16 / B whole sequences
+// per thread, in registers (the B = 16 pattern with A = 16 S a-values per
+// item): thread (col, t) owns a = t + 16 s, s < S.
+template <int B>
+__device__ __forceinline__ void p1_bsmall(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
+                                          const Args& a, uint64_t keep_pol) {
+  constexpr int S = 16 / B, A = 16 * S;
+  const int col = lane & 15, t = 2 * warp + (lane >> 4);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int bb = 0; bb < B; ++bb) v[s * B + bb] = lds64(b + 8u * swz(A * bb + t + 16 * s, col));
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    if constexpr (B == 8) {
+      float2 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) u[q] = v[s * 8 + q];
+      dft8(u);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[s * 8 + q] = u[q];
+    } else {
+      dft4c(v[s * 4], v[s * 4 + 1], v[s * 4 + 2], v[s * 4 + 3]);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int ar = A * g + t + 16 * s;
+    const float2 wa = __ldg(a.twr + ar);  // W_R^a
+    float2 w = wa;
+#pragma unroll
+    for (int k1 = 1; k1 < B; ++k1) {
+      v[s * B + k1] = cmul(v[s * B + k1], w);
+      w = cmul(w, wa);
+    }
+    float2* dst = slot + swz(ar, col);
+#pragma unroll
+    for (int k1 = 0; k1 < B; ++k1) st_l2_hint(dst + 4096 * k1, v[s * B + k1], keep_pol);
+  }
+}
+
 // P1 for B = 32 and 128: L = B / 16 lanes per (column, a) sequence, the
 // B = 64 pattern above with general L (b = L b1 + b0, k1 = m0 + 16 m1, lane j
 // owns m0 = Q j + ii, Q = 16 / L; exchange slot beta = gL(m0) ^ b0 with
@@ -252,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, 3)
 fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
              const __grid_constant__ typename MapSet<PEER>::type tout, const Args a) {
   constexpr int A = TILE / (16 * B);  // a values per P1 item
-  constexpr int LOGB = B == 16 ? 4 : (B == 32 ? 5 : (B == 64 ? 6 : 7));
+  constexpr int LOGB = B == 4 ? 2 : (B == 8 ? 3 : (B == 16 ? 4 : (B == 32 ? 5 : (B == 64 ? 6 : 7))));
   extern __shared__ __align__(1024) float2 smem[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t done[S];
@@ -391,6 +432,8 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
       else
         if constexpr (B == 64)
           p1_b64<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
+        else if constexpr (B < 16)
+          p1_bsmall<B>(v, b, warp, lane, g, slot, a, keep_pol);
         else
           p1_bL<B / 16>(v, b, warp, lane, g, slot, a, keep_pol);
     } else {
@@ -470,7 +513,8 @@ static int colring_prepare(int* ctas) {
 // has no ring schedule.
 int fft2d_colring_init(FftPlan* p) {
   const int64_t R = p->n0;
-  if (!(R == 4096 || R == 8192 || R == 16384 || R == 32768) || p->n1 % 16) return DPP_ENOTSUP;
+  if (!(R == 1024 || R == 2048 || R == 4096 || R == 8192 || R == 16384 || R == 32768) || p->n1 % 16)
+    return DPP_ENOTSUP;
   if (const char* e = getenv("DPP_FFT_COLRING"))
     if (atoi(e) == 0) return DPP_ENOTSUP;
   if (g_col_discard < 0) {
@@ -478,7 +522,9 @@ int fft2d_colring_init(FftPlan* p) {
     g_col_discard = e ? atoi(e) != 0 : 1;
   }
   const int B = (int)(R / 256);
-  int rc = B == 16 ? colring_prepare<16>(&p->col_ring_ctas)
+  int rc = B == 4    ? colring_prepare<4>(&p->col_ring_ctas)
+           : B == 8  ? colring_prepare<8>(&p->col_ring_ctas)
+           : B == 16 ? colring_prepare<16>(&p->col_ring_ctas)
                    : B == 32 ? colring_prepare<32>(&p->col_ring_ctas)
                              : B == 64 ? colring_prepare<64>(&p->col_ring_ctas)
                                        : colring_prepare<128>(&p->col_ring_ctas);
@@ -584,6 +630,8 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
       colring::fft_cols_l2w<BB, false><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); \
     break;
     switch (B) {
+      COLRING_PLAIN(4)
+      COLRING_PLAIN(8)
       COLRING_PLAIN(16)
       COLRING_PLAIN(32)
       COLRING_PLAIN(64)
@@ -661,6 +709,8 @@ int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, flo
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
   const size_t smem = colring_smem(false);
   switch (B) {
+    case 4: colring::fft_cols_l2w<4, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+    case 8: colring::fft_cols_l2w<8, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
     case 16: colring::fft_cols_l2w<16, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
     case 32: colring::fft_cols_l2w<32, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
     case 64: colring::fft_cols_l2w<64, true, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;

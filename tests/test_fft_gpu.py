@@ -120,7 +120,7 @@ def test_large_batch_checksum_against_sampled_oracle(cuda):
         assert rel_l2(y[row].cpu().numpy(), fo.fft(xr)) <= tol(n)
 
 
-@pytest.mark.parametrize("shape", [(256, 32), (512, 64), (1024, 256), (2048, 16), (4096, 64),
+@pytest.mark.parametrize("shape", [(256, 32), (512, 64), (1024, 256), (1024, 16), (2048, 16), (2048, 32), (4096, 64),
                                    (8192, 8), (8192, 32), (16384, 8), (32768, 16)])
 def test_2d_vs_composed_oracle(cuda, shape):
     import torch
@@ -296,7 +296,7 @@ from conftest import complex_signals, rel_l2
 from paper_1203_4938_b200 import ops
 worst = 0.0
 import os
-shapes = [(4096, 64, 5), (8192, 32, 3), (16384, 32, 3)]
+shapes = [(1024, 64, 5), (2048, 32, 5), (4096, 64, 5), (8192, 32, 3), (16384, 32, 3)]
 if os.environ.get("DPP_FFT_COLRING") != "0":
     shapes.append((32768, 16, 2))  # the column ring is the only column pass for 32768 rows
 for (r, c, b) in shapes:

@@ -134,7 +134,7 @@ def test_rejects_unsupported_shapes():
         PeerShardedFft2d(4096, 24, 1)
 
 
-@pytest.mark.parametrize("n0,n1", [(8192, 64), (32768, 32)])
+@pytest.mark.parametrize("n0,n1", [(1024, 64), (2048, 32), (8192, 64), (32768, 32)])
 def test_single_rank_other_column_lengths(n0, n1):
     """The PEER column pass for the 32- and 128-row-group rings (8192, 32768 rows)."""
     from paper_1203_4938_b200.distributed import PeerShardedFft2d
