@@ -127,7 +127,7 @@ def test_rejects_unsupported_shapes():
     assert lib.dpp_fft2d_columns_sharded(plan._h, arr, arr, 3, 0, 1, 1, None) == _lib.DPP_EINVAL
     # 256 columns do not split into 16-column tiles over 32 ranks
     assert lib.dpp_fft2d_columns_sharded(plan._h, arr, arr, 32, 0, 1, 1, None) == _lib.DPP_EINVAL
-    plan_small = ops.fft_plan(2, 1024, 256, 1)  # no column ring for 1024 rows
+    plan_small = ops.fft_plan(2, 512, 256, 1)  # no column ring for 512 rows
     assert lib.dpp_fft2d_columns_sharded(plan_small._h, arr, arr, 2, 0, 1, 1, None) == _lib.DPP_ENOTSUP
     with pytest.raises((PlanError, ValueError)):
         from paper_1203_4938_b200.distributed import PeerShardedFft2d
