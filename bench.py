@@ -1,31 +1,41 @@
-"""Benchmark: batched 1-D complex FFT N=2^16 x 4096 (BASELINE.json configs[1]).
+"""Benchmark: batched 1-D complex FFT N=2^16 x 4096 per GPU (BASELINE.json configs[1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one forward transform of the whole batch (4096 signals of 65536
-complex64 = 2 GiB in, 2 GiB out), inputs resident in HBM; inputs are larger
-than L2 (126 MB) so no flush is needed.  Rank 0 prints ONE JSON line.
+One step = one forward transform of the whole per-GPU batch (4096 signals of
+65536 complex64 = 2 GiB in, 2 GiB out), inputs resident in HBM; inputs are
+larger than L2 (126 MB) so no flush is needed.  Rank 0 prints ONE JSON line.
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (one process per GPU, NCCL).
 
-* value: FFT GFLOP/s, 5*N*log2(N) per transform, whole job (all ranks).
+* value: FFT GFLOP/s, 5*N*log2(N) per transform, whole job (all ranks, weak
+  scaling: every rank transforms its own 4096 signals, no collective).
 * roofline: HBM-bound; achieved = 16*N bytes per transform / kernel time.
-* e2e: same metric through the public API (apps.fft.fft_batch) with pinned
-  host buffers, H2D + transform + D2H inside the timed region.
-* cpu_baseline: the oracle restatement of the reference fft()
-  (oracle/fft_oracle.py) on the host, bounded sample, rank 0 only.
-* secondary.compression: C4 (8192^2 gray, block transform + quantise +
-  order, 256-entry codebook) MPixel/s on the same GPU.
-Multi-GPU (torchrun): every rank runs the full per-GPU batch (weak
-scaling, no collective on the data path); time = max over ranks.
+* e2e: the same metric through the public API (apps.fft.fft_batch) from
+  pinned host tensors, H2D + transform + D2H inside the timed region;
+  e2e_graph: through the reference-shaped graph API (run() on numpy streams).
+* parity: size-independent identities on every signal (checksum, Parseval),
+  numpy float64 FFTs of sampled signals, and — rank 0 at N=1, in the
+  cpu_baseline leg — the oracle restatement of the reference fft() on the
+  sampled signals it times.
+* secondary: C1 latency, C3 2-D 16384^2 (row-sharded at N>1, exchange fused
+  into the column pass over NVLink), C4 8192^2 compression of the §8(d) frame
+  (tile-sharded across ranks, bitstream SHA-256 vs the reference's), C5 chain
+  of 64 4096^2 images (image-sharded), each with roofline, parity and CPU
+  baseline.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 from pathlib import Path
@@ -34,13 +44,17 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+GOLDEN = ROOT / "tests" / "golden"
 
 N = 1 << 16
 BATCH = 4096
 FLOPS_PER_TRANSFORM = 5.0 * N * 16  # 5 N log2 N
 BYTES_PER_TRANSFORM = 16.0 * N      # complex64 read once + written once
 METRIC = "FFT GFLOP/s (5N·log2N)"
-WORKLOAD = "batched 1D complex fp32 FFT N=2^16, batch 4096, on 1 B200 (configs[1])"
+
+
+def workload(n_gpus: int) -> str:
+    return f"batched 1D complex fp32 FFT N=2^16, batch 4096 per GPU, on {n_gpus} B200 (configs[1])"
 
 
 def peaks() -> dict:
@@ -121,25 +135,21 @@ def max_over_ranks(value: float, world: int) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64,
+                     device="cpu" if dist.get_backend() == "gloo" else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-
-
-# ---------------------------------------------------------------------------
-# CPU baseline (oracle restatement of the reference fft(); tests/bench only)
-
-def _cpu_chunk(args):
-    seed, count = args
-    from oracle import fft_oracle
-    rng = np.random.default_rng(seed)
-    x = (rng.standard_normal((count, N), dtype=np.float32)
-         + 1j * rng.standard_normal((count, N), dtype=np.float32)).astype(np.complex64)
-    t0 = time.perf_counter()
-    for row in x:
-        fft_oracle.fft(row)
-    return time.perf_counter() - t0, count
 
 
 def host_info() -> dict:
@@ -157,42 +167,136 @@ def host_info() -> dict:
             "threads_env": {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")}}
 
 
-def cpu_baseline(threads: int, seconds: float = 12.0) -> dict:
-    """Reference-algorithm FFT on host cores: per-signal fft() calls, bounded sample."""
+def sha(b) -> str:
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+def rel_l2(got, ref) -> float:
+    """Relative L2 error with plain numpy reductions (np.linalg.norm would use
+    multi-threaded BLAS and oversubscribe the CPU legs' worker processes)."""
+    got = np.asarray(got, np.complex128)
+    ref = np.asarray(ref, np.complex128)
+    num = float(np.sum((got.real - ref.real) ** 2 + (got.imag - ref.imag) ** 2))
+    den = float(np.sum(ref.real ** 2 + ref.imag ** 2))
+    return float(np.sqrt(num / max(den, 1e-300)))
+
+
+def _pool(threads: int):
+    """Spawn pool for the CPU legs, one single-threaded numpy per process."""
     import multiprocessing as mp
-    per_worker = 4
-    with mp.get_context("spawn").Pool(threads) as pool:
-        pool.map(_cpu_chunk, [(1, 1)] * threads)  # warm imports
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(k, "1")
+    return mp.get_context("spawn").Pool(threads)
+
+
+def timed(fn, steps: int, stream) -> float:
+    """Average device ms per call of fn() over `steps` calls (CUDA events on `stream`)."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the oracle restatement of the reference algorithms on host cores
+# (test infrastructure, used here only as the checker and the CPU baseline)
+
+def _fft_rows_leg(args):
+    """Oracle fft() on rows [lo, hi) of the memory-mapped sample; returns
+    (seconds of compute, rows, max rel-L2 of the GPU rows against it)."""
+    path_x, path_y, lo, hi = args
+    from oracle import fft_oracle
+    x = np.load(path_x, mmap_mode="r")[lo:hi]
+    y = np.load(path_y, mmap_mode="r")[lo:hi]
+    worst = 0.0
+    t = 0.0
+    for xr, yr in zip(x, y):
+        xr = np.array(xr)
         t0 = time.perf_counter()
-        done = 0
-        seed = 100
-        while time.perf_counter() - t0 < seconds:
-            res = pool.map(_cpu_chunk, [(seed + i, per_worker) for i in range(threads)])
-            seed += threads
-            done += sum(c for _, c in res)
+        ref = fft_oracle.fft(xr)
+        t += time.perf_counter() - t0
+        worst = max(worst, rel_l2(yr, ref))
+    return t, hi - lo, worst
+
+
+def c2_cpu_leg(x_host, y_host, threads: int, seconds: float) -> dict:
+    """Reference fft() algorithm (oracle port) on the host, every core: the
+    first signals of the GPU's own batch, cycled for ~`seconds`; also the
+    GPU-vs-oracle parity of every sampled signal."""
+    rows = min(len(x_host), 4 * threads)
+    tmp = Path(tempfile.mkdtemp(prefix="dpp_bench_"))
+    px, py = tmp / "x.npy", tmp / "y.npy"
+    np.save(px, np.ascontiguousarray(x_host[:rows]))
+    np.save(py, np.ascontiguousarray(y_host[:rows]))
+    per = max(1, rows // threads)
+    tasks = [(str(px), str(py), lo, min(rows, lo + per)) for lo in range(0, rows, per)]
+    worst, done = 0.0, 0
+    with _pool(threads) as pool:
+        pool.map(_fft_rows_leg, [(str(px), str(py), 0, 1)] * threads)  # warm imports
+        t0 = time.perf_counter()
+        while True:
+            for _, cnt, w in pool.map(_fft_rows_leg, tasks):
+                done += cnt
+                worst = max(worst, w)
+            if time.perf_counter() - t0 >= seconds:
+                break
         wall = time.perf_counter() - t0
+    for p in (px, py):
+        p.unlink()
+    tmp.rmdir()
     value = done * FLOPS_PER_TRANSFORM / wall / 1e9
     return {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port", "host": host_info(),
-            "sample": f"{done} signals of N=2^16 (the step is 4096), reference fft() algorithm "
-                      f"(oracle/fft_oracle.py: host bit-reversal, binary32 dft8 leaves, binary64 "
-                      f"butterflies), {threads} processes, {wall:.1f} s wall"}
+            "sample": f"{done} signals of N=2^16 (the first {rows} of the GPU batch, cycled; the step is 4096), "
+                      f"reference fft() algorithm (oracle/fft_oracle.py: host bit-reversal, binary32 dft8 "
+                      f"leaves, binary64 butterflies), {threads} processes, {wall:.1f} s wall",
+            "oracle_signals": rows, "oracle_max_rel_l2": worst}
 
 
-def _c4_chunk(args):
-    """Reference compress() steps 1-8 (codebook given, like the GPU node) on one image."""
-    seed, side = args
+def _c4_band_leg(args):
+    """Oracle compress() steps 1-8 (codebook given, like the GPU node) on one band of the frame."""
+    path, lo, hi, cb = args
     from oracle import imgc_oracle as io
-    rng = np.random.default_rng(seed)
-    g = rng.integers(0, 256, (side, side), dtype=np.uint8)
-    img = np.repeat(g[..., None], 3, 2)
-    cb = rng.standard_normal((256, 16))
-    cb = ((cb - cb.mean(1, keepdims=True)) / cb.std(1, keepdims=True)).astype(np.float32)
+    g = np.load(path, mmap_mode="r")[4 * lo:4 * hi]
+    img = np.repeat(np.asarray(g)[..., None], 3, 2)
     t0 = time.perf_counter()
-    io.encode(img, cb)
-    return time.perf_counter() - t0, side * side
+    f = io.encode(img, cb)
+    t = time.perf_counter() - t0
+    rec = np.stack([f["means"], f["sigma_idx"], f["indices"]], 1)
+    return t, img.shape[0] * img.shape[1], lo, rec, f["cb"].ravel(), f["cr"].ravel()
 
 
-def _c3_chunk(args):
+def c4_cpu_leg(gray, codebook, rec, cbp, crp, threads: int) -> dict:
+    """Oracle encoder on `threads` bands of 32 block rows of the same frame;
+    parity = records / chroma bytes of those bands against the GPU's."""
+    tmp = Path(tempfile.mkdtemp(prefix="dpp_bench_"))
+    path = tmp / "g.npy"
+    np.save(path, gray)
+    bh, bw = gray.shape[0] // 4, gray.shape[1] // 4
+    rows_per = 32
+    starts = np.linspace(0, bh - rows_per, threads).astype(int)
+    with _pool(threads) as pool:
+        pool.map(_c4_band_leg, [(str(path), 0, 1, codebook)] * threads)
+        t0 = time.perf_counter()
+        res = pool.map(_c4_band_leg, [(str(path), int(s), int(s) + rows_per, codebook) for s in starts])
+        wall = time.perf_counter() - t0
+    path.unlink()
+    tmp.rmdir()
+    bad = 0
+    for _, _, lo, r, c1, c2 in res:
+        sl = slice(lo * bw, (lo + rows_per) * bw)
+        bad += int((rec[sl] != r).any(axis=1).sum() + (cbp[sl] != c1).sum() + (crp[sl] != c2).sum())
+    px = sum(r[1] for r in res)
+    return {"value": round(px / wall / 1e6, 4), "unit": "MPixel/s", "cores": threads, "kind": "port",
+            "sample": f"{len(res)} bands of {rows_per} block rows of the same frame through compress() steps "
+                      f"1-8 with the reference codebook (k-means excluded, as on the GPU), {wall:.1f} s wall",
+            "oracle_blocks": len(res) * rows_per * bw, "oracle_differing": bad}
+
+
+def _c3_rows_leg(args):
     seed, count, n = args
     from oracle import fft_oracle
     rng = np.random.default_rng(seed)
@@ -203,11 +307,21 @@ def _c3_chunk(args):
     return time.perf_counter() - t0, count
 
 
-def secondary_cpu_baselines(threads: int) -> dict:
-    """Bounded host samples of the reference algorithms for C1, C3 and C4 (oracle port)."""
-    import multiprocessing as mp
+def c3_cpu_leg(threads: int) -> dict:
+    with _pool(threads) as pool:
+        pool.map(_c3_rows_leg, [(1, 1, 256)] * threads)
+        t0 = time.perf_counter()
+        res = pool.map(_c3_rows_leg, [(7 + i, 64, 16384) for i in range(threads)])
+        wall = time.perf_counter() - t0
+    rows = sum(c for _, c in res)
+    # the 2-D transform is 2 x 16384 such row transforms (composition)
+    return {"value": round(rows * 5.0 * 16384 * 14 / wall / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
+            "kind": "port", "sample": f"{rows} row transforms of 16384 (reference fft() per row; the 2-D result "
+                                      f"is the composition over 2 x 16384 rows), {wall:.1f} s wall"}
+
+
+def c1_cpu_leg() -> dict:
     from oracle import fft_oracle
-    out = {}
     rng = np.random.default_rng(42)
     x1 = (rng.standard_normal(1024) + 1j * rng.standard_normal(1024)).astype(np.complex64)
     fft_oracle.fft(x1)
@@ -217,29 +331,42 @@ def secondary_cpu_baselines(threads: int) -> dict:
         fft_oracle.fft(x1)
         lat.append((time.perf_counter() - t0) * 1e3)
     lat.sort()
-    out["c1"] = {"value": round(lat[len(lat) // 2], 4), "unit": "ms (median)", "cores": 1, "kind": "port",
-                 "sample": "20 calls of fft(x), N=1024 k=3 (the port has no kernel-language compile; the "
-                           "reference's fft() spends ~7 ms of its 8.35 ms there, BASELINE.md §2)"}
-    with mp.get_context("spawn").Pool(threads) as pool:
-        pool.map(_c3_chunk, [(1, 1, 256)] * threads)
-        t0 = time.perf_counter()
-        res = pool.map(_c3_chunk, [(7 + i, 64, 16384) for i in range(threads)])
-        wall = time.perf_counter() - t0
-        rows = sum(c for _, c in res)
-        # the 2-D transform is 2 x 16384 such row transforms (composition)
-        gflops = rows * 5.0 * 16384 * 14 / wall / 1e9
-        out["c3"] = {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                     "sample": f"{rows} row transforms of 16384 (reference fft() per row; the 2-D result is "
-                               f"the composition over 2 x 16384 rows), {wall:.1f} s wall"}
-        pool.map(_c4_chunk, [(1, 64)] * threads)
-        t0 = time.perf_counter()
-        res = pool.map(_c4_chunk, [(11 + i, 1536) for i in range(threads)])
-        wall = time.perf_counter() - t0
-        px = sum(c for _, c in res)
-        out["c4"] = {"value": round(px / wall / 1e6, 4), "unit": "MPixel/s", "cores": threads, "kind": "port",
-                     "sample": f"{len(res)} gray 1536^2 images through compress() steps 1-8 with a given "
-                               f"256-entry codebook (k-means excluded, as on the GPU), {wall:.1f} s wall"}
-    return out
+    return {"value": round(lat[len(lat) // 2], 4), "unit": "ms (median)", "cores": 1, "kind": "port",
+            "sample": "20 calls of fft(x), N=1024 k=3 (the port has no kernel-language compile; the "
+                      "reference's fft() spends ~7 ms of its 8.35 ms there, BASELINE.md §2)"}
+
+
+def c5_cpu_leg(gray0, codebook0, spec_gpu, out0) -> dict:
+    """Oracle chain on image 0 (composed reference FFT, the adapter as the
+    engine evaluates it, compress() with the given codebook), 1 core, x64;
+    parity: adapter mismatches and records of the oracle encoder on the
+    GPU's own adapter output."""
+    from oracle import chain_oracle as co
+    from oracle import fft_oracle as fo
+    from oracle import imgc_oracle as io
+    from paper_1203_4938_b200.apps.chain import ALPHA
+    t0 = time.perf_counter()
+    spec = co.spectrum_u8(fo.fft2(co.to_complex(gray0)), ALPHA)
+    f_ref = io.encode(np.repeat(spec[..., None], 3, 2), codebook0)
+    secs = time.perf_counter() - t0
+    f = f_ref if np.array_equal(spec, spec_gpu) else io.encode(np.repeat(spec_gpu[..., None], 3, 2), codebook0)
+    bad = int(((out0["mu"] != f["means"]) | (out0["sig"] != f["sigma_idx"]) | (out0["idx"] != f["indices"])).sum()
+              + (out0["cb"] != f["cb"].ravel()).sum() + (out0["cr"] != f["cr"].ravel()).sum())
+    ref_secs = None
+    gp = GOLDEN / "c5_golden.npz"
+    if gp.exists():
+        g = np.load(gp)
+        ref_secs = [round(float(v), 1) for v in g["seconds_0"]]
+    return {"value": round(1.0 / secs, 5), "unit": "images/s", "cores": 1, "kind": "port",
+            "sample": f"image 0 of 64 through the oracle chain (composed reference fft() rows+columns, adapter, "
+                      f"compress() steps 1-8 with the given codebook), {secs:.1f} s; the step is 64 images, "
+                      f"extrapolated x64 = {64 * secs:.0f} s",
+            "reference_seconds_image0_build_container": ref_secs,
+            "reference_note": "the REFERENCE itself on image 0 in the build container (tests/golden/"
+                              "make_fullsize_golden.py): [fft() rows+columns, adapter on the engine, "
+                              "compress() incl. k-means] seconds",
+            "parity": {"adapter_mismatches": int((spec != spec_gpu).sum()), "pixels": int(spec.size),
+                       "records_differing": bad}}
 
 
 # ---------------------------------------------------------------------------
@@ -249,19 +376,45 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
+    n_gpus = world if world > 1 else args.gpus
     steps = []
+    seconds = max(5.0, 60.0 / (args.warmup + args.steps))
+    rng = np.random.default_rng(42)
+    x = (rng.standard_normal((4 * threads, N), dtype=np.float32)
+         + 1j * rng.standard_normal((4 * threads, N), dtype=np.float32)).astype(np.complex64)
     for _ in range(args.warmup + args.steps):
-        steps.append(cpu_baseline(threads, seconds=max(5.0, 60.0 / (args.warmup + args.steps))))
-    timed = steps[args.warmup:]
-    value = statistics.median(s["value"] for s in timed)
+        steps.append(c2_cpu_leg(x, x, threads, seconds))
+    timed_steps = steps[args.warmup:]
+    value = statistics.median(s["value"] for s in timed_steps)
+    cpu = {k: v for k, v in timed_steps[-1].items() if not k.startswith("oracle_")}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": BATCH * FLOPS_PER_TRANSFORM / (value * 1e9) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "n": N, "batch": BATCH},
-            "cpu_baseline": {**timed[-1], "value": value},
+            "data": "synthetic", "config": {"workload": workload(n_gpus), "n": N, "batch": BATCH},
+            "cpu_baseline": {**cpu, "value": value},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torchrun: re-launch this script as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def _gen_image(args):
+    side, seed = args
+    from paper_1203_4938_b200.apps.imgc import synthetic_image
+    return synthetic_image(side, side, seed=seed)[..., 1].copy()
 
 
 def run_ours(args) -> None:
@@ -281,13 +434,17 @@ def run_ours(args) -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cores = len(os.sched_getaffinity(0))
+    cpu_legs = world == 1 and not args.no_cpu and rank == 0
 
     from paper_1203_4938_b200 import ops
     from paper_1203_4938_b200.apps import fft as afft
-    from paper_1203_4938_b200.apps import imgc as aimgc
 
-    gen = torch.Generator(device=dev).manual_seed(42 + rank)
-    x = torch.randn((BATCH, N), dtype=torch.complex64, device=dev, generator=gen)
+    # ------------------------------------------------------------------ C2
+    rng = np.random.default_rng(42 + rank)  # SURVEY §8(d) C2 recipe (rank 0)
+    x_host = (rng.standard_normal((BATCH, N), dtype=np.float32)
+              + 1j * rng.standard_normal((BATCH, N), dtype=np.float32)).astype(np.complex64)
+    x = torch.from_numpy(x_host).to(dev)
     y = torch.empty_like(x)
     plan = ops.fft_plan(1, N, 1, BATCH, dev)
     stream = torch.cuda.current_stream(dev)
@@ -324,10 +481,26 @@ def run_ours(args) -> None:
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
 
+    # parity of the timed output (no oracle here: identities on every signal,
+    # numpy float64 FFTs of sampled signals; the oracle runs in the CPU leg)
+    lhs = y.to(torch.complex128).sum(dim=1)  # sum_k X[k] = N x[0]
+    rhs = N * x[:, 0].to(torch.complex128)
+    checksum = float(((lhs - rhs).abs() / (N * np.sqrt(N))).max().item())
+    ex = (x.abs().to(torch.float64) ** 2).sum(dim=1)
+    ey = (y.abs().to(torch.float64) ** 2).sum(dim=1) / N
+    parseval = float(((ex - ey).abs() / ex).max().item())
+    y_host = y.cpu().numpy()
+    sample_rows = [0, 1, 1777, BATCH - 1]
+    np_err = max(rel_l2(y_host[r], np.fft.fft(x_host[r].astype(np.complex128))) for r in sample_rows)
+    parity = {"tolerance_rel_l2": 1e-5 * 16, "checksum_max_err_all_signals": checksum,
+              "parseval_max_rel_all_signals": parseval, "np_fft_f64_signals": len(sample_rows),
+              "np_fft_f64_max_rel_l2": np_err}
+    del lhs, rhs, ex, ey
+
     # e2e through the public API with pinned host buffers (H2D + FFT + D2H)
     e2e_steps = max(1, min(args.steps, 3))
     host_in = torch.empty((BATCH, N), dtype=torch.complex64, pin_memory=True)
-    host_in.copy_(x.cpu())
+    host_in.copy_(torch.from_numpy(x_host))
     host_out = torch.empty_like(host_in, pin_memory=True)
     afft.fft_batch(host_in, N, out=host_out)  # warm
     torch.cuda.synchronize()
@@ -338,108 +511,202 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - e0, world)
     e2e_value = world * BATCH * FLOPS_PER_TRANSFORM * e2e_steps / e2e_s / 1e9
-
-    # secondary: C4 compression throughput (fused encode kernel, 8192^2 gray)
-    h = w = 8192
-    img = torch.randint(0, 256, (h, w), dtype=torch.uint8, device=dev, generator=gen)
-    cb = torch.randn((256, 16), dtype=torch.float32, device=dev, generator=gen)
-    cb = (cb - cb.mean(1, keepdim=True)) / cb.std(1, unbiased=False, keepdim=True)
-    nb = (h // 4) * (w // 4)
-    rec = torch.empty(nb * 3, dtype=torch.uint8, device=dev)
-    cbp = torch.empty(nb, dtype=torch.uint8, device=dev)
-    crp = torch.empty(nb, dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        ops.encode(img, 1, h, w, cb, rec, cbp, crp)
-    torch.cuda.synchronize()
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    csteps = max(3, min(args.steps, 10))
-    c0.record(stream)
-    for _ in range(csteps):
-        ops.encode(img, 1, h, w, cb, rec, cbp, crp)
-    c1.record(stream)
-    torch.cuda.synchronize()
-    c_ms = max_over_ranks(c0.elapsed_time(c1) / csteps, world)
-    comp_bytes = h * w + nb * 5
-    compression = {"metric": "compression MPixel/s", "value": round(world * h * w / (c_ms / 1e3) / 1e6, 2),
-                   "unit": "MPixel/s", "ms_per_image": round(c_ms, 4),
-                   "config": "8192x8192 gray (R=G=B), 256-entry codebook, exact VQ, bit-exact with the "
-                             "reference (configs[3])",
-                   "roofline": {"bound": "fp32", "hbm_frac": round(comp_bytes / (c_ms / 1e3) / 1e9
-                                                                    / pk["hbm_gbs"], 5),
-                                "vq_flop_per_block": 12288,
-                                # the exact search's fp32 work per second (it runs as TF32 MMAs + a
-                                # CUDA-core re-check of the ambiguous blocks)
-                                "vq_effective_tflops": round(12288 * nb / (c_ms / 1e3) / 1e12, 1),
-                                # 3xTF32 scores: 3 MMAs x 2 x 256 centroids x 16 K per block
-                                "tf32_mma_tflops": round(24576 * nb / (c_ms / 1e3) / 1e12, 1),
-                                "tf32_peak_tflops": round(pk["bf16_tflops"] / 2, 1),
-                                "tf32_frac": round(24576 * nb / (c_ms / 1e3) / 1e12 / (pk["bf16_tflops"] / 2), 4),
-                                "peak_source": pk["source"] + " (tf32 = bf16 dense / 2)"}}
-
+    del host_in, host_out
+    # ... and through the reference-shaped graph API: run() on numpy StreamFiles
+    afft.fft_batch(x_host, N)  # warm: page-locked staging slots of the full size
+    barrier(world)
+    g0 = time.perf_counter()
+    y_graph = afft.fft_batch(x_host, N)
+    g_s = max_over_ranks(time.perf_counter() - g0, world)
+    graph_ok = bool(np.array_equal(y_graph[:4], y_host[:4]))
+    del y_graph
+    e2e_graph = {"value": round(world * BATCH * FLOPS_PER_TRANSFORM / g_s / 1e9, 2), "unit": "GFLOP/s",
+                 "api": "apps.fft.fft_batch(numpy) -> run(backend, fft65536 program, StreamFile) -> numpy",
+                 "h2d_bytes_per_step": BATCH * N * 8, "d2h_bytes_per_step": BATCH * N * 8,
+                 "same_output_as_device_path": graph_ok}
     del x, y
 
-    # secondary: C5 chain on 64 x 4096^2 gray images (device-resident edges)
-    from paper_1203_4938_b200.apps import chain as achain
-    from paper_1203_4938_b200 import CudaBackend
-    nimg, side = 64, 4096
-    imgs = torch.randint(0, 256, (nimg, side, side), dtype=torch.uint8, device=dev, generator=gen)
-    cbs = torch.randn((nimg, 256, 16), dtype=torch.float32, device=dev, generator=gen)
-    # codebooks as k-means leaves them: centroids of normalised blocks (zero mean, unit deviation)
-    cbs = (cbs - cbs.mean(-1, keepdim=True)) / cbs.std(-1, unbiased=False, keepdim=True)
-    be = CudaBackend(outputs="device")
-    achain.run_chain(imgs, cbs, backend=be)
-    torch.cuda.synchronize()
-    e0c, e1c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0c.record(stream)
-    for _ in range(2):
-        achain.run_chain(imgs, cbs, backend=be)
-    e1c.record(stream)
-    torch.cuda.synchronize()
-    ms_chain = max_over_ranks(e0c.elapsed_time(e1c) / 2, world)
-    chain5 = {"metric": "chain images/s", "config": "64 x 4096^2 gray: to_complex -> fft2d -> spectrum_u8 -> "
-                                                     "imgc_encode (256 centroids/image), one graph, device edges",
-              "value": round(world * nimg / (ms_chain / 1e3), 2), "ms_per_step": round(ms_chain, 2),
-              "mpixel_s": round(world * nimg * side * side / (ms_chain / 1e3) / 1e6, 1)}
-    del imgs, cbs
+    # ------------------------------------------------------------------ C4
+    from paper_1203_4938_b200.apps.imgc import CompressedImage, synthetic_image
+    from paper_1203_4938_b200.distributed import encode_band, shard_range
+    compression = {"metric": "compression MPixel/s"}
+    try:
+        h = w = 8192
+        gold = np.load(GOLDEN / "c4_golden.npz")
+        gray = synthetic_image(w, h, seed=7)[..., 1].copy()  # SURVEY §8(d) C4 (R=G=B)
+        px = torch.from_numpy(gray).to(dev).reshape(-1)
+        cb = torch.from_numpy(gold["codebook"]).to(dev)
+        bh, bw = h // 4, w // 4
+        band = shard_range(bh, world, rank)
+        nb = (band[1] - band[0]) * bw
+        bufs = (torch.empty((nb, 3), dtype=torch.uint8, device=dev), torch.empty(nb, dtype=torch.uint8, device=dev),
+                torch.empty(nb, dtype=torch.uint8, device=dev))
+        for _ in range(3):
+            encode_band(px, 1, h, w, cb, band, bufs)
+        torch.cuda.synchronize()
+        barrier(world)
+        csteps = max(3, min(args.steps, 10))
+        c_ms = max_over_ranks(timed(lambda: encode_band(px, 1, h, w, cb, band, bufs), csteps, stream), world)
+        ties = ops.rounding_ties(px[4 * band[0] * w:4 * band[1] * w], 1, 4 * (band[1] - band[0]), w)
+        ties = (int(sum_over_ranks(ties[0], world)), int(sum_over_ranks(ties[1], world)))
+        # the bitstream: bands concatenated at fixed offsets (imgc.py:295-305)
+        mine = torch.cat([b.reshape(-1) for b in bufs])
+        if world > 1:
+            import torch.distributed as dist
+            most = (bh // world + (1 if bh % world else 0)) * bw * 5
+            pad = torch.zeros(most, dtype=torch.uint8, device=dev)
+            pad[:mine.numel()] = mine
+            parts = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(parts, pad)
+        else:
+            parts = [mine]
+        recs, cbs, crs = [], [], []
+        for r in range(world):
+            a, b = shard_range(bh, world, r)
+            k = (b - a) * bw
+            p = parts[r].cpu().numpy()
+            recs.append(p[:3 * k])
+            cbs.append(p[3 * k:4 * k])
+            crs.append(p[4 * k:5 * k])
+        rec_all, cb_all, cr_all = np.concatenate(recs).reshape(-1, 3), np.concatenate(cbs), np.concatenate(crs)
+        blob = CompressedImage.from_records(w, h, gold["codebook"], rec_all, cb_all, cr_all).to_bytes()
+        nblocks = bh * bw
+        comp_bytes = h * w + nblocks * 5
+        compression.update({
+            "value": round(h * w / (c_ms / 1e3) / 1e6, 2), "unit": "MPixel/s", "ms_per_frame": round(c_ms, 4),
+            "scaling": "strong",
+            "config": f"synthetic_image(8192, 8192, seed=7) green channel as gray (R=G=B), the 256-entry codebook "
+                      f"the reference compress() trained on it (configs[3]; tests/golden/c4_golden.npz), "
+                      f"{world} GPU(s): block-row bands of {bh // world} rows per rank",
+            "roofline": {"bound": "tensor+fp32 (exact VQ)",
+                         "hbm_frac": round(comp_bytes / world / (c_ms / 1e3) / 1e9 / pk["hbm_gbs"], 5),
+                         "vq_flop_per_block": 12288,
+                         "vq_effective_tflops": round(12288 * nblocks / world / (c_ms / 1e3) / 1e12, 1),
+                         "tf32_mma_tflops": round(24576 * nblocks / world / (c_ms / 1e3) / 1e12, 1),
+                         "tf32_peak_tflops": round(pk["bf16_tflops"] / 2, 1),
+                         "tf32_frac": round(24576 * nblocks / world / (c_ms / 1e3) / 1e12
+                                            / (pk["bf16_tflops"] / 2), 4),
+                         "peak_source": pk["source"] + " (tf32 = bf16 dense / 2)"},
+            "parity": {"bitstream_sha256": sha(blob)[:16], "reference_sha256": str(gold["blob_sha"])[:16],
+                       "bitstream_equal_reference": sha(blob) == str(gold["blob_sha"]),
+                       "rounding_ties_mean_sigma": list(ties),
+                       "reference_ties_mean_sigma": [int(gold["mean_ties"]), int(gold["sigma_ties"])],
+                       "reference_seconds_build_container": round(float(gold["seconds"]), 1)}})
+        c4_state = (gray, gold["codebook"], rec_all, cb_all, cr_all)
+        del px, bufs, parts, mine
+    except Exception as exc:  # keep the headline line alive on partial failures
+        compression["error"] = f"{type(exc).__name__}: {exc}"[:300]
+        c4_state = None
 
-    # secondary: C1 — one N=1024 signal through the graph API (numpy in/out:
-    # H2D, the fft1024 node, D2H), latency; the reference's fft() takes 8.35 ms
-    # here, mostly plan/compile
-    rng = np.random.default_rng(42)
-    x1 = (rng.standard_normal(1024) + 1j * rng.standard_normal(1024)).astype(np.complex64)
+    # ------------------------------------------------------------------ C5
+    from paper_1203_4938_b200 import CudaBackend
+    from paper_1203_4938_b200.apps import chain as achain
+    chain5 = {"metric": "chain images/s"}
+    c5_state = None
+    try:
+        import multiprocessing as mp
+        nimg, side = 64, 4096
+        lo, hi = shard_range(nimg, world, rank)
+        with mp.get_context("spawn").Pool(max(1, min(16, cores // world))) as pool:
+            imgs_np = np.stack(pool.map(_gen_image, [(side, 1000 + i) for i in range(lo, hi)]))
+        g5 = np.load(GOLDEN / "c5_golden.npz")
+        cbk = [g5["codebook_0"], g5["codebook_63"]]
+        cbs_np = np.stack([cbk[0] if i % 2 == 0 else cbk[1] for i in range(lo, hi)])
+        imgs = torch.from_numpy(imgs_np).to(dev)
+        cbs = torch.from_numpy(cbs_np).to(dev)
+        be = CudaBackend(outputs="device")
+        out = achain.run_chain(imgs, cbs, backend=be)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms_chain = max_over_ranks(timed(lambda: achain.run_chain(imgs, cbs, backend=be), 2, stream), world)
+        per_img = side * side
+        # bytes the two-pass design moves per image: u8 in, complex64 row-pass
+        # result written and read back, u8 spectrum written and read by the
+        # encoder, records + planes out (5 B per 16 px)
+        moved = per_img * (1 + 8 + 8 + 1 + 1) + per_img // 16 * 5
+        compulsory = per_img * 16 + per_img // 16 * 21  # FFT 16 B/px + compression 21 B/block
+        chain5.update({
+            "config": f"64 x synthetic_image(4096, 4096, seed=1000+i) green channel: to_complex -> fft2d -> "
+                      f"spectrum_u8 -> imgc_encode (reference-trained codebooks of images 0 and 63, alternating), "
+                      f"one graph, device-resident edges; {world} GPU(s), {hi - lo} images per rank",
+            "value": round(nimg / (ms_chain / 1e3), 2), "unit": "images/s", "ms_per_step": round(ms_chain, 2),
+            "scaling": "strong", "mpixel_s": round(nimg * per_img / (ms_chain / 1e3) / 1e6, 1),
+            "roofline": {"bound": "hbm (FFT passes) + tensor/fp32 (encoder)",
+                         "bytes_moved_per_image": moved,
+                         "achieved_gbs": round((hi - lo) * moved / (ms_chain / 1e3) / 1e9, 1),
+                         "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round((hi - lo) * moved / (ms_chain / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                         "survey_algorithmic_bytes_per_image": compulsory,
+                         "frac_of_survey_algorithmic": round((hi - lo) * compulsory / (ms_chain / 1e3) / 1e9
+                                                             / pk["hbm_gbs"], 4),
+                         "vq_effective_tflops": round(12288 * (hi - lo) * per_img / 16 / (ms_chain / 1e3) / 1e12,
+                                                      1)}})
+        if rank == 0:
+            spec0 = torch.empty(per_img, dtype=torch.uint8, device=dev)
+            ops.fft2d_u8_spectrum(imgs[0].reshape(-1), side, side, achain.ALPHA, spec0)
+            nb5 = per_img // 16
+            c5_state = (imgs_np[0], cbs_np[0], spec0.view(side, side).cpu().numpy(),
+                        {k: v.reshape(-1)[:nb5].cpu().numpy() for k, v in out.items()})
+        del imgs, cbs, out
+    except Exception as exc:
+        chain5["error"] = f"{type(exc).__name__}: {exc}"[:300]
+
+    # ------------------------------------------------------------------ C1
+    rng1 = np.random.default_rng(42)
+    x1 = (rng1.standard_normal(1024) + 1j * rng1.standard_normal(1024)).astype(np.complex64)
     for _ in range(5):
         afft.fft(x1)
     lat = []
     for _ in range(50):
         t0 = time.perf_counter()
-        afft.fft(x1)
+        y1 = afft.fft(x1)
         lat.append((time.perf_counter() - t0) * 1e3)
     lat.sort()
     c1 = {"metric": "C1 latency (ms, lower is better)", "config": "fft(x), N=1024, numpy complex64 in/out through "
                                                                    "the fft1024 graph node (configs[0])",
-          "median_ms": round(lat[len(lat) // 2], 4), "p10_ms": round(lat[len(lat) // 10], 4)}
+          "median_ms": round(lat[len(lat) // 2], 4), "p10_ms": round(lat[len(lat) // 10], 4),
+          "parity": {"np_fft_f64_rel_l2": rel_l2(y1, np.fft.fft(x1.astype(np.complex128)))}}
 
-    # secondary: C3 2-D FFT 16384^2, measured last: at P > 1 it is the only
-    # path that maps peer memory, so nothing after it depends on its context —
-    # one GPU: row pass + column-ring pass;
-    # P GPUs: row-sharded; the exchange is fused into the column pass (each rank
-    # reads its column block out of every peer's row slab over NVLink and stores
-    # the results back into the peers' slabs: natural row-sharded output, no
-    # NCCL); the NCCL all-to-all composition is the fallback
+    # ------------------------------------------------------------------ C3
+    # measured last: at P > 1 it is the only path that maps peer memory.
+    # one GPU: row pass + column-ring pass; P GPUs: row-sharded, the exchange
+    # fused into the column pass (each rank reads its column block out of
+    # every peer's row slab over NVLink and stores the results back into the
+    # peers' slabs: natural row-sharded output, no NCCL); the NCCL all-to-all
+    # composition is the fallback
     n2d = 16384
     flops2d = 5.0 * n2d * n2d * 28
     exchange = "single-GPU row + column pass"
     a2a_passes = 1
     c3_failed = False
+    nvlink = None
     try:
         rows = n2d // world
+        if world > 1 and rank == 0 and torch.cuda.device_count() > 1:
+            # NVLink peak measured here: a 1 GiB device-to-device copy to the next GPU
+            a_ = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+            b_ = torch.empty(1 << 30, dtype=torch.uint8, device=torch.device("cuda", (local + 1) % world))
+            for _ in range(2):
+                b_.copy_(a_)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(5):
+                b_.copy_(a_)
+            torch.cuda.synchronize()
+            nvlink = round(5 * (1 << 30) / (time.perf_counter() - t0) / 1e9, 1)
+            del a_, b_
+        rng3 = np.random.default_rng(43)  # SURVEY §8(d) C3 recipe, this rank's rows
         if world == 1:
-            x2 = torch.randn((rows, n2d), dtype=torch.complex64, device=dev, generator=gen)
+            x3_host = (rng3.standard_normal((n2d, n2d), dtype=np.float32)
+                       + 1j * rng3.standard_normal((n2d, n2d), dtype=np.float32)).astype(np.complex64)
+            x2 = torch.from_numpy(x3_host).to(dev)
+            y2 = torch.empty_like(x2)
 
             def step2d():
-                ops.fft2d_forward(x2, n2d, n2d, out=x2)
+                ops.fft2d_forward(x2, n2d, n2d, out=y2)
         else:
             import torch.distributed as dist
+            x3_host = None
             sh, peer_err = None, None
             try:
                 from paper_1203_4938_b200.distributed import PeerShardedFft2d
@@ -448,6 +715,7 @@ def run_ours(args) -> None:
                 peer_err = exc
             agree = torch.tensor([0 if sh is None else 1], dtype=torch.int32, device=dev)
             dist.all_reduce(agree, op=dist.ReduceOp.MIN)  # every rank takes the same path
+            gen = torch.Generator(device=dev).manual_seed(43 + rank)
             if int(agree.item()) == 1:
                 sh.slab.copy_(torch.randn((1, rows, n2d), dtype=torch.complex64, device=dev, generator=gen))
 
@@ -470,55 +738,81 @@ def run_ours(args) -> None:
             step2d()
         torch.cuda.synchronize()
         barrier(world)
-        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d0.record(stream)
-        for _ in range(3):
-            step2d()
-        d1.record(stream)
-        torch.cuda.synchronize()
-        ms2d = max_over_ranks(d0.elapsed_time(d1) / 3, world)
+        ms2d = max_over_ranks(timed(step2d, 3, stream), world)
+        c3_parity = None
+        if world == 1:
+            # two full output rows k1 of the 2-D transform, independently in
+            # float64: Y[k1, :] = fft(sum_r x[r, :] W^{r k1})
+            y3 = y2.cpu().numpy()
+            errs = []
+            xd = x3_host.astype(np.complex128)
+            for k1 in (0, 12345):
+                wv = np.exp(-2j * np.pi * ((np.arange(n2d) * k1) % n2d) / n2d)
+                errs.append(rel_l2(y3[k1], np.fft.fft(wv @ xd)))
+            del xd
+            c3_parity = {"tolerance_rel_l2": 1e-5 * 28, "np_f64_rows_checked": 2, "np_f64_max_rel_l2": max(errs),
+                         "full_size_oracle_test": "tests/test_fullsize_gpu.py::test_c3_every_row_and_column_vs_oracle"}
+            del y3
         a2a = 0 if world == 1 else a2a_passes * (world - 1) / world * 8 * n2d * n2d / world
-        step2d = x2 = sh = None  # free the 2 GiB before C5
+        step2d = x2 = y2 = sh = x3_host = None  # free the 2 GiB
         fft2d = {"metric": "2-D FFT GFLOP/s (5N^2 log2 N^2)",
                  "config": f"16384x16384 complex64, {world} GPU(s) (configs[2]), " + exchange,
-                 "value": round(flops2d / (ms2d / 1e3) / 1e9, 1), "ms": round(ms2d, 3),
+                 "value": round(flops2d / (ms2d / 1e3) / 1e9, 1), "ms": round(ms2d, 3), "scaling": "strong",
                  "roofline": {"bound": "hbm" if world == 1 else "nvlink",
                               "two_pass_bytes_per_gpu": 32 * n2d * n2d / world,
                               "frac_of_two_pass": round(32 * n2d * n2d / world / (ms2d / 1e3) / 1e9
                                                         / pk["hbm_gbs"], 4),
                               "nvlink_bytes_per_gpu": a2a,
-                              "nvlink_frac_at_770GBs": round(a2a / (ms2d / 1e3) / 770e9, 4) if a2a else None}}
+                              "nvlink_peak_gbs": nvlink,
+                              "nvlink_peak_source": "measured: 1 GiB device-to-device copy, rank 0 -> rank 1"
+                              if nvlink else None,
+                              "nvlink_frac": round(a2a / (ms2d / 1e3) / 1e9 / nvlink, 4) if (a2a and nvlink) else None},
+                 "parity": c3_parity}
     except Exception as exc:  # keep the headline line alive on partial failures
         fft2d = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         c3_failed = True
 
+    # ------------------------------------------------------------- CPU legs
+    cpu = None
+    if cpu_legs:
+        cpu = c2_cpu_leg(x_host, y_host, cores, seconds=10.0)
+        parity["oracle_signals"] = cpu.pop("oracle_signals")
+        parity["oracle_max_rel_l2"] = cpu.pop("oracle_max_rel_l2")
+        try:
+            c1["cpu_baseline"] = c1_cpu_leg()
+            fft2d["cpu_baseline"] = c3_cpu_leg(cores)
+            if c4_state is not None:
+                c4 = c4_cpu_leg(c4_state[0], c4_state[1], c4_state[2], c4_state[3], c4_state[4], cores)
+                compression["parity"]["oracle_blocks_checked"] = c4.pop("oracle_blocks")
+                compression["parity"]["oracle_differing_records"] = c4.pop("oracle_differing")
+                compression["cpu_baseline"] = c4
+            if c5_state is not None:
+                c5 = c5_cpu_leg(*c5_state)
+                chain5["parity"] = c5.pop("parity")
+                chain5["cpu_baseline"] = c5
+        except Exception as exc:  # keep the headline line alive
+            compression.setdefault("cpu_baseline", {"error": f"{type(exc).__name__}: {exc}"[:200]})
+    del x_host, y_host
+
     if rank == 0:
-        cpu = cpu_baseline(len(os.sched_getaffinity(0)), seconds=10.0) if world == 1 and not args.no_cpu \
-            else None
-        if cpu is not None:
-            try:
-                sec = secondary_cpu_baselines(len(os.sched_getaffinity(0)))
-                c1["cpu_baseline"] = sec["c1"]
-                fft2d["cpu_baseline"] = sec["c3"]
-                compression["cpu_baseline"] = sec["c4"]
-            except Exception as exc:  # keep the headline line alive
-                compression["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": N, "batch": BATCH, "parallelism": f"batch-shard x{world}",
+            "config": {"workload": workload(world), "n": N, "batch": BATCH, "parallelism": f"batch-shard x{world}",
                        "l2": "inputs 2 GiB > L2, no flush", "kernel": plan.description},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
                          "traffic": traffic, "peak_source": pk["source"],
                          "algorithmic_bytes_per_launch": BATCH * BYTES_PER_TRANSFORM,
                          "avg_launch_ms": round(avg_kernel_ms, 4)},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 2), "unit": "GFLOP/s",
                     "h2d_bytes_per_step": BATCH * N * 8, "d2h_bytes_per_step": BATCH * N * 8,
                     "api": "apps.fft.fft_batch(pinned host tensor)"},
+            "e2e_graph": e2e_graph,
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
             "secondary": {"c1_latency": c1, "compression_c4": compression, "fft2d_c3": fft2d, "chain_c5": chain5},
@@ -537,8 +831,10 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

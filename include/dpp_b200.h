@@ -226,6 +226,15 @@ int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_
                          int64_t row_stride, int64_t image_stride, int64_t batch, double sigma_min,
                          double* norm64, float* block_grad, void* stream);
 
+/* Parity report of the codec's two binary64 quantisers (imgc.py:398-401,
+ * SURVEY §8(d) C4): adds to ties[0] the number of blocks whose mean, and to
+ * ties[1] the number whose sigma / 0.25, lies within 1e-9 of a half-integer
+ * (the values where rint() depends on the last bits).  Same statistics code
+ * as the encoder; ties is a device array of two counters. */
+int dpp_imgc_rounding_ties(const uint8_t* px, int channels, int64_t height, int64_t width,
+                           int64_t row_stride, int64_t image_stride, int64_t batch,
+                           unsigned long long* ties, void* stream);
+
 /* k-means codebook trainer (imgc.py:221-273) on device: k-means++ seeding
  * from the caller's RNG stream (index of the first pick and a HOST array of
  * k-1 uniforms in [0,1), as numpy's Generator.choice consumes them), then

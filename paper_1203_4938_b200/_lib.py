@@ -44,6 +44,7 @@ SIGNATURES = {
     "dpp_u8_to_complex": (_int, [_vp, _vp, _i64, _vp]),
     "dpp_spectrum_u8": (_int, [_vp, _vp, _i64, C.c_float, _vp]),
     "dpp_imgc_block_stats": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, C.c_double, _vp, _vp, _vp]),
+    "dpp_imgc_rounding_ties": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "dpp_kmeans": (_int, [_vp, _i64, _int, _i64, C.POINTER(C.c_double), _int, _vp,
                           C.POINTER(C.c_double), C.POINTER(_int), _vp]),
     "dpp_fft2d_u8_spectrum": (_int, [_vp, _vp, _vp, C.c_float, _vp, _i64, _vp]),

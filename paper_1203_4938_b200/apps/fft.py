@@ -292,6 +292,10 @@ def fft_batch(signals, n: int | None = None, backend: CudaBackend | None = None,
         return out
     stream, dev = _as_stream(signals, n)
     backend = _backend_for(backend, dev)
+    if not dev and backend.chunk_size is None and stream.values.nbytes > _PIPE_CHUNK_BYTES:
+        # large host batches: whole signals per chunk, so the engine pipelines
+        # H2D / transform / D2H over max_in_flight device slots (client.run)
+        backend = replace(backend, chunk_size=max(1, _PIPE_CHUNK_BYTES // (8 * n)) * n)
     out = run(backend, fft_program(n), {"0.x": stream})["0.y"]
     return _unstream(out, shape, isinstance(out, DeviceStream))
 

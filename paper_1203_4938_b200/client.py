@@ -112,8 +112,21 @@ def run(backend: CudaBackend | None, program, inputs: dict) -> dict:
             arrays[name] = to_device(arrays[name], dev)
     stream = backend.stream
     with torch.cuda.device(dev):
-        run_stream(p, chunk_arrays(p, arrays), writer=collect, workers=backend.parallelism,
-                   pool=backend.pool, stream=stream)
+        cur = torch.cuda.current_stream(dev)
+        if stream is not None:
+            # inputs were staged on the current stream; the caller's stream runs
+            # the nodes (and owns their output allocations), then hands back
+            stream.wait_stream(cur)
+            with torch.cuda.stream(stream):
+                run_stream(p, chunk_arrays(p, arrays), writer=collect, workers=backend.parallelism,
+                           pool=backend.pool, stream=stream)
+            cur.wait_stream(stream)
+            for bufs in parts.values():
+                for b in bufs:
+                    b.record_stream(cur)
+        else:
+            run_stream(p, chunk_arrays(p, arrays), writer=collect, workers=backend.parallelism,
+                       pool=backend.pool, stream=stream)
         out = {}
         for fp in p.free_outputs:
             bufs = parts[fp.stream]

@@ -229,6 +229,70 @@ __device__ __forceinline__ void load_rgb(const uint8_t* row, int64_t x, float& r
   }
 }
 
+// Binary64 block mean and standard deviation exactly as numpy computes
+// blocks.mean(axis=1) / blocks.std(axis=1) (imgc.py:384-386): pairwise-8
+// sums, x / 16 (== x * 0.0625, a power of two: the same rounding); on return
+// bd[i] = y_i - mean, the centred block.
+__device__ __forceinline__ void block_moments(const float (&yv)[16], double (&bd)[16], double& mean, double& sd) {
+  double sq[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) bd[i] = (double)yv[i];
+  mean = __dmul_rn(pw16d(bd), 0.0625);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    bd[i] = __dsub_rn(bd[i], mean);
+    sq[i] = __dmul_rn(bd[i], bd[i]);
+  }
+  sd = __dsqrt_rn(__dmul_rn(pw16d(sq), 0.0625));
+}
+
+// a / b correctly rounded in binary64 from one shared reciprocal (Markstein's
+// theorem): with y = RN(1/b) and q = RN(a*y) — within one ulp of a/b — the
+// residual r = a - b*q is exact under FMA and RN(q + r*y) = RN(a/b).  The 16
+// divisions of a block by the same deviation then cost 3 DFMA each instead of
+// a full __ddiv_rn (reciprocal iteration, scaling checks and a slow path).
+__device__ __forceinline__ double div_rn_rcp(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, y, q);
+}
+
+// Rounding-tie exceptions of the two binary64 quantisers:
+// a value whose fractional part is within 1e-9 of one half is where a
+// different rounding rule or a last-bit difference in the statistics could
+// change rint(); counted so parity reports can state them.
+__device__ __forceinline__ bool near_half(double x) { return fabs(__dsub_rn(x, floor(x)) - 0.5) < 1e-9; }
+
+template <int CH>
+__global__ void __launch_bounds__(256) ties_kernel(const EncodeArgs a, unsigned long long* ties) {
+  const int64_t img = blockIdx.y;
+  const int64_t bw = a.width / 4, nblocks = bw * (a.height / 4);
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool tm = false, ts = false;
+  if (k < nblocks) {
+    const int64_t by = k / bw, bx = k - by * bw;
+    const uint8_t* base = a.px + img * a.image_stride;
+    float yv[16];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float R, G, B;
+        load_rgb<CH>(base + (4 * by + r) * a.row_stride, 4 * bx + c, R, G, B);
+        yv[4 * r + c] = luma(R, G, B);
+      }
+    double bd[16], mean, sd;
+    block_moments(yv, bd, mean, sd);
+    tm = near_half(mean);
+    ts = near_half(__dmul_rn(sd, 4.0));
+  }
+  const unsigned cm = __popc(__ballot_sync(0xffffffffu, tm)), cs = __popc(__ballot_sync(0xffffffffu, ts));
+  if ((threadIdx.x & 31) == 0) {
+    if (cm) atomicAdd(ties, (unsigned long long)cm);
+    if (cs) atomicAdd(ties + 1, (unsigned long long)cs);
+  }
+}
+
 // STATS = true: the k-means training pass — only block_grad and the binary64
 // normalised blocks (imgc.py:378-388), no chroma, VQ or records.
 // Forward block transform of block k of image img (imgc.py:358-401 steps 1-4
@@ -303,26 +367,19 @@ __device__ __forceinline__ bool block_front(const EncodeArgs& a, int64_t img, in
     }
 
     // block statistics in binary64 (imgc.py:384-388)
-    double bd[16], sq[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) bd[i] = (double)yv[i];
-    mean = __ddiv_rn(pw16d(bd), 16.0);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      bd[i] = __dsub_rn(bd[i], mean);
-      sq[i] = __dmul_rn(bd[i], bd[i]);
-    }
-    sd = __dsqrt_rn(__ddiv_rn(pw16d(sq), 16.0));
+    double bd[16];
+    block_moments(yv, bd, mean, sd);
     const double safe = fmax(sd, a.sigma_min);  // np.maximum(sigmas, sigma_min)
+    const double rsafe = __drcp_rn(safe);
     if constexpr (STATS) {
       // training rows for the k-means trainer: normalised blocks in binary64
       double* dst = a.norm64 + (img * nblocks + k) * 16;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) dst[i] = __ddiv_rn(bd[i], safe);
+      for (int i = 0; i < 16; ++i) dst[i] = div_rn_rcp(bd[i], safe, rsafe);
       return false;
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) nb[i] = __double2float_rn(__ddiv_rn(bd[i], safe));
+    for (int i = 0; i < 16; ++i) nb[i] = __double2float_rn(div_rn_rcp(bd[i], safe, rsafe));
     if (a.norm32) {
       float4* dst = reinterpret_cast<float4*>(a.norm32 + (img * nblocks + k) * 16);
 #pragma unroll
@@ -376,14 +433,19 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
 // The exact search costs 31 binary32 ops per (block, centroid).  Here a
 // 128-block tile is multiplied against the whole 256-entry codebook on the
 // 5th-gen tensor cores (3xTF32 split: n_hi.c_hi + n_hi.c_lo + n_lo.c_hi,
-// fp32 accumulation in TMEM), giving approximate scores
-//   s_j = |c_j|^2 - 2 n.c_j  =  D_j - |n|^2  (+- DELTA)
-// One epilogue pass (tcgen05.ld, 6 ops per score) finds the best and second
-// best.  When the runner-up is more than 2*DELTA away, the approximate
-// argmin IS the reference's index; otherwise the block is re-checked with
-// the reference's exact binary32 distance over every centroid whose score is
-// within 2*DELTA of the best, in index order with strict <, so ties resolve
-// to the first index exactly like vq_program (imgc.py:175-178).
+// fp32 accumulation in TMEM), plus one bias MMA (a constant A column against
+// the per-centroid |c_j|^2/2 + 8), so TMEM holds
+//   v_j = |c_j|^2/2 + 8 - n.c_j  =  (D_j - |n|^2)/2 + 8  (+- DELTA/2)
+// which is >= D_j/2 >= 0 for every normalised block (|n|^2 <= 16): the fp32
+// bit patterns order like the values, so the epilogue works on integer KEYS
+// — the bits with the centroid index in the low byte — and keeps the best and
+// runner-up with a min/max tournament (2.5 integer min/max per score, 3-input
+// VIMNMX3) instead of compare-and-select chains.
+// When the runner-up is more than 2*DELTA (+ the key quantum) away, the
+// approximate argmin IS the reference's index; otherwise the block is
+// re-checked with the reference's exact binary32 distance over every centroid
+// whose score is within the band, in index order with strict <, so ties
+// resolve to the first index exactly like vq_program (imgc.py:175-178).
 // DELTA bounds |s_j - (D^fp32_j - |n|^2)|: 3xTF32 truncation (3*2^-20 per
 // product), fp32 accumulation of 48 products, the fp32 norm, and the
 // reference's own rounding of D (<= 7u*D); see DESIGN.md.  It is scaled by
@@ -391,34 +453,32 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
 namespace tc {
 constexpr int M = 128;      // blocks per tile (TMEM lanes)
 constexpr int NCB = 256;    // centroids (padded; TMEM columns)
-// DPP_TC_SPLIT=1 (measured slower: 0.667 vs 0.54 ms per 8192^2 frame, the
-// helpers idle through the binary64 statistics and 3 CTAs/SM overlap less):
-// 256 threads per CTA — warps 4-7 take the second half of
-// every 128-column score pass (the epilogue is the kernel's largest cost),
-// 3 CTAs per SM (24 warps) instead of 4 x 128 threads (16 warps)
-#ifndef DPP_TC_SPLIT
-#define DPP_TC_SPLIT 0
-#endif
-constexpr int THREADS = DPP_TC_SPLIT ? 256 : 128;
-constexpr int CTAS_PER_SM = DPP_TC_SPLIT ? 3 : 4;
+constexpr int THREADS = 128;
+constexpr int CTAS_PER_SM = 4;
+constexpr float BIAS = 8.f;  // >= |n|^2 / 2 for every normalised block
 // K-major canonical layout, no swizzle: 8-row groups of 8 K-quarters (4 tf32)
 __device__ __forceinline__ uint32_t off(int row, int k) {
   return (uint32_t)((row >> 3) * 1024 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+// shared-memory matrix descriptor: lbo = byte offset of the next K-quarter,
+// sbo = byte offset of the next 8-row group (0: every group reads the same rows)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo = 128, uint32_t sbo = 1024) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)(128u >> 4) << 16;    // leading byte offset: next K-quarter
-  d |= (uint64_t)(1024u >> 4) << 32;   // stride byte offset: next 8-row group
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
   return d;                            // base offset 0, layout SWIZZLE_NONE
 }
-// kind::tf32, fp32 accumulate, A/B K-major, N = 256, M = 128
+// kind::tf32, fp32 accumulate, A/B K-major, N = 128, M = 128
 constexpr int NH = 128;     // centroids per MMA pass = TMEM columns allocated
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) |
                            ((uint32_t)(M >> 4) << 24);
 constexpr size_t A_BYTES = M * 32 * 4, B_BYTES = NCB * 32 * 4;
-// 49 KB -> 4 CTAs per SM, and 4 x 128 TMEM columns = the whole 512
-constexpr size_t SMEM = A_BYTES + B_BYTES + NCB * sizeof(float);
+constexpr size_t CN_OFF = A_BYTES + B_BYTES;            // |c_j|^2 (fp32), the re-check filter
+constexpr size_t ABIAS_OFF = CN_OFF + NCB * 4;          // 8 rows x [1 1 0 0 | 0 0 0 0]
+constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;           // per centroid [hi lo 0 0] of |c|^2/2 + 8
+// 53.3 KB -> 4 CTAs per SM, and 4 x 128 TMEM columns = the whole 512
+constexpr size_t SMEM = BBIAS_OFF + NCB * 16;
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
@@ -443,33 +503,36 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// keys: the score bits with centroid index j in the low byte — non-negative
+// fp32 values order like their bit patterns, so an integer min picks the
+// smallest score (to within the low byte) and carries its index along
+__device__ __forceinline__ float key_value(int k) { return __int_as_float(k & (int)0xFFFFFF00u); }
+// best (m1) and runner-up (m2) keys after two more candidates x, y:
+// the second smallest of {m1, m2, x, y} is min(m2, max(m1, min(x, y)), max(x, y))
+__device__ __forceinline__ void top2(int& m1, int& m2, int x, int y) {
+  const int lo = min(x, y), hi = max(x, y);
+  m2 = __vimin3_s32(m2, max(m1, lo), hi);
+  m1 = min(m1, lo);
+}
 }  // namespace tc
 
 template <int CH>
-#if DPP_TC_SPLIT
-#define DPP_TC_BOUNDS __launch_bounds__(tc::THREADS, tc::CTAS_PER_SM)
-#else
-#define DPP_TC_BOUNDS __launch_bounds__(tc::THREADS)
-#endif
-__global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch, float delta_scale,
-                                                               unsigned long long* ambiguous) {
+__global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs a, int64_t batch,
+                                                                float delta_scale, unsigned long long* ambiguous) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   uint8_t* sA = tsm;
   uint8_t* sB = tsm + tc::A_BYTES;
-  float* scn = reinterpret_cast<float*>(sB + tc::B_BYTES);  // |c_j|^2
+  float* scn = reinterpret_cast<float*>(tsm + tc::CN_OFF);  // |c_j|^2
   __shared__ uint8_t srec[tc::M * 3];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
-  __shared__ float h_m1[tc::M], h_m2[tc::M];  // DPP_TC_SPLIT: the helper half's best / runner-up ...
-  __shared__ int h_i1[tc::M];                 // ... and best index per block
   const int tid = threadIdx.x, warp = tid >> 5;
-  const bool primary = !DPP_TC_SPLIT || tid < tc::M;  // one block (A row, TMEM lane) per primary thread
-  const int row = DPP_TC_SPLIT ? (tid & (tc::M - 1)) : tid;
-  // Each CTA owns a contiguous range of the flat (image, tile) space, so the
-  // grid is one balanced wave for any batch; the codebook (B operand, norms,
-  // band) is restaged only when the range crosses into the next image.
+  const int row = tid;  // one block (A row, TMEM lane) per thread
+  // Each CTA strides over the flat (image, tile) space (neighbouring CTAs on
+  // neighbouring tiles); the codebook (B operand, norms, band) is restaged
+  // only when the stride crosses into the next image.
   auto stage_codebook = [&](int64_t img) {
     const float* cbk = a.codebook + img * a.codebook_stride;
     for (int e = tid; e < tc::NCB * 16; e += tc::THREADS) {
@@ -483,12 +546,21 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
       cmax_bits = 0;
       zero_key = ~0ull;
     }
+    if (tid < 64) {  // bias A operand: rows [1 1 0 0 | 0 0 0 0] (one 8-row group, sbo = 0)
+      reinterpret_cast<float*>(tsm + tc::ABIAS_OFF)[tid] = (tid < 32 && (tid & 3) < 2) ? 1.f : 0.f;
+    }
     __syncthreads();
     for (int j = tid; j < tc::NCB; j += tc::THREADS) {
       float s = 0.f;
       if (j < a.ncb)
         for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
       scn[j] = j < a.ncb ? s : 1e30f;
+      // bias B operand: |c_j|^2/2 + 8 as tf32 hi + exact remainder (padding
+      // centroids get a huge score so they never win)
+      const float bv = j < a.ncb ? fmaf(0.5f, s, tc::BIAS) : 1e30f;
+      const float bh = __uint_as_float(__float_as_uint(bv) & 0xFFFFE000u);
+      *reinterpret_cast<float4*>(tsm + tc::BBIAS_OFF + (j >> 3) * 128 + (j & 7) * 16) =
+          make_float4(bh, __fsub_rn(bv, bh), 0.f, 0.f);
       if (j < a.ncb) {
         atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
         // a constant block normalises to exactly 0: its index is the exact
@@ -508,19 +580,8 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
   const int64_t nblocks = (a.width / 4) * (a.height / 4);
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
   const int64_t all_tiles = ntiles * batch;
-#ifndef DPP_TC_CONTIG
-#define DPP_TC_CONTIG 0
-#endif
-  // DPP_TC_CONTIG: each CTA a contiguous range of the flat tile space (one
-  // codebook stage per image boundary); default: grid-stride over the flat
-  // space (neighbouring CTAs on neighbouring tiles, codebook restaged when a
-  // CTA's stride crosses into the next image)
-  const int64_t t_lo = DPP_TC_CONTIG ? all_tiles * blockIdx.x / gridDim.x : blockIdx.x;
-  const int64_t t_hi = DPP_TC_CONTIG ? all_tiles * (blockIdx.x + 1) / gridDim.x : all_tiles;
-  const int64_t t_step = DPP_TC_CONTIG ? 1 : gridDim.x;
-  int64_t img = t_lo / ntiles;
+  int64_t img = blockIdx.x / ntiles;
   stage_codebook(img);
-
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base_s)));
@@ -535,7 +596,7 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
-  const uint32_t taddr = tmem + ((uint32_t)((DPP_TC_SPLIT ? (warp & 3) : warp) * 32) << 16);  // warp w reads lanes 32 (w % 4)..
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);  // warp w reads TMEM lanes 32w..32w+31
   // band half-width: 1.5e-3 at |c| <= 4 (the normalised-block scale), growing
   // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
   auto band = [&]() {
@@ -546,7 +607,7 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
 
   uint32_t phase = 0;
   unsigned long long namb = 0;
-  for (int64_t ft = t_lo; ft < t_hi; ft += t_step) {
+  for (int64_t ft = blockIdx.x; ft < all_tiles; ft += gridDim.x) {
     if (ft / ntiles != img) {  // next image: its codebook (the previous MMAs have completed)
       img = ft / ntiles;
       __syncthreads();
@@ -557,7 +618,7 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
     }
     const int64_t t = ft - img * ntiles;
     const int64_t k = t * tc::M + row;
-    const bool active = primary && k < nblocks;
+    const bool active = k < nblocks;
     float nb[16];
     double mean = 0.0, sd = 0.0;
     if (active) {
@@ -566,26 +627,24 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
 #pragma unroll
       for (int i = 0; i < 16; ++i) nb[i] = 0.f;
     }
-    // A row: n_hi (K 0..15) and the exact remainder n_lo (K 16..31)
+    // A row: -n_hi (K 0..15) and the exact remainder -n_lo (K 16..31)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      if (!primary) break;
       float4 hi, lo;
       float* h = &hi.x;
       float* l = &lo.x;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        h[e] = __uint_as_float(__float_as_uint(nb[4 * q + e]) & 0xFFFFE000u);
-        l[e] = __fsub_rn(nb[4 * q + e], h[e]);
+        const float v = -nb[4 * q + e];
+        h[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        l[e] = __fsub_rn(v, h[e]);
       }
       *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
       *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
     }
-    // two MMA passes of 128 centroids each through the same 128 TMEM columns;
-    // pass 1 keeps the best and runner-up approximate score
-    float m1 = 3.0e38f, m2 = 3.0e38f;
-    int i1 = 0;
-#pragma unroll 1
+    // two MMA passes of 128 centroids each through the same 128 TMEM columns
+    int m1 = 0x7fffffff, m2 = 0x7fffffff;
+#pragma unroll
     for (int h = 0; h < tc::NCB / tc::NH; ++h) {
       fence_proxy_async_smem();
       tc::fence_before();
@@ -598,59 +657,38 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
 #pragma unroll
         for (int m = 0; m < 6; ++m)
           tc::mma_tf32(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
+        // + |c_j|^2/2 + 8: A = [1 1 0 0 | 0...] in every row, B = [hi lo . . | same quarter again]
+        tc::mma_tf32(tmem, tc::sdesc(smem_u32(tsm + tc::ABIAS_OFF), 128, 0),
+                     tc::sdesc(smem_u32(tsm + tc::BBIAS_OFF) + h * (tc::NH / 8) * 128, 0, 128), 1u);
         tc::commit(&bar);
       }
       mbar_wait(&bar, phase);
       phase ^= 1;
       tc::fence_after();
-      constexpr int CHUNKS = DPP_TC_SPLIT ? tc::NH / 64 : tc::NH / 32;
-#pragma unroll 1
-      for (int cq = 0; cq < CHUNKS; ++cq) {
-        const int ch = (DPP_TC_SPLIT && !primary) ? CHUNKS + cq : cq;
+#pragma unroll
+      for (int cq = 0; cq < tc::NH / 32; ++cq) {
         uint32_t r[32];
-        tc::ld32(taddr + ch * 32, r);
-        const int j0 = h * tc::NH + ch * 32;
-        const float4* cn4 = reinterpret_cast<const float4*>(scn + j0);
+        tc::ld32(taddr + cq * 32, r);
+        const int j0 = h * tc::NH + cq * 32;
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 cn = cn4[c4];
-          const float cv[4] = {cn.x, cn.y, cn.z, cn.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float s = fmaf(-2.f, __uint_as_float(r[4 * c4 + e]), cv[e]);
-            const bool p = s < m1;
-            m2 = p ? m1 : fminf(m2, s);
-            i1 = p ? j0 + 4 * c4 + e : i1;
-            m1 = p ? s : m1;
-          }
+        for (int e = 0; e < 32; e += 4) {
+          // four indices packed in one register; PRMT puts byte q of it into
+          // the low byte of the score bits: one instruction per key
+          const uint32_t jq = (uint32_t)(j0 + e) | (uint32_t)(j0 + e + 1) << 8 | (uint32_t)(j0 + e + 2) << 16 |
+                              (uint32_t)(j0 + e + 3) << 24;
+          tc::top2(m1, m2, (int)__byte_perm(r[e], jq, 0x3214), (int)__byte_perm(r[e + 1], jq, 0x3215));
+          tc::top2(m1, m2, (int)__byte_perm(r[e + 2], jq, 0x3216), (int)__byte_perm(r[e + 3], jq, 0x3217));
         }
       }
     }
-    if (DPP_TC_SPLIT) {
-      // the two halves of each pass: best of both, runner-up = the better of
-      // the other half's best and the two runners-up (exact ties give m2 == m1:
-      // ambiguous, settled by the exact re-check)
-      if (!primary) {
-        h_m1[row] = m1;
-        h_m2[row] = m2;
-        h_i1[row] = i1;
-      }
-      __syncthreads();
-      if (primary) {
-        const float bm1 = h_m1[row], bm2 = h_m2[row];
-        const int bi1 = h_i1[row];
-        const float nm2 = fminf(fmaxf(m1, bm1), fminf(m2, bm2));
-        if (bm1 < m1) {
-          m1 = bm1;
-          i1 = bi1;
-        }
-        m2 = nm2;
-      }
-    }
+    const int i1 = m1 & 0xFF;
+    const float v1 = tc::key_value(m1), v2 = tc::key_value(m2);
+    // keys drop the low byte: the true best lies in [v1, v1 + quantum)
+    const float quant = __int_as_float((m2 & 0x7F800000) | 0) * 0x1p-15f;  // 2^8 ulps of the runner-up
     bool zero = active;
 #pragma unroll
     for (int e = 0; e < 16; ++e) zero = zero && nb[e] == 0.f;
-    const bool amb = active && !zero && !(m2 - m1 > delta2);
+    const bool amb = active && !zero && !(v2 - v1 > 0.5f * delta2 + quant);
     int bj = zero ? (zero_key == ~0ull ? 0 : (int)(zero_key & 0xffffffffu)) : i1;
     unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
     // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block at
@@ -665,7 +703,8 @@ __global__ void DPP_TC_BOUNDS encode_tc_kernel(const EncodeArgs a, int64_t batch
       float nv[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) nv[i] = __shfl_sync(0xffffffffu, nb[i], src);
-      const float lim = __shfl_sync(0xffffffffu, m1 + delta2, src);
+      // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8)
+      const float lim = __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
       float2 bp[8];
       vq_pack(nv, bp);
       float best = VQ_BEST_INIT;
@@ -925,6 +964,30 @@ int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_
     default: dpp::encode_kernel<4, true><<<grid, 256, 0, s>>>(a); break;
   }
   DPP_LAUNCH_CHECK("encode_kernel<stats>");
+  return DPP_OK;
+}
+
+int dpp_imgc_rounding_ties(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
+                           int64_t image_stride, int64_t batch, unsigned long long* ties, void* stream) {
+  if (height % 4 || width % 4 || height < 4 || width < 4)
+    return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
+                     (long long)height);
+  if (channels != 1 && channels != 3 && channels != 4)
+    return dpp::fail(DPP_EINVAL, "channels must be 1, 3 or 4, got %d", channels);
+  if (!ties) return dpp::fail(DPP_EINVAL, "ties is required");
+  if (batch < 0 || batch > 65535) return dpp::fail(DPP_EINVAL, "batch must be in 0..65535");
+  if (batch == 0) return DPP_OK;
+  dpp::EncodeArgs a{px, height, width, row_stride, image_stride, nullptr, 0, 0, 0.25,
+                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  const int64_t nblocks = (height / 4) * (width / 4);
+  dim3 grid(dpp::grid1(nblocks, 256), (unsigned)batch);
+  auto s = (cudaStream_t)stream;
+  switch (channels) {
+    case 1: dpp::ties_kernel<1><<<grid, 256, 0, s>>>(a, ties); break;
+    case 3: dpp::ties_kernel<3><<<grid, 256, 0, s>>>(a, ties); break;
+    default: dpp::ties_kernel<4><<<grid, 256, 0, s>>>(a, ties); break;
+  }
+  DPP_LAUNCH_CHECK("ties_kernel");
   return DPP_OK;
 }
 

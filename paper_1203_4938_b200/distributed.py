@@ -9,6 +9,11 @@
   peer pointers) and, for natural-order output, TMA-stores the results straight
   back into the peers' slabs.  No NCCL and no staging copies on the data path;
   two stream-ordered flag barriers per call.
+* ``compress_tile_sharded`` (C4): one frame's block rows split
+  into P contiguous bands; each rank encodes its band (records, Cb and Cr rows
+  are block-local, so a band is an independent sub-image) and the bitstream is
+  the concatenation of the bands at fixed offsets (imgc.py:295-305) — one
+  all-gather of the finished bytes, no data-path collective.
 * ``fft2d_row_sharded`` (C3, the NCCL baseline): a 2-D transform whose rows are
   split contiguously over P ranks.  Row FFTs run locally; ONE all-to-all
   turns each rank's row slab into a column slab (the send buffer is packed
@@ -30,7 +35,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "fft2d_row_sharded", "pack_column_blocks", "unpack_column_blocks",
-           "PeerShardedFft2d"]
+           "PeerShardedFft2d", "encode_band", "compress_tile_sharded"]
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -234,3 +239,79 @@ class PeerShardedFft2d:
             self.close()
         except Exception:  # interpreter shutdown
             pass
+
+
+def encode_band(px: torch.Tensor, channels: int, height: int, width: int, codebook: torch.Tensor,
+                band: tuple[int, int], out: tuple | None = None, stream=None):
+    """Encode block rows [lo, hi) of one (height, width) frame on this GPU.
+
+    px: the frame's pixels (height * width * channels uint8, CUDA); the band is
+    a view (row offset 4*lo), so nothing is copied.  Returns (records
+    (blocks, 3), cb (blocks,), cr (blocks,)) of the band: exactly the byte
+    ranges [3*lo*bw, 3*hi*bw) and [lo*bw, hi*bw) of the single-GPU outputs."""
+    from . import ops
+    lo, hi = band
+    bw = width // 4
+    nb = (hi - lo) * bw
+    rows = px.reshape(height, width * channels)[4 * lo:4 * hi]
+    rec, cbp, crp = out if out is not None else (
+        torch.empty((nb, 3), dtype=torch.uint8, device=px.device),
+        torch.empty(nb, dtype=torch.uint8, device=px.device),
+        torch.empty(nb, dtype=torch.uint8, device=px.device))
+    if nb:
+        ops.encode(rows, channels, 4 * (hi - lo), width, codebook, rec, cbp, crp, stream=stream)
+    return rec, cbp, crp
+
+
+def compress_tile_sharded(image, codebook, *, group=None, device=None, encode: Callable | None = None):
+    """C4 across the ranks of ``group``: every rank passes the same frame
+    ((h, w) gray or (h, w, 3|4) uint8, numpy or CUDA) and codebook; rank r
+    encodes block rows shard_range(h/4, P, r) and the finished band bytes are
+    all-gathered.  Returns the ``CompressedImage`` on every rank.
+
+    ``encode(px, channels, h, w, codebook, band)`` defaults to the sm_100a
+    encoder (``encode_band``); the gloo choreography tests inject a stand-in."""
+    import numpy as np
+
+    from .apps.imgc import CompressedImage, _validate_image
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    h, w, ch = _validate_image(image)
+    bh, bw = h // 4, w // 4
+    lo, hi = shard_range(bh, world, rank)
+    cents = codebook.centroids if hasattr(codebook, "centroids") else codebook
+    if encode is None:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        px = image.to(dev).contiguous() if isinstance(image, torch.Tensor) else \
+            torch.from_numpy(np.ascontiguousarray(image)).to(dev)
+        cb_t = torch.as_tensor(np.ascontiguousarray(cents, np.float32)).to(dev) \
+            if not isinstance(cents, torch.Tensor) else cents.to(dev, torch.float32).contiguous()
+        rec, cbp, crp = encode_band(px.reshape(-1), ch, h, w, cb_t, (lo, hi))
+        mine = torch.cat([rec.reshape(-1), cbp, crp]).cpu()
+    else:
+        rec, cbp, crp = encode(image, ch, h, w, cents, (lo, hi))
+        mine = torch.cat([torch.as_tensor(np.ascontiguousarray(x)).reshape(-1) for x in (rec, cbp, crp)])
+    # bands differ by at most one block row: pad to the largest, gather, trim
+    most = (bh // world + (1 if bh % world else 0)) * bw * 5
+    buf = torch.zeros(most, dtype=torch.uint8)
+    buf[:mine.numel()] = mine
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    if world > 1:
+        on_gpu = dist.get_backend(group) == "nccl"  # NCCL gathers device buffers, gloo host ones
+        gbuf = buf.to(torch.device("cuda", torch.cuda.current_device())) if on_gpu else buf
+        gparts = [torch.empty_like(gbuf) for _ in range(world)]
+        dist.all_gather(gparts, gbuf, group=group)
+        parts = [p.cpu() for p in gparts]
+    else:
+        parts = [buf]
+    recs, cbs, crs = [], [], []
+    for r in range(world):
+        a, b = shard_range(bh, world, r)
+        nb = (b - a) * bw
+        p = parts[r].numpy()
+        recs.append(p[:3 * nb])
+        cbs.append(p[3 * nb:4 * nb])
+        crs.append(p[4 * nb:5 * nb])
+    return CompressedImage.from_records(w, h, np.asarray(cents.cpu() if isinstance(cents, torch.Tensor) else cents,
+                                                         np.float32),
+                                        np.concatenate(recs), np.concatenate(cbs), np.concatenate(crs))

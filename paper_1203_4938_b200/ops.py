@@ -216,6 +216,25 @@ def encode(px: torch.Tensor, channels: int, height: int, width: int, codebook: t
         _lib.ptr(norm32), stream_handle(stream)), "imgc encode")
 
 
+def rounding_ties(px: torch.Tensor, channels: int, height: int, width: int, batch: int = 1,
+                  stream=None) -> tuple[int, int]:
+    """(mean, sigma) rounding-tie counts of the encoder's binary64 quantisers.
+
+    A tie is a block whose mean (or sigma / 0.25) lies within 1e-9 of a
+    half-integer, where rint() (imgc.py:398-401) depends on the last bits; the
+    encoder reproduces those bits exactly, so ties are reported, not errors."""
+    _check_cuda(px, "px", torch.uint8)
+    image_bytes = height * width * channels
+    if px.numel() < batch * image_bytes:
+        raise PlanError(f"pixel buffer holds {px.numel()} bytes, need {batch * image_bytes}")
+    ties = torch.zeros(2, dtype=torch.int64, device=px.device)
+    _lib.check(_lib.load().dpp_imgc_rounding_ties(
+        px.data_ptr(), channels, height, width, width * channels, image_bytes, batch, ties.data_ptr(),
+        stream_handle(stream)), "imgc rounding ties")
+    m, s = ties.tolist()
+    return int(m), int(s)
+
+
 def u8_to_complex(x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
     _check_cuda(x, "x", torch.uint8)
     _check_cuda(y, "y")
