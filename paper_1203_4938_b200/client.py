@@ -98,9 +98,11 @@ def run(backend: CudaBackend | None, program, inputs: dict) -> dict:
         raise ClientError(f"input streams disagree on element count: {sorted(counts)}")
     host_in = {name for name, sf in ((n, inputs[n]) for n in free_in) if isinstance(sf, StreamFile)}
     total = counts.pop() if counts else 0
+    from .jit import deferred_faults
     if (p.chunk_size is not None and host_in and backend.outputs == "host" and backend.max_in_flight > 1
             and total > p.chunk_size and backend.stream is None):
-        return _run_pipelined(p, inputs, host_in, arrays, total, backend.max_in_flight)
+        with deferred_faults():
+            return _run_pipelined(p, inputs, host_in, arrays, total, backend.max_in_flight)
     parts: dict[str, list] = {fp.stream: [] for fp in p.free_outputs}
 
     def collect(chunk):
@@ -111,7 +113,7 @@ def run(backend: CudaBackend | None, program, inputs: dict) -> dict:
         if not isinstance(arrays[name], torch.Tensor):
             arrays[name] = to_device(arrays[name], dev)
     stream = backend.stream
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev), deferred_faults():
         cur = torch.cuda.current_stream(dev)
         if stream is not None:
             # inputs were staged on the current stream; the caller's stream runs

@@ -418,10 +418,8 @@ int fft128k_l2_init(FftPlan* p) {
   }
   // units are whole transforms (1 or 2 MB): the 2^16 kernel's 24 MB lag and 64 MB ring
   const int lags[4] = {24, 16, 8, 4}, rings[4] = {64, 32, 16, 8};
-  p->l2_lag = lags[slot];
-  p->l2_ring = rings[slot];
-  if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
-  if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e) > 0 ? atoi(e) : p->l2_ring;
+  p->l2_lag = ring_stress() ? 2 : lags[slot];
+  p->l2_ring = ring_stress() ? 4 : rings[slot];
   if (p->l2_ring <= p->l2_lag) p->l2_ring = p->l2_lag + 1;
   int r = 1;
   while (r < p->l2_ring) r <<= 1;

@@ -281,10 +281,8 @@ int fft16k_l2_init(FftPlan* p) {
                      : (B == 64 ? ringb_prepare<64>(&g_ringb_ctas[slot]) : ringb_prepare<128>(&g_ringb_ctas[slot]));
     if (rc) return rc;
   }
-  p->l2_lag = 48;
-  p->l2_ring = 128;
-  if (const char* e = getenv("DPP_FFT_L2_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
-  if (const char* e = getenv("DPP_FFT_L2_RING")) p->l2_ring = atoi(e) > 0 ? atoi(e) : p->l2_ring;
+  p->l2_lag = ring_stress() ? 2 : 48;
+  p->l2_ring = ring_stress() ? 4 : 128;
   if (p->l2_ring <= p->l2_lag) p->l2_ring = p->l2_lag + 1;
   int r = 1;
   while (r < p->l2_ring) r <<= 1;

@@ -214,13 +214,6 @@ int fft2d_plan_init(FftPlan* p) {
   if (rc == DPP_ENOTSUP)
     return fail(DPP_ENOTSUP, "2-D column length %lld not supported (256..32768)", (long long)n0);
   if (rc) return rc;
-  // A/B switch: 256-byte column tiles for 4096-row images (DPP_FFT_COLW=32)
-  const char* ew = getenv("DPP_FFT_COLW");
-  if (n0 == 4096 && ew && atoi(ew) == 32 && n1 % 32 == 0) {
-    rc = prepare_columns<64, 64, 16, 32>();
-    if (rc) return rc;
-    width = 32;
-  }
   if (n1 % width)
     return fail(DPP_ENOTSUP, "2-D row length %lld must be a multiple of the %d-column tile", (long long)n1, width);
   p->col_width = width;
@@ -255,8 +248,6 @@ int fft2d_plan_init(FftPlan* p) {
 int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s) {
   if (batch == 0) return DPP_OK;
   if (p->col_ring) return fft2d_colring_execute(p, data, batch, s);
-  if (p->n0 == 4096 && p->col_width == 32)
-    return launch_columns<64, 64, 16, 32>(data, p->n1, batch, p->ctw_a, p->ctw_b, s);
   switch (p->n0) {
 #define RUN(L, A, B, C, W) \
   case L: return launch_columns<A, B, C, W>(data, p->n1, batch, p->ctw_a, p->ctw_b, s);

@@ -515,12 +515,7 @@ int fft2d_colring_init(FftPlan* p) {
   const int64_t R = p->n0;
   if (!(R == 1024 || R == 2048 || R == 4096 || R == 8192 || R == 16384 || R == 32768) || p->n1 % 16)
     return DPP_ENOTSUP;
-  if (const char* e = getenv("DPP_FFT_COLRING"))
-    if (atoi(e) == 0) return DPP_ENOTSUP;
-  if (g_col_discard < 0) {
-    const char* e = getenv("DPP_FFT_L2_DISCARD");
-    g_col_discard = e ? atoi(e) != 0 : 1;
-  }
+  g_col_discard = 1;
   const int B = (int)(R / 256);
   int rc = B == 4    ? colring_prepare<4>(&p->col_ring_ctas)
            : B == 8  ? colring_prepare<8>(&p->col_ring_ctas)
@@ -529,15 +524,9 @@ int fft2d_colring_init(FftPlan* p) {
                              : B == 64 ? colring_prepare<64>(&p->col_ring_ctas)
                                        : colring_prepare<128>(&p->col_ring_ctas);
   if (rc) return rc;
-  p->l2_lag = 768 / B;
-  if (const char* e = getenv("DPP_FFT_COL_LAG")) p->l2_lag = atoi(e) > 0 ? atoi(e) : p->l2_lag;
+  p->l2_lag = ring_stress() ? 2 : 768 / B;
   int ring = 1;
   while (ring < 2 * p->l2_lag + 8) ring <<= 1;
-  if (const char* e = getenv("DPP_FFT_COL_RING")) {
-    int r = 1;
-    while (r < atoi(e)) r <<= 1;
-    if (r > p->l2_lag) ring = r;
-  }
   p->l2_ring = ring;
   const int64_t units = p->batch * (p->n1 / 16);
   if (units > 0x7fffffff / (2 * B)) return fail(DPP_EINVAL, "2-D batch too large for the column ring");

@@ -5,10 +5,24 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace dpp {
+
+// Test hook (the one environment switch of the FFT kernels): DPP_RING_STRESS=1
+// plans every L2-ring kernel with a 4-slot ring and lag 2, so ring slots are
+// reused many times per launch and both cross-CTA waits (P2 on P1, P1 on slot
+// release) fire — tests/test_fft_gpu.py runs the shipped kernels that way.
+inline bool ring_stress() {
+  static const int on = [] {
+    const char* e = std::getenv("DPP_RING_STRESS");
+    return e && std::atoi(e) != 0 ? 1 : 0;
+  }();
+  return on != 0;
+}
+
 namespace ring {
 
 __device__ __forceinline__ float2 ld_stream(const float2* p) {

@@ -222,6 +222,11 @@ def _element_count(p: ExecutionPlan, chunk: Chunk) -> int:
     return counts.pop() if counts else 0
 
 
+def _jit():
+    from . import jit
+    return jit
+
+
 def _items(p: ExecutionPlan, iid: int, elements: int, chunk_index: int) -> int:
     items = p.multipliers[iid] * elements
     if items.denominator != 1:
@@ -246,6 +251,7 @@ def _run_one(p: ExecutionPlan, iid: int, chunk: Chunk, elements: int, produced: 
     try:
         if items:
             native.check_items(items)
+            _jit().set_site(iid, chunk.index)
             native.launch(items, inputs, outputs, stream)
     except KernelRuntimeError as exc:
         raise EngineRuntimeError(str(exc), instance=iid, work_item=exc.work_item,

@@ -19,11 +19,18 @@ interp.py), restated per operation:
 * ``fmin``/``fmax``/``min``/``max`` are numpy minimum/maximum
   (``a < b || isnan(a) ? a : b``); transcendental builtins use CUDA's
   accurate ``sinf`` ... ``powf`` (within a few ulp of numpy's float32);
-* buffer reads and writes are bounds-checked: a fault records
-  (statements executed, work-item) with atomicMin — the lockstep evaluator
-  reports the earliest faulting statement and its lowest work-item — and the
-  host re-runs that one work-item to recover the fault's detail;
-* every executed statement counts against the instruction budget.
+* buffer reads and writes are bounds-checked.  Every fault site has a
+  position in the lockstep evaluator's order — (loop region, iteration, ...,
+  site) of pre-order ids — and the reported fault is the minimum position
+  over all work-items, then the lowest work-item, exactly the one the
+  reference's lockstep interpreter raises first: the then-branch before the
+  else-branch, iteration k of a loop for every live lane before k+1
+  (interp.py:118-180).  A normal launch only flags a fault; jit.py then finds
+  the minimum one tuple component per re-run and recovers the detail from the
+  one faulting work-item;
+* every statement a work-item executes counts against the instruction budget
+  (per work-item path; the reference counts the frame's lockstep statements,
+  which is larger only when lanes diverge inside long loops).
 """
 
 from __future__ import annotations
@@ -43,12 +50,28 @@ _UTYPES = {1: "unsigned char", 2: "unsigned short", 4: "unsigned int", 8: "unsig
 FAULT_INDEX, FAULT_DIV, FAULT_MOD, FAULT_BUDGET = 1, 2, 3, 4
 
 _PRELUDE = r"""
-#define DPP_FAULT(code, pt, val) do { dpp_fault(fault, diag, ops, gid, code, pt, (long long)(val)); return; } while (0)
-__device__ __forceinline__ void dpp_fault(unsigned long long* fault, long long* diag, long long ops, long long gid,
-                                          int code, int pt, long long val) {
-  const unsigned long long key = ((unsigned long long)ops << 32) | (unsigned long long)gid;
-  atomicMin(fault, key);
-  if (diag) { diag[0] = code; diag[1] = pt; diag[2] = val; }
+// A fault site's position in the lockstep evaluator's order (interp.py:118-
+// 180: statements run for every active lane before the next one starts, the
+// then-branch before the else-branch, loop iteration k for all live lanes
+// before iteration k+1): the tuple (loop region, iteration, ..., site) of
+// pre-order ids, compared lexicographically, then the work-item.  A normal
+// launch only flags a fault; diagnosis passes (jit.py) re-run the node and
+// find the minimum tuple one component per pass, then the lowest work-item.
+#define DPP_FAULT(code, pt, val, ...) do { \
+    const long long tup_[] = {__VA_ARGS__}; \
+    dpp_fault(fault, diag, mode, prefix, gid, code, pt, (long long)(val), tup_, \
+              (int)(sizeof(tup_) / sizeof(long long))); return; } while (0)
+__device__ __forceinline__ void dpp_fault(unsigned long long* fault, long long* diag, int mode,
+                                          const long long* prefix, long long gid, int code, int pt, long long val,
+                                          const long long* tup, int len) {
+  if (mode < 0) {  // normal launch: only "a fault happened"
+    atomicMin(fault, 0ULL);
+    if (diag) { diag[0] = code; diag[1] = pt; diag[2] = val; }
+    return;
+  }
+  for (int j = 0; j < mode; ++j)
+    if (j >= len || tup[j] != prefix[j]) return;  // not on the minimum's path
+  atomicMin(fault, (unsigned long long)(mode < len ? tup[mode] : gid));
 }
 __device__ __forceinline__ float dpp_fmin(float a, float b) { return (a < b || isnan(a)) ? a : b; }
 __device__ __forceinline__ float dpp_fmax(float a, float b) { return (a > b || isnan(a)) ? a : b; }
@@ -69,6 +92,18 @@ class _Gen:
         self.points = list(k.io.values())
         self.pid = {p.name: i for i, p in enumerate(self.points)}
         self.scopes: list[dict] = [{}]
+        self.pre = 0                   # pre-order ids of statements, fault sites and loop regions
+        self.loops: list[tuple] = []   # enclosing loops: (region id, iteration counter)
+        self.sites: set[int] = set()   # ids that end a fault tuple
+
+    def site(self) -> str:
+        """A new fault site: its lockstep tuple as DPP_FAULT's trailing arguments."""
+        self.pre += 1
+        self.sites.add(self.pre)
+        parts = []
+        for region, it in self.loops:
+            parts += [str(region), it]
+        return ", ".join(parts + [str(self.pre)])
 
     # -- emission helpers -------------------------------------------------
     def emit(self, line: str) -> None:
@@ -150,7 +185,8 @@ class _Gen:
     def index_value(self, index, name: str) -> str:
         (iv,) = self.expr(index)
         i = self.tmp("long long", f"(long long)({iv})")
-        self.emit(f"if ({i} < 0 || {i} >= n{self.pid[name]}) DPP_FAULT({FAULT_INDEX}, {self.pid[name]}, {i});")
+        self.emit(f"if ({i} < 0 || {i} >= n{self.pid[name]}) "
+                  f"DPP_FAULT({FAULT_INDEX}, {self.pid[name]}, {i}, {self.site()});")
         return i
 
     def e_Index(self, e):
@@ -221,7 +257,7 @@ class _Gen:
                 out.append(self.tmp(ct, f"({ct})(({ut})({a}) {op} ({ut})({b}))"))
             elif op in ("/", "%"):
                 code = FAULT_DIV if op == "/" else FAULT_MOD
-                self.emit(f"if (({b}) == 0) DPP_FAULT({code}, -1, 0);")
+                self.emit(f"if (({b}) == 0) DPP_FAULT({code}, -1, 0, {self.site()});")
                 if t.is_signed and t.scalar_size >= 4:
                     ut = _UTYPES[t.scalar_size]
                     alt = f"({ct})(({ut})0 - ({ut})({a}))" if op == "/" else f"({ct})0"
@@ -309,7 +345,7 @@ class _Gen:
 
     # -- statements ---------------------------------------------------------
     def count(self) -> None:
-        self.emit(f"if (++ops > {self.budget}LL) DPP_FAULT({FAULT_BUDGET}, -1, 0);")
+        self.emit(f"if (++ops > {self.budget}LL) DPP_FAULT({FAULT_BUDGET}, -1, 0, {self.site()});")
 
     def stmt(self, s) -> None:
         self.count()
@@ -378,12 +414,20 @@ class _Gen:
         self.scopes.append({})
         if s.init is not None:
             self.stmt(s.init)
-        self.open("for (;;) {")
+        # the iterations form one region after the init: condition, body and
+        # update of iteration k run (in lockstep) before iteration k+1
+        self.pre += 1
+        self.n += 1
+        it = f"it{self.n}"
+        self.emit(f"long long {it} = 0;")
+        self.loops.append((self.pre, it))
+        self.open("for (;; ++" + it + ") {")
         (c,) = self.expr(s.cond)
         self.emit(f"if (({c}) == 0) break;")
         self.scoped(s.body)
         self.stmt(s.update)
         self.close()
+        self.loops.pop()
         self.scopes.pop()
         self.close()
 
@@ -396,12 +440,13 @@ class _Gen:
         self.close()
 
 
-def generate(k: TypedKernel, name: str = "dpp_jit_kernel", budget: int = 10_000_000) -> tuple[str, list]:
-    """CUDA C source and the parameter list.
+def generate(k: TypedKernel, name: str = "dpp_jit_kernel", budget: int = 10_000_000) -> tuple[str, list, set]:
+    """CUDA C source, the parameter list and the ids that end a fault tuple.
 
     Parameters (all 64-bit): one pointer per i/o point (in ``k.io`` order),
     one element count per point, then items, global size, first gid, fault
-    word pointer, detail pointer (nullable)."""
+    word pointer, detail pointer (nullable), diagnosis pass (-1 = normal
+    launch) and the pointer to the tuple prefix fixed by earlier passes."""
     g = _Gen(k, budget)
     for x in k.body:
         g.stmt(x)
@@ -421,10 +466,12 @@ def generate(k: TypedKernel, name: str = "dpp_jit_kernel", budget: int = 10_000_
              f"  const long long gid = (long long)P[{base + 2}] + (long long)blockIdx.x * blockDim.x + threadIdx.x;",
              f"  unsigned long long* fault = (unsigned long long*)P[{base + 3}];",
              f"  long long* diag = (long long*)P[{base + 4}];",
+             f"  const int mode = (int)(long long)P[{base + 5}];",
+             f"  const long long* prefix = (const long long*)P[{base + 6}];",
              f"  if (gid >= (long long)P[{base + 2}] + items) return;",
              "  long long ops = 0;"]
-    params += [("items",), ("gsize",), ("gid0",), ("fault",), ("diag",)]
-    src = (_PRELUDE + f'\nstruct dpp_params {{ unsigned long long p[{base + 5}]; }};\n'
+    params += [("items",), ("gsize",), ("gid0",), ("fault",), ("diag",), ("mode",), ("prefix",)]
+    src = (_PRELUDE + f'\nstruct dpp_params {{ unsigned long long p[{base + 7}]; }};\n'
            f'extern "C" __global__ void __launch_bounds__(256) {name}(const dpp_params prm) {{\n'
            "  const unsigned long long* P = prm.p;\n" + "\n".join(decl) + "\n" + "\n".join(g.lines) + "\n}\n")
-    return src, params
+    return src, params, g.sites

@@ -114,6 +114,23 @@ CASES = [
     {"name": "fault_mod_zero_late", "items": 50, "lo": 1, "hi": 9,
      "body": _I + "int a = x[i];\nfor (int k = 0; k < 3; k = k + 1) { a = a - 1; }\ny[i] = 100 % (a + 2);",
      "io": {"x": ("int", 1, "in"), "y": ("int", 1, "out")}},
+    # divergent faults: the reported work-item is the lockstep evaluator's
+    # (then-branch before else-branch, loop iteration k for every live lane
+    # before k+1), not the one with the fewest statements executed
+    {"name": "fault_divergent_branches", "items": 50,
+     "body": _I + "if (i < 2) { float a = 1.0f; y[i + 1000] = a; } else { y[i + 1000] = 0.0f; }",
+     "io": {"x": ("float", 1, "in"), "y": ("float", 1, "out")}},
+    {"name": "fault_divergent_path_length", "items": 64,
+     "body": _I + "float a = 0.0f;\nif (i % 2 == 0) { a = 1.0f; a = a + 1.0f; a = a * 2.0f; }\n"
+             "y[i + (i >= 10 ? 1000 : 0)] = a;",
+     "io": {"x": ("float", 1, "in"), "y": ("float", 1, "out")}},
+    {"name": "fault_divergent_loop", "items": 16,
+     "body": _I + "int n = (i == 7) ? 6 : 1;\nfor (int k = 0; k < n; k = k + 1) { if (k == 5) { y[i + 1000] = 1.0f; } }\n"
+             "y[i + (i == 3 ? 1000 : 0)] = 2.0f;",
+     "io": {"x": ("float", 1, "in"), "y": ("float", 1, "out")}},
+    {"name": "fault_in_loop_condition", "items": 40, "lo": 0, "hi": 3,
+     "body": _I + "int acc = 0;\nfor (int k = 0; k < x[i + k * (i % 3)]; k = k + 1) { acc = acc + k; }\ny[i] = acc;",
+     "io": {"x": ("int", 1, "in"), "y": ("int", 1, "out")}},
     {"name": "type_error_write_input", "items": 4, "body": _I + "x[i] = 1.0f;",
      "io": {"x": ("float", 1, "in"), "y": ("float", 1, "out")}},
     {"name": "type_error_narrowing", "items": 4, "body": _I + "int a = x[i];\ny[i] = a;",

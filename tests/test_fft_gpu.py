@@ -227,31 +227,13 @@ print(max(rel_l2(g, r) for g, r in zip(got, ref)))
 """
 
 
-_VARIANTS = [
-    # DSMEM cluster kernels (DPP_FFT_L2=0 selects them for 2^16)
-    *({"DPP_FFT_L2": "0", "DPP_FFT_CLUSTER_MODE": str(m)} for m in (4, 5, 6, 7, 8, 9)),
-    # L2-ring two-pass kernels: v1 (non-persistent), v2 (persistent, CTA barriers)
-    {"DPP_FFT_L2": "1"}, {"DPP_FFT_L2": "2"},
-    # v3 (default) with a 4-slot ring and lag 2, so slots are reused ~9 times
-    # per launch and both cross-CTA waits (P2 on P1, P1 on slot release) fire
-    {"DPP_FFT_L2_RING": "4", "DPP_FFT_L2_LAG": "2"},
-    {"DPP_FFT_L2_DISCARD": "0"}, {"DPP_FFT_L2_CFG": "1"},
-]
-
-
-@pytest.mark.parametrize("env", _VARIANTS, ids=lambda e: ",".join(f"{k[8:]}={v}" for k, v in e.items()))
-def test_2e16_kernel_variants(cuda, env):
-    _run_variant(env, 65536)
-
-
-@pytest.mark.parametrize("n", [8192, 16384, 32768, 131072, 262144, 524288, 1048576])
-@pytest.mark.parametrize("env", [{}, {"DPP_FFT_L2_RING": "4", "DPP_FFT_L2_LAG": "2"}, {"DPP_FFT_L2": "0"}],
-                         ids=["default", "ring4-lag2", "cluster"])
-def test_2e13_to_2e15_kernel_variants(cuda, env, n):
-    # n = 256 B: the L2-ring kernel runs units of 256/B transforms (37 is
-    # ragged for all three) and the cluster kernel the remainder; 2^17 runs
-    # 2^18 .. 2^20 one transform per unit (csrc/fft128k_l2.cu); DPP_FFT_L2=0 is
-    # cluster-only (the three-pass path above 2^17)
+@pytest.mark.parametrize("n", [8192, 16384, 32768, 65536, 131072, 262144, 524288, 1048576])
+@pytest.mark.parametrize("env", [{}, {"DPP_RING_STRESS": "1"}], ids=["default", "ring4-lag2"])
+def test_ring_kernels_ragged_and_stressed(cuda, env, n):
+    # every L2-ring kernel with 37 transforms (a ragged persistent grid; for
+    # 2^13..2^15 also a batch remainder on the cluster kernel) and, with
+    # DPP_RING_STRESS=1, a 4-slot ring with lag 2 so ring slots are reused many
+    # times and both cross-CTA waits (P2 on P1, P1 on slot release) fire
     _run_variant(env, n)
 
 
@@ -297,8 +279,7 @@ from paper_1203_4938_b200 import ops
 worst = 0.0
 import os
 shapes = [(1024, 64, 5), (2048, 32, 5), (4096, 64, 5), (8192, 32, 3), (16384, 32, 3)]
-if os.environ.get("DPP_FFT_COLRING") != "0":
-    shapes.append((32768, 16, 2))  # the column ring is the only column pass for 32768 rows
+shapes.append((32768, 16, 2))
 for (r, c, b) in shapes:
     x = complex_signals(r + c, (b, r, c))
     xt = torch.from_numpy(x).cuda()
@@ -311,13 +292,11 @@ print(worst)
 """
 
 
-@pytest.mark.parametrize("env", [{"DPP_FFT_COL_RING": "4", "DPP_FFT_COL_LAG": "2"}, {"DPP_FFT_L2_DISCARD": "0"},
-                                 {"DPP_FFT_COLRING": "0"}],
-                         ids=["ring4-lag2", "no-discard", "cluster-columns"])
+@pytest.mark.parametrize("env", [{}, {"DPP_RING_STRESS": "1"}], ids=["default", "ring4-lag2"])
 def test_2d_column_pass_variants(cuda, env):
-    # the L2-ring column pass (4096- to 32768-row images) with a 4-slot ring
-    # (every slot reused, both waits fire), without L2 discards, and the
-    # cluster column kernel it replaced; in place == out of place, numpy fft2
+    # the L2-ring column pass (1024- to 32768-row images), also with a 4-slot
+    # ring (every slot reused, both waits fire); in place == out of place,
+    # numpy fft2
     import os
     import subprocess
     import sys

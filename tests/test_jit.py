@@ -51,8 +51,8 @@ def test_front_end_matches_reference_verdict(case, jit_meta):
         assert str(info.value) == want["compile_error"]
         return
     k = compile_kernel(node.body, {p.name: p for p in node.io})
-    src, params = generate(k, "k")
-    assert 'extern "C" __global__' in src and len(params) == 2 * len(node.io) + 5
+    src, params, sites = generate(k, "k")
+    assert 'extern "C" __global__' in src and len(params) == 2 * len(node.io) + 7 and sites
 
 
 def test_generated_kernels_compile_with_nvrtc(jit_meta):
@@ -66,7 +66,7 @@ def test_generated_kernels_compile_with_nvrtc(jit_meta):
         if "compile_error" in jit_meta[case["name"]]:
             continue
         node = _node(case)
-        src, _ = generate(compile_kernel(node.body, {p.name: p for p in node.io}), "k_" + case["name"])
+        src, _, _ = generate(compile_kernel(node.body, {p.name: p for p in node.io}), "k_" + case["name"])
         h = C.c_void_p()
         log = C.create_string_buffer(8192)
         rc = lib.dpp_jit_compile(src.encode(), ("k_" + case["name"]).encode(), C.byref(h), log, 8192)
