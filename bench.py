@@ -667,6 +667,45 @@ def run_ours(args) -> None:
           "median_ms": round(lat[len(lat) // 2], 4), "p10_ms": round(lat[len(lat) // 10], 4),
           "parity": {"np_fft_f64_rel_l2": rel_l2(y1, np.fft.fft(x1.astype(np.complex128)))}}
 
+    # ------------------------------------------------- large 1-D, 2^28 points
+    # one signal of 2^28 complex64 (2 GiB): one GPU runs the local large-size
+    # schedule (transpose + rows + twiddled column ring); P GPUs hold 2^28/P
+    # contiguous samples each and run the row-sharded four-step (two NCCL
+    # all-to-alls + one for natural-order output), strong scaling
+    fft1d = {"metric": "1-D FFT GFLOP/s (5N log2 N), N = 2^28"}
+    try:
+        n1d = 1 << 28
+        g1 = torch.Generator(device=dev).manual_seed(11 + rank)
+        part = torch.randn(n1d // world, dtype=torch.complex64, device=dev, generator=g1)
+        if world == 1:
+            out1 = torch.empty_like(part)
+
+            def step1d():
+                ops.fft_forward(part, n1d, out=out1)
+            how = "local: transpose + 16384-point rows + twiddled 16384-point column ring (3 HBM passes)"
+        else:
+            from paper_1203_4938_b200.distributed import fft1d_row_sharded
+
+            def step1d():
+                fft1d_row_sharded(part, n1d)
+            how = (f"row-sharded four-step over {world} GPUs: NCCL all-to-all, column FFTs + twiddle, "
+                   f"all-to-all, row FFTs, all-to-all to natural order")
+        for _ in range(2):
+            step1d()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms1 = max_over_ranks(timed(step1d, 3, stream), world)
+        fft1d.update({"config": f"one 2^28-point complex64 signal, {world} GPU(s): " + how,
+                      "value": round(5.0 * n1d * 28 / (ms1 / 1e3) / 1e9, 1), "ms": round(ms1, 3),
+                      "scaling": "strong",
+                      "roofline": {"bound": "hbm" if world == 1 else "nvlink",
+                                   "compulsory_bytes_per_gpu": 16 * n1d / world,
+                                   "frac_of_compulsory": round(16 * n1d / world / (ms1 / 1e3) / 1e9 / pk["hbm_gbs"],
+                                                               4)}})
+        part = out1 = step1d = None
+    except Exception as exc:
+        fft1d["error"] = f"{type(exc).__name__}: {exc}"[:300]
+
     # ------------------------------------------------------------------ C3
     # measured last: at P > 1 it is the only path that maps peer memory.
     # one GPU: row pass + column-ring pass; P GPUs: row-sharded, the exchange
@@ -815,7 +854,8 @@ def run_ours(args) -> None:
             "e2e_graph": e2e_graph,
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
-            "secondary": {"c1_latency": c1, "compression_c4": compression, "fft2d_c3": fft2d, "chain_c5": chain5},
+            "secondary": {"c1_latency": c1, "compression_c4": compression, "fft2d_c3": fft2d, "chain_c5": chain5,
+                          "fft1d_2e28": fft1d},
         }
         print(json.dumps(line), flush=True)
     if c3_failed and world > 1:

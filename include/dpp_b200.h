@@ -90,6 +90,15 @@ int dpp_fft_c2c_forward_batch(const dpp_fft_plan* plan, const float* in, float* 
  * (SURVEY §8(e) C3). */
 int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, void* stream);
 
+/* Four-step twiddle of the row-sharded 1-D transform, in place: for a
+ * rows x cols row-major complex64 block whose first column is global column
+ * col0 of an R x C view of an n-point signal, data[r][c] *= W_n^{r (col0 + c)}
+ * (angles in binary64 from the exact integer phase).  The sharded 1-D FFT
+ * (distributed.fft1d_row_sharded; the reference's fft() for any power of two,
+ * apps/fft.py:150-174) applies it to each rank's column slab between the
+ * column FFTs and the all-to-all back to row slabs. */
+int dpp_fft_twiddle(float* data, int64_t rows, int64_t cols, int64_t col0, int64_t n, void* stream);
+
 /* C5 fusion: to_complex -> 2-D FFT -> spectrum_u8 in two passes.  in: batch
  * n0 x n1 u8 images; out: batch n0 x n1 u8 spectra (the spectrum_u8 node's
  * arithmetic); work: batch * n0 * n1 complex64 (the row-pass result).  Needs

@@ -31,6 +31,7 @@ SIGNATURES = {
     "dpp_fft_c2c_forward_batch": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "dpp_fft_plan_destroy": (None, [_vp]),
     "dpp_fft_c2c_columns": (_int, [_vp, _vp, _i64, _vp]),
+    "dpp_fft_twiddle": (_int, [_vp, _i64, _i64, _i64, _i64, _vp]),
     "dpp_fft_leaf": (_int, [_int, _vp, _vp, _i64, _vp]),
     "dpp_naive_dft": (_int, [_vp, _vp, _i64, _i64, _vp]),
     "dpp_imgc_ycbcr": (_int, [_vp, _vp, _vp, _vp, _i64, _vp]),

@@ -157,6 +157,12 @@ int dpp_fft_c2c_columns(const dpp_fft_plan* plan, float* data, int64_t batch, vo
                                     static_cast<cudaStream_t>(stream));
 }
 
+int dpp_fft_twiddle(float* data, int64_t rows, int64_t cols, int64_t col0, int64_t n, void* stream) {
+  if (rows * cols > 0 && !data) return dpp::fail(DPP_EINVAL, "NULL data pointer");
+  return dpp::fft_twiddle_slab(reinterpret_cast<float2*>(data), rows, cols, col0, n,
+                               static_cast<cudaStream_t>(stream));
+}
+
 int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* out, float alpha, float* work,
                           int64_t batch, void* stream) {
   if (!plan) return dpp::fail(DPP_EINVAL, "plan is NULL");

@@ -37,7 +37,37 @@ __global__ void __launch_bounds__(256) transpose_c64(const float2* __restrict__ 
   for (int k = 0; k < 32; k += 8) __stcs(dst + (c0 + ty + k) * rows + r0 + tx, t[tx][ty + k]);
 }
 
+// data[r][c] *= W_n^{r (c0 + c)} for a rows x cols row-major block: the
+// four-step twiddle of the row-sharded 1-D transform (distributed.py), whose
+// column slab of rank q starts at global column c0.  Angles in binary64 from
+// the exact integer phase (r (c0 + c)) mod n, rounded once.
+__global__ void __launch_bounds__(256) twiddle_slab(float2* __restrict__ data, int64_t rows, int64_t cols, int64_t c0,
+                                                    int64_t n) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const int64_t m = (int64_t)(((unsigned __int128)r * (uint64_t)(c0 + c)) % (uint64_t)n);
+    double sn, cs;
+    sincospi(-2.0 * (double)m / (double)n, &sn, &cs);
+    const float2 v = data[e];
+    data[e] = cmul(v, make_float2((float)cs, (float)sn));
+  }
+}
+
 }  // namespace
+
+int fft_twiddle_slab(float2* data, int64_t rows, int64_t cols, int64_t c0, int64_t n, cudaStream_t s) {
+  if (rows < 0 || cols < 0 || c0 < 0 || n < 1) return fail(DPP_EINVAL, "bad twiddle block");
+  if (rows * cols == 0) return DPP_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (rows * cols + 255) / 256;
+  const unsigned grid = (unsigned)(blocks < 8LL * sms ? blocks : 8LL * sms);
+  twiddle_slab<<<grid, 256, 0, s>>>(data, rows, cols, c0, n);
+  DPP_LAUNCH_CHECK("twiddle_slab");
+  return DPP_OK;
+}
 
 int fft_large_init(FftPlan* p) {
   const int64_t n = p->n0;

@@ -65,6 +65,7 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
                           uint8_t* spec_out = nullptr, float alpha = 0.f, float2* dst = nullptr,
                           const float2* twlo = nullptr, const float2* twhi = nullptr);
 int fft_large_init(FftPlan* p);
+int fft_twiddle_slab(float2* data, int64_t rows, int64_t cols, int64_t c0, int64_t n, cudaStream_t s);
 int fft_large_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, float2* const* outs, int np, int rank,
                                int tb, int64_t batch, cudaStream_t s);

@@ -9,6 +9,11 @@
   peer pointers) and, for natural-order output, TMA-stores the results straight
   back into the peers' slabs.  No NCCL and no staging copies on the data path;
   two stream-ordered flag barriers per call.
+* ``fft1d_row_sharded`` (large 1-D, north star "large 2D and 1D FFTs shard by
+  rows"): one n-point signal split contiguously over P ranks, n = R x C
+  four-step — all-to-all to column slabs, R-point column FFTs and the
+  W_n^{r c} twiddle on device, all-to-all back, C-point row FFTs; optionally
+  a third all-to-all returns natural-order contiguous output.
 * ``compress_tile_sharded`` (C4): one frame's block rows split
   into P contiguous bands; each rank encodes its band (records, Cb and Cr rows
   are block-local, so a band is an independent sub-image) and the bitstream is
@@ -35,7 +40,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "fft2d_row_sharded", "pack_column_blocks", "unpack_column_blocks",
-           "PeerShardedFft2d", "encode_band", "compress_tile_sharded"]
+           "PeerShardedFft2d", "encode_band", "compress_tile_sharded", "fft1d_split", "fft1d_row_sharded"]
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -315,3 +320,65 @@ def compress_tile_sharded(image, codebook, *, group=None, device=None, encode: C
     return CompressedImage.from_records(w, h, np.asarray(cents.cpu() if isinstance(cents, torch.Tensor) else cents,
                                                          np.float32),
                                         np.concatenate(recs), np.concatenate(cbs), np.concatenate(crs))
+
+
+def fft1d_split(n: int, world: int) -> tuple[int, int]:
+    """n = R x C for the sharded four-step: R = 2^ceil(lg n / 2) >= C, both
+    multiples of the world size (every rank owns R/P rows and C/P columns)."""
+    if n < 4 or n & (n - 1):
+        raise ValueError(f"transform size must be a power of two >= 4, got {n}")
+    lg = n.bit_length() - 1
+    r = 1 << ((lg + 1) // 2)
+    c = n // r
+    if r % world or c % world:
+        raise ValueError(f"{n} = {r} x {c} does not shard over {world} ranks")
+    return r, c
+
+
+def _default_twiddle(x: torch.Tensor, rows: int, cols: int, col0: int, n: int) -> torch.Tensor:
+    from . import ops
+    return ops.fft_twiddle(x, rows, cols, col0, n)
+
+
+def fft1d_row_sharded(local: torch.Tensor, n: int, *, group=None, natural_output: bool = True,
+                      row_fft: Callable | None = None, col_fft: Callable | None = None,
+                      twiddle: Callable | None = None) -> torch.Tensor:
+    """Forward 1-D FFT (the reference's fft(), apps/fft.py:150-174, unnormalised)
+    of one n-point complex64 signal whose samples are split contiguously over
+    the ranks of ``group``: ``local`` holds samples [p n/P, (p+1) n/P).
+
+    Four-step with n = R x C (``fft1d_split``), M[r][c] = x[r C + c]:
+      X[k_r + R k_c] = sum_c W_C^{c k_c} W_n^{c k_r} sum_r M[r][c] W_R^{r k_r}
+    Each rank's row slab goes to column slabs (all-to-all), R-point column
+    FFTs + twiddle run there, the result returns to row slabs (all-to-all) and
+    C-point row FFTs finish: rank p then holds Z[k_r][k_c] = X[k_r + R k_c]
+    for its R/P values of k_r (returned as (R/P, C) if not natural_output).
+    natural_output: a third all-to-all and a local transpose give rank p the
+    contiguous outputs X[p n/P .. (p+1) n/P).  The local transforms default
+    to the sm_100a kernels; the gloo tests inject the oracle."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    r, c = fft1d_split(n, world)
+    if local.numel() != n // world:
+        raise ValueError(f"rank holds {local.numel()} samples, expected {n // world}")
+    cw = c // world
+    twiddle = twiddle or _default_twiddle
+    inner = col_fft or _default_cols
+
+    def columns(slab: torch.Tensor) -> torch.Tensor:  # (R, C/P): this rank's columns, all rows
+        slab = inner(slab)
+        return twiddle(slab, r, cw, rank * cw, n)
+
+    z = fft2d_row_sharded(local.reshape(r // world, c), r, group=group, transpose_back=True,
+                          row_fft=lambda x: x, col_fft=columns)
+    z = (row_fft or _default_rows)(z.contiguous())
+    if not natural_output:
+        return z
+    send = pack_column_blocks(z, world)             # (P, R/P, C/P): block s -> rank s (its k_c)
+    recv = torch.empty_like(send)
+    if world > 1:
+        _all_to_all(recv, send, group)
+    else:
+        recv = send
+    # rows k_r of every rank in order = Z[:, this rank's k_c]; X[k_r + R k_c] natural
+    return recv.reshape(r, cw).t().contiguous().reshape(-1)

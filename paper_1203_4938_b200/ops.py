@@ -129,6 +129,17 @@ def fft2d_forward(x: torch.Tensor, n0: int, n1: int, out: torch.Tensor | None = 
     return out
 
 
+def fft_twiddle(x: torch.Tensor, rows: int, cols: int, col0: int, n: int,
+                stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """In place: x[r][c] *= W_n^{r (col0 + c)} on a rows x cols complex64 block."""
+    _check_cuda(x, "x", torch.complex64)
+    if x.numel() != rows * cols:
+        raise PlanError(f"twiddle block holds {x.numel()} samples, expected {rows} x {cols}")
+    _lib.check(_lib.load().dpp_fft_twiddle(x.data_ptr(), rows, cols, col0, n, stream_handle(stream)),
+               "fft twiddle")
+    return x
+
+
 def fft_columns(x: torch.Tensor, n0: int, n1: int, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """In place: n0-point FFT of every column of batched n0 x n1 row-major arrays."""
     _check_cuda(x, "x", torch.complex64)
