@@ -43,14 +43,17 @@ int fail(int code, const char* fmt, ...);
 // negation are free modifiers).  Halves the FP issue slots of the butterflies.
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-// a * w = a.x * (w.x, w.y) + a.y * (-w.y, w.x)
+// a * w = a.x * (w.x, w.y) + a.y * (-w.y, w.x).  The rotated pair is the FIRST
+// FFMA2 operand: only there does ptxas encode it as a swap + lane-negate
+// modifier (-R.F32x2.LO_HI.NP); as the second operand it materialises the pair
+// with a MOV + FADD per multiply.  Products commute, so the bits are the same.
 __device__ __forceinline__ float2 cmul(float2 a, float2 w) {
-  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x),
-                    __fmul2_rn(make_float2(a.x, a.x), w));
+  return __ffma2_rn(make_float2(-w.y, w.x), make_float2(a.y, a.y),
+                    __fmul2_rn(w, make_float2(a.x, a.x)));
 }
 // same with the rotated twiddle (-w.y, w.x) precomputed (tables store both halves)
 __device__ __forceinline__ float2 cmul_pre(float2 a, float2 w, float2 wrot) {
-  return __ffma2_rn(make_float2(a.y, a.y), wrot, __fmul2_rn(make_float2(a.x, a.x), w));
+  return __ffma2_rn(wrot, make_float2(a.y, a.y), __fmul2_rn(w, make_float2(a.x, a.x)));
 }
 // multiply by -i
 __device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a.x); }
