@@ -299,26 +299,58 @@ __global__ void __launch_bounds__(256) ties_kernel(const EncodeArgs a, unsigned 
 // for one block): pixels -> Y/Cb/Cr (binary32), chroma planes, optional
 // gradient filter, binary64 mean/std, normalised block.  Returns false in
 // STATS mode (outputs written, nothing left to quantise).
+// Gray input (CH = 1, R = G = B = v): Y, Cb, Cr of a pixel are functions of
+// its byte alone, so a 256-entry table of the reference's binary32 results
+// (the same ycc() evaluation, once per value) replaces 9 FMUL + 8 FADD + I2F
+// per pixel with one LDS.128.
+__device__ __forceinline__ void gray_lut_fill(float4* lut, int tid, int nthreads) {
+  for (int v = tid; v < 256; v += nthreads) {
+    const YCC o = ycc((float)v, (float)v, (float)v);
+    lut[v] = make_float4(o.y, o.cb, o.cr, 0.f);
+  }
+}
+
 template <int CH, bool STATS>
 __device__ __forceinline__ bool block_front(const EncodeArgs& a, int64_t img, int64_t k, float (&nb)[16],
-                                            double& mean, double& sd) {
+                                            double& mean, double& sd, const float4* lut = nullptr,
+                                            bool aligned4 = false) {
   const int64_t bw = a.width / 4, bh = a.height / 4, nblocks = bw * bh;
   {
     const int64_t by = k / bw, bx = k - by * bw;
     const uint8_t* base = a.px + img * a.image_stride;
     float yv[16];
     float cbs = 0.f, crs = 0.f;
+    if (CH == 1 && lut) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint8_t* row = base + (4 * by + r) * a.row_stride;
+      for (int r = 0; r < 4; ++r) {
+        const uint8_t* row = base + (4 * by + r) * a.row_stride + 4 * bx;
+        uint32_t w;
+        if (aligned4) {
+          w = __ldg(reinterpret_cast<const unsigned int*>(row));
+        } else {
+          w = (uint32_t)row[0] | (uint32_t)row[1] << 8 | (uint32_t)row[2] << 16 | (uint32_t)row[3] << 24;
+        }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float R, G, B;
-        load_rgb<CH>(row, 4 * bx + c, R, G, B);
-        const YCC o = ycc(R, G, B);
-        yv[4 * r + c] = o.y;
-        cbs = (r == 0 && c == 0) ? o.cb : __fadd_rn(cbs, o.cb);
-        crs = (r == 0 && c == 0) ? o.cr : __fadd_rn(crs, o.cr);
+        for (int c = 0; c < 4; ++c) {
+          const float4 e = lut[(w >> (8 * c)) & 255u];
+          yv[4 * r + c] = e.x;
+          cbs = (r == 0 && c == 0) ? e.y : __fadd_rn(cbs, e.y);
+          crs = (r == 0 && c == 0) ? e.z : __fadd_rn(crs, e.z);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint8_t* row = base + (4 * by + r) * a.row_stride;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float R, G, B;
+          load_rgb<CH>(row, 4 * bx + c, R, G, B);
+          const YCC o = ycc(R, G, B);
+          yv[4 * r + c] = o.y;
+          cbs = (r == 0 && c == 0) ? o.cb : __fadd_rn(cbs, o.cb);
+          crs = (r == 0 && c == 0) ? o.cr : __fadd_rn(crs, o.cr);
+        }
       }
     }
     if constexpr (!STATS) {
@@ -516,26 +548,90 @@ __device__ __forceinline__ void top2(int& m1, int& m2, int x, int y) {
 }
 }  // namespace tc
 
+// Warp-specialised, double-buffered encoder (round 2).  One CTA per SM, 16
+// warps in two independent pipelines b = 0, 1 (local tiles i = b, b + 2, ...):
+//   front group FG_b (warps 4b..4b+3): pixels -> Y/Cb/Cr (gray: table), chroma
+//     bytes, binary64 statistics, normalised block (one block per thread) ->
+//     A operand A_b (-n as tf32 hi + exact lo), mean/sigma bytes; then one
+//     elected thread issues the 3xTF32 + bias MMAs of the WHOLE codebook
+//     (N = 256) into TMEM columns [256 b, 256 b + 256) and commits mma_done[b];
+//   epilogue group EG_b (warps 8 + 4b..): waits mma_done[b], reads the 256
+//     scores of its row (tcgen05.ld), integer-key best / runner-up, the exact
+//     re-check of the rare ambiguous block, index byte; writes the tile's
+//     records and arrives eg_done[b].
+// FG_b computes the statistics of tile i + 2 while EG_b scores tile i and the
+// tensor core runs the other pipeline's MMA; it waits for eg_done[b] only to
+// overwrite A_b / TMEM_b.  Round 1 ran the same phases back to back inside
+// four 128-thread CTAs per SM with two CTA barriers and two MMA waits per tile.
+// Images are processed one after another with every CTA striding over the
+// image's tiles; the codebook (B operand) is restaged between images after a
+// CTA-wide barrier.
+namespace ws {
+constexpr int THREADS = 512;
+constexpr size_t A_BYTES = tc::M * 32 * 4;                  // 16 KB per buffer
+constexpr size_t B_OFF = 0;                                 // codebook hi|lo, 256 x 32 tf32
+constexpr size_t A_OFF = B_OFF + tc::B_BYTES;               // two A buffers
+constexpr size_t CN_OFF = A_OFF + 2 * A_BYTES;              // |c_j|^2
+constexpr size_t ABIAS_OFF = CN_OFF + tc::NCB * 4;          // 8 rows x [1 1 0 0 | 0 0 0 0]
+constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;               // per centroid [hi lo 0 0] of |c|^2/2 + 8
+constexpr size_t LUT_OFF = BBIAS_OFF + tc::NCB * 16;        // gray table, 256 x float4
+constexpr size_t SMEM = LUT_OFF + 256 * 16;
+// kind::tf32, M = 128, N = 256 (the whole codebook in one instruction)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(tc::NCB >> 3) << 17) |
+                           ((uint32_t)(tc::M >> 4) << 24);
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void top2_chunk(int& m1, int& m2, const uint32_t (&r)[32], int j0) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 4) {
+    // four indices packed in one register; PRMT puts byte q of it into the low
+    // byte of the score bits: one instruction per key
+    const uint32_t jq = (uint32_t)(j0 + e) | (uint32_t)(j0 + e + 1) << 8 | (uint32_t)(j0 + e + 2) << 16 |
+                        (uint32_t)(j0 + e + 3) << 24;
+    tc::top2(m1, m2, (int)__byte_perm(r[e], jq, 0x3214), (int)__byte_perm(r[e + 1], jq, 0x3215));
+    tc::top2(m1, m2, (int)__byte_perm(r[e + 2], jq, 0x3216), (int)__byte_perm(r[e + 3], jq, 0x3217));
+  }
+}
+}  // namespace ws
+
 template <int CH>
-__global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs a, int64_t batch,
-                                                                float delta_scale, unsigned long long* ambiguous) {
+__global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeArgs a, int64_t batch,
+                                                                   float delta_scale, unsigned long long* ambiguous) {
   extern __shared__ __align__(1024) uint8_t tsm[];
-  uint8_t* sA = tsm;
-  uint8_t* sB = tsm + tc::A_BYTES;
-  float* scn = reinterpret_cast<float*>(tsm + tc::CN_OFF);  // |c_j|^2
-  __shared__ uint8_t srec[tc::M * 3];
-  __shared__ uint64_t bar;
+  uint8_t* sB = tsm + ws::B_OFF;
+  float* scn = reinterpret_cast<float*>(tsm + ws::CN_OFF);  // |c_j|^2
+  float4* lut = reinterpret_cast<float4*>(tsm + ws::LUT_OFF);
+  __shared__ uint8_t srec[2][tc::M * 3];
+  __shared__ uint8_t szero[2][tc::M];
+  __shared__ __align__(8) uint64_t mma_done[2], eg_done[2], fg_done[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int row = tid;  // one block (A row, TMEM lane) per thread
-  // Each CTA strides over the flat (image, tile) space (neighbouring CTAs on
-  // neighbouring tiles); the codebook (B operand, norms, band) is restaged
-  // only when the stride crosses into the next image.
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool front = warp < 8;
+  const int b = (warp >> 2) & 1;  // pipeline
+  const int row = tid & 127;      // tile row (block) = TMEM lane of this thread
+  const bool aligned4 = (((uintptr_t)a.px | (uintptr_t)a.row_stride | (uintptr_t)a.image_stride) & 3) == 0;
+
   auto stage_codebook = [&](int64_t img) {
     const float* cbk = a.codebook + img * a.codebook_stride;
-    for (int e = tid; e < tc::NCB * 16; e += tc::THREADS) {
+    for (int e = tid; e < tc::NCB * 16; e += ws::THREADS) {
       const int j = e >> 4, k = e & 15;
       const float c = j < a.ncb ? cbk[j * 16 + k] : 0.f;
       const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
@@ -546,11 +642,8 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
       cmax_bits = 0;
       zero_key = ~0ull;
     }
-    if (tid < 64) {  // bias A operand: rows [1 1 0 0 | 0 0 0 0] (one 8-row group, sbo = 0)
-      reinterpret_cast<float*>(tsm + tc::ABIAS_OFF)[tid] = (tid < 32 && (tid & 3) < 2) ? 1.f : 0.f;
-    }
     __syncthreads();
-    for (int j = tid; j < tc::NCB; j += tc::THREADS) {
+    for (int j = tid; j < tc::NCB; j += ws::THREADS) {
       float s = 0.f;
       if (j < a.ncb)
         for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
@@ -559,13 +652,12 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
       // centroids get a huge score so they never win)
       const float bv = j < a.ncb ? fmaf(0.5f, s, tc::BIAS) : 1e30f;
       const float bh = __uint_as_float(__float_as_uint(bv) & 0xFFFFE000u);
-      *reinterpret_cast<float4*>(tsm + tc::BBIAS_OFF + (j >> 3) * 128 + (j & 7) * 16) =
+      *reinterpret_cast<float4*>(tsm + ws::BBIAS_OFF + (j >> 3) * 128 + (j & 7) * 16) =
           make_float4(bh, __fsub_rn(bv, bh), 0.f, 0.f);
       if (j < a.ncb) {
         atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
         // a constant block normalises to exactly 0: its index is the exact
-        // (reference-order) argmin of |c_j|^2, strict <, first index — every
-        // centroid of a normalised codebook ties within the band otherwise
+        // (reference-order) argmin of |c_j|^2, strict <, first index
         float c[16];
         for (int k = 0; k < 16; ++k) c[k] = cbk[j * 16 + k];
         float2 zp[8], cp[8];
@@ -576,188 +668,198 @@ __global__ void __launch_bounds__(tc::THREADS) encode_tc_kernel(const EncodeArgs
         if (d < VQ_BEST_INIT) atomicMin(&zero_key, ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)j);
       }
     }
+    fence_proxy_async_smem();
+    __syncthreads();
   };
-  const int64_t nblocks = (a.width / 4) * (a.height / 4);
-  const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
-  const int64_t all_tiles = ntiles * batch;
-  int64_t img = blockIdx.x / ntiles;
-  stage_codebook(img);
 
+  if (tid < 64)  // bias A operand: rows [1 1 0 0 | 0 0 0 0] (one 8-row group, sbo = 0)
+    reinterpret_cast<float*>(tsm + ws::ABIAS_OFF)[tid] = (tid < 32 && (tid & 3) < 2) ? 1.f : 0.f;
+  if (CH == 1) gray_lut_fill(lut, tid, ws::THREADS);
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(&bar, 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&mma_done[q], 1);
+      mbar_init(&eg_done[q], 4);
+      mbar_init(&fg_done[q], 1);
+    }
     fence_mbar_init();
   }
-  fence_proxy_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = tmem_base_s;
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);  // warp w reads TMEM lanes 32w..32w+31
-  // band half-width: 1.5e-3 at |c| <= 4 (the normalised-block scale), growing
-  // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
-  auto band = [&]() {
-    const float cmax = sqrtf(__uint_as_float(cmax_bits));
-    return 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
-  };
-  float delta2 = band();
+  const uint32_t tmem = tmem_base_s + 256u * b;                         // this pipeline's 256 columns
+  const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);     // lanes 32 (w % 4) ..
+  uint8_t* sA = tsm + ws::A_OFF + b * ws::A_BYTES;
 
-  uint32_t phase = 0;
+  const int64_t nblocks = (a.width / 4) * (a.height / 4);
+  const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
+  uint32_t uses = 0;  // tiles this thread's pipeline has run (barrier phases)
   unsigned long long namb = 0;
-  for (int64_t ft = blockIdx.x; ft < all_tiles; ft += gridDim.x) {
-    if (ft / ntiles != img) {  // next image: its codebook (the previous MMAs have completed)
-      img = ft / ntiles;
-      __syncthreads();
-      stage_codebook(img);
-      fence_proxy_async_smem();
-      __syncthreads();
-      delta2 = band();
-    }
-    const int64_t t = ft - img * ntiles;
-    const int64_t k = t * tc::M + row;
-    const bool active = k < nblocks;
-    float nb[16];
-    double mean = 0.0, sd = 0.0;
-    if (active) {
-      block_front<CH, false>(a, img, k, nb, mean, sd);
-    } else {
+  for (int64_t img = 0; img < batch; ++img) {
+    stage_codebook(img);
+    const float cmax = sqrtf(__uint_as_float(cmax_bits));
+    // band half-width: 1.5e-3 at |c| <= 4 (the normalised-block scale), growing
+    // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
+    const float delta2 = 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
+    const int zero_idx = zero_key == ~0ull ? 0 : (int)(zero_key & 0xffffffffu);
+    // local tiles i = 0, 1, ... of this CTA in this image: t = blockIdx.x + gridDim.x * i
+    for (int64_t t = blockIdx.x + (int64_t)gridDim.x * b; t < ntiles; t += 2 * (int64_t)gridDim.x, ++uses) {
+      const int64_t k = t * tc::M + row;
+      const bool active = k < nblocks;
+      if (front) {
+        // ------------------------------------------------------------ front
+        float nb[16];
+        double mean = 0.0, sd = 0.0;
+        if (active) {
+          block_front<CH, false>(a, img, k, nb, mean, sd, CH == 1 ? lut : nullptr, aligned4);
+        } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) nb[i] = 0.f;
-    }
-    // A row: -n_hi (K 0..15) and the exact remainder -n_lo (K 16..31)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float4 hi, lo;
-      float* h = &hi.x;
-      float* l = &lo.x;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float v = -nb[4 * q + e];
-        h[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-        l[e] = __fsub_rn(v, h[e]);
-      }
-      *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
-      *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
-    }
-    // two MMA passes of 128 centroids each through the same 128 TMEM columns
-    int m1 = 0x7fffffff, m2 = 0x7fffffff;
-#pragma unroll
-    for (int h = 0; h < tc::NCB / tc::NH; ++h) {
-      fence_proxy_async_smem();
-      tc::fence_before();
-      __syncthreads();  // A written (h = 0) / previous half's TMEM reads done (h = 1)
-      if (tid == 0) {
-        tc::fence_after();
-        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB) + h * (tc::NH / 8) * 1024;
-        // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
-        const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
-#pragma unroll
-        for (int m = 0; m < 6; ++m)
-          tc::mma_tf32(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
-        // + |c_j|^2/2 + 8: A = [1 1 0 0 | 0...] in every row, B = [hi lo . . | same quarter again]
-        tc::mma_tf32(tmem, tc::sdesc(smem_u32(tsm + tc::ABIAS_OFF), 128, 0),
-                     tc::sdesc(smem_u32(tsm + tc::BBIAS_OFF) + h * (tc::NH / 8) * 128, 0, 128), 1u);
-        tc::commit(&bar);
-      }
-      mbar_wait(&bar, phase);
-      phase ^= 1;
-      tc::fence_after();
-#pragma unroll
-      for (int cq = 0; cq < tc::NH / 32; ++cq) {
-        uint32_t r[32];
-        tc::ld32(taddr + cq * 32, r);
-        const int j0 = h * tc::NH + cq * 32;
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          // four indices packed in one register; PRMT puts byte q of it into
-          // the low byte of the score bits: one instruction per key
-          const uint32_t jq = (uint32_t)(j0 + e) | (uint32_t)(j0 + e + 1) << 8 | (uint32_t)(j0 + e + 2) << 16 |
-                              (uint32_t)(j0 + e + 3) << 24;
-          tc::top2(m1, m2, (int)__byte_perm(r[e], jq, 0x3214), (int)__byte_perm(r[e + 1], jq, 0x3215));
-          tc::top2(m1, m2, (int)__byte_perm(r[e + 2], jq, 0x3216), (int)__byte_perm(r[e + 3], jq, 0x3217));
+          for (int i = 0; i < 16; ++i) nb[i] = 0.f;
         }
-      }
-    }
-    const int i1 = m1 & 0xFF;
-    const float v1 = tc::key_value(m1), v2 = tc::key_value(m2);
-    // keys drop the low byte: the true best lies in [v1, v1 + quantum)
-    const float quant = __int_as_float((m2 & 0x7F800000) | 0) * 0x1p-15f;  // 2^8 ulps of the runner-up
-    bool zero = active;
+        bool zero = true;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) zero = zero && nb[e] == 0.f;
-    const bool amb = active && !zero && !(v2 - v1 > 0.5f * delta2 + quant);
-    int bj = zero ? (zero_key == ~0ull ? 0 : (int)(zero_key & 0xffffffffu)) : i1;
-    unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
-    // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block at
-    // a time — each lane rescores 8 centroids on the CUDA cores (fp32, error
-    // << DELTA) and runs the reference's exact distance on those inside the
-    // band; a lexicographic (distance, index) warp minimum then reproduces
-    // "strict <, first index wins" over all 256.
-    const int lane = tid & 31;
-    while (amb_lanes) {
-      const int src = __ffs(amb_lanes) - 1;
-      amb_lanes &= amb_lanes - 1;
-      float nv[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) nv[i] = __shfl_sync(0xffffffffu, nb[i], src);
-      // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8)
-      const float lim = __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
-      float2 bp[8];
-      vq_pack(nv, bp);
-      float best = VQ_BEST_INIT;
-      int bx = 0x7fffffff;
-#pragma unroll 1
-      for (int j = lane; j < a.ncb; j += 32) {
-        float c[16];
+        for (int e = 0; e < 16; ++e) zero = zero && nb[e] == 0.f;
+        // A_b, TMEM_b and srec[b] are free once EG_b has finished tile i - 2
+        mbar_wait(&eg_done[b], (uses & 1) ^ 1);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 hi = *reinterpret_cast<const float4*>(sB + tc::off(j, 4 * q));
-          const float4 lo = *reinterpret_cast<const float4*>(sB + tc::off(j, 16 + 4 * q));
-          c[4 * q] = __fadd_rn(hi.x, lo.x);  // hi + lo == c exactly
-          c[4 * q + 1] = __fadd_rn(hi.y, lo.y);
-          c[4 * q + 2] = __fadd_rn(hi.z, lo.z);
-          c[4 * q + 3] = __fadd_rn(hi.w, lo.w);
-        }
-        float dotv = 0.f;
+          float4 hi, lo;
+          float* h = &hi.x;
+          float* l = &lo.x;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dotv = fmaf(nv[i], c[i], dotv);
-        if (fmaf(-2.f, dotv, scn[j]) <= lim) {
-          float2 cp[8];
-          vq_pack(c, cp);
-          const float d = vq_dist_pairs(bp, cp);
-          if (d < best) { best = d; bx = j; }
+          for (int e = 0; e < 4; ++e) {
+            const float v = -nb[4 * q + e];
+            h[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            l[e] = __fsub_rn(v, h[e]);
+          }
+          *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
+          *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
         }
-      }
+        srec[b][3 * row + 0] = q8d(mean);
+        srec[b][3 * row + 1] = q8d(__dmul_rn(sd, 4.0));  // sd / 0.25 is exact
+        szero[b][row] = active && zero ? 1 : 0;
+        fence_proxy_async_smem();
+        ws::named_sync(1 + b, 128);
+        if ((tid & 127) == 0) {
+          tc::fence_after();
+          const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+          // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
+          const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float od = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bx, o);
-        if (od < best || (od == best && oj < bx)) { best = od; bx = oj; }
-      }
-      if (lane == src) {
-        bj = bx == 0x7fffffff ? 0 : bx;
-        ++namb;
+          for (int m = 0; m < 6; ++m)
+            ws::mma(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
+          // + |c_j|^2/2 + 8: A = [1 1 0 0 | 0...] in every row, B = [hi lo . . | same quarter again]
+          ws::mma(tmem, tc::sdesc(smem_u32(tsm + ws::ABIAS_OFF), 128, 0),
+                  tc::sdesc(smem_u32(tsm + ws::BBIAS_OFF), 0, 128), 1u);
+          tc::commit(&mma_done[b]);
+          // srec / szero of this tile (written by all 128 front threads before
+          // the named barrier) are published to the epilogue group
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fg_done[b])) : "memory");
+        }
+      } else {
+        // --------------------------------------------------------- epilogue
+        mbar_wait(&mma_done[b], uses & 1);
+        mbar_wait(&fg_done[b], uses & 1);
+        tc::fence_after();
+        int m1 = 0x7fffffff, m2 = 0x7fffffff;
+#pragma unroll
+        for (int cq = 0; cq < tc::NCB / 32; cq += 2) {
+          uint32_t r0[32], r1[32];
+          ws::ld32_nowait(taddr + cq * 32, r0);
+          ws::ld32_nowait(taddr + cq * 32 + 32, r1);
+          ws::ld_wait();
+          ws::top2_chunk(m1, m2, r0, cq * 32);
+          ws::top2_chunk(m1, m2, r1, cq * 32 + 32);
+        }
+        const int i1 = m1 & 0xFF;
+        const float v1 = tc::key_value(m1), v2 = tc::key_value(m2);
+        // keys drop the low byte: the true best lies in [v1, v1 + quantum)
+        const float quant = __int_as_float((m2 & 0x7F800000) | 0) * 0x1p-15f;  // 2^8 ulps of the runner-up
+        const bool zero = szero[b][row] != 0;
+        const bool amb = active && !zero && !(v2 - v1 > 0.5f * delta2 + quant);
+        int bj = zero ? zero_idx : i1;
+        unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
+        // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block
+        // at a time — each lane rescores 8 centroids on the CUDA cores (fp32,
+        // error << DELTA) and runs the reference's exact distance on those inside
+        // the band; a lexicographic (distance, index) warp minimum reproduces
+        // "strict <, first index wins" over all 256.  The block comes back from
+        // A_b (-(hi + lo) == n exactly).
+        while (amb_lanes) {
+          const int src = __ffs(amb_lanes) - 1;
+          amb_lanes &= amb_lanes - 1;
+          const int srow = (row & ~31) + src;
+          float nv[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 hi = *reinterpret_cast<const float4*>(sA + tc::off(srow, 4 * q));
+            const float4 lo = *reinterpret_cast<const float4*>(sA + tc::off(srow, 16 + 4 * q));
+            nv[4 * q] = -__fadd_rn(hi.x, lo.x);
+            nv[4 * q + 1] = -__fadd_rn(hi.y, lo.y);
+            nv[4 * q + 2] = -__fadd_rn(hi.z, lo.z);
+            nv[4 * q + 3] = -__fadd_rn(hi.w, lo.w);
+          }
+          // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8)
+          const float lim = __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
+          float2 bp[8];
+          vq_pack(nv, bp);
+          float best = VQ_BEST_INIT;
+          int bx = 0x7fffffff;
+#pragma unroll 1
+          for (int j = lane; j < a.ncb; j += 32) {
+            float c[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 hi = *reinterpret_cast<const float4*>(sB + tc::off(j, 4 * q));
+              const float4 lo = *reinterpret_cast<const float4*>(sB + tc::off(j, 16 + 4 * q));
+              c[4 * q] = __fadd_rn(hi.x, lo.x);  // hi + lo == c exactly
+              c[4 * q + 1] = __fadd_rn(hi.y, lo.y);
+              c[4 * q + 2] = __fadd_rn(hi.z, lo.z);
+              c[4 * q + 3] = __fadd_rn(hi.w, lo.w);
+            }
+            float dotv = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dotv = fmaf(nv[i], c[i], dotv);
+            if (fmaf(-2.f, dotv, scn[j]) <= lim) {
+              float2 cp[8];
+              vq_pack(c, cp);
+              const float d = vq_dist_pairs(bp, cp);
+              if (d < best) { best = d; bx = j; }
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const float od = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bx, o);
+            if (od < best || (od == best && oj < bx)) { best = od; bx = oj; }
+          }
+          if (lane == src) {
+            bj = bx == 0x7fffffff ? 0 : bx;
+            ++namb;
+          }
+        }
+        if (active) srec[b][3 * row + 2] = (uint8_t)bj;
+        tc::fence_before();
+        ws::named_sync(3 + b, 128);
+        const int64_t k0 = t * tc::M;
+        const int64_t nrec = (nblocks - k0 < tc::M ? nblocks - k0 : tc::M) * 3;
+        uint8_t* rec = a.records + (img * nblocks + k0) * 3;
+        for (int e = row; e < nrec; e += tc::M) rec[e] = srec[b][e];
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&eg_done[b])) : "memory");
       }
     }
-    if (active) {
-      srec[3 * tid + 0] = q8d(mean);
-      srec[3 * tid + 1] = q8d(__dmul_rn(sd, 4.0));
-      srec[3 * tid + 2] = (uint8_t)bj;
-    }
-    tc::fence_before();
+    // every MMA of this image has been waited for by its epilogue group and
+    // every epilogue has finished reading A/B: the codebook may be replaced
     __syncthreads();
-    const int64_t k0 = t * tc::M;
-    const int64_t nrec = (nblocks - k0 < tc::M ? nblocks - k0 : tc::M) * 3;
-    uint8_t* rec = a.records + (img * nblocks + k0) * 3;
-    for (int e = tid; e < nrec; e += tc::THREADS) rec[e] = srec[e];
   }
   if (ambiguous && namb) atomicAdd(ambiguous, namb);
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_s));
 }
 
 // DPP_IMGC_VQ=exact selects the CUDA-core brute force (1), default tensor cores (0)
@@ -775,24 +877,25 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
     cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (sm_count <= 0) sm_count = 148;
   }
+  // one CTA per SM (all 512 TMEM columns); every CTA takes every image's tiles
+  // in a stride of the grid, so a grid larger than one image's tiles idles
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
-  const int64_t all_tiles = ntiles * batch;
-  const int64_t resident = tc::CTAS_PER_SM * (int64_t)sm_count;  // SMEM, TMEM columns, registers
-  dim3 grid((unsigned)(all_tiles < resident ? all_tiles : resident));
-  const size_t smem = tc::SMEM;
+  const int64_t want = ntiles < 2 ? 1 : (ntiles + 1) / 2;  // both pipelines of a CTA busy
+  dim3 grid((unsigned)(want < sm_count ? want : sm_count));
+  const size_t smem = ws::SMEM;
   switch (channels) {
 #define TC_CASE(CHN)                                                                                        \
   case CHN:                                                                                                 \
-    DPP_CUDA_CHECK(cudaFuncSetAttribute(encode_tc_kernel<CHN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(encode_ws_kernel<CHN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         (int)smem));                                                        \
-    encode_tc_kernel<CHN><<<grid, tc::THREADS, smem, s>>>(a, batch, delta_scale, ambiguous);                       \
+    encode_ws_kernel<CHN><<<grid, ws::THREADS, smem, s>>>(a, batch, delta_scale, ambiguous);              \
     break;
     TC_CASE(1)
     TC_CASE(3)
     TC_CASE(4)
 #undef TC_CASE
   }
-  DPP_LAUNCH_CHECK("encode_tc_kernel");
+  DPP_LAUNCH_CHECK("encode_ws_kernel");
   return DPP_OK;
 }
 
