@@ -72,6 +72,11 @@ typedef struct dpp_fft_plan dpp_fft_plan;
 int dpp_fft_plan_create(dpp_fft_plan** plan, int rank, int64_t n0, int64_t n1,
                         int64_t batch, size_t* workspace_bytes);
 
+/* 1 when dpp_fft_plan_create would accept (rank, n0, n1), else 0.  Pure
+ * shape rules: no device, no allocation (plan-time validation in the graph
+ * engine, engine.py:82-135, must not touch a GPU). */
+int dpp_fft_plan_supported(int rank, int64_t n0, int64_t n1);
+
 /* Human-readable kernel schedule of a plan (for logs and bench lines). */
 int dpp_fft_plan_describe(const dpp_fft_plan* plan, char* buf, size_t len);
 
@@ -215,6 +220,16 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
                     const float* codebook, int n_cb, int64_t codebook_stride, double sigma_min,
                     uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
                     float* block_grad, float* norm32, void* stream);
+
+/* Same encoder with the three record bytes written as planes (per block:
+ * mu_plane[k], sig_plane[k], idx_plane[k]; strides per image = blocks), the
+ * layout of the graph node's mu / sig / idx outputs, so a device-resident
+ * edge needs no de-interleaving pass. */
+int dpp_imgc_encode_planar(const uint8_t* px, int channels, int64_t height, int64_t width,
+                           int64_t row_stride, int64_t image_stride, int64_t batch,
+                           const float* codebook, int n_cb, int64_t codebook_stride, double sigma_min,
+                           uint8_t* mu_plane, uint8_t* sig_plane, uint8_t* idx_plane,
+                           uint8_t* cb_plane, uint8_t* cr_plane, void* stream);
 
 /* The encoder's nearest-centroid search runs on the tensor cores (tcgen05
  * kind::tf32, 3xTF32 split) with an exact binary32 re-check of every

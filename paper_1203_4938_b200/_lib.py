@@ -27,6 +27,7 @@ SIGNATURES = {
     "dpp_last_error": (C.c_char_p, []),
     "dpp_fft_plan_create": (_int, [C.POINTER(_vp), _int, _i64, _i64, _i64, C.POINTER(_sz)]),
     "dpp_fft_plan_describe": (_int, [_vp, C.c_char_p, _sz]),
+    "dpp_fft_plan_supported": (_int, [_int, _i64, _i64]),
     "dpp_fft_c2c_forward": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "dpp_fft_c2c_forward_batch": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "dpp_fft_plan_destroy": (None, [_vp]),
@@ -40,6 +41,8 @@ SIGNATURES = {
     "dpp_imgc_vqnearest": (_int, [_vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "dpp_imgc_encode": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _int, _i64,
                                C.c_double, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dpp_imgc_encode_planar": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _int, _i64,
+                                      C.c_double, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dpp_imgc_decode": (_int, [_vp, _vp, _vp, _vp, _int, _i64, _i64, _vp, _vp]),
     "dpp_imgc_encode_tc_debug": (_int, [_vp, _int, _i64, _i64, _vp, _int, _vp, _vp, _vp, C.c_float, _vp, _vp]),
     "dpp_u8_to_complex": (_int, [_vp, _vp, _i64, _vp]),

@@ -116,6 +116,12 @@ int dpp_fft_plan_create(dpp_fft_plan** plan, int rank, int64_t n0, int64_t n1, i
   return DPP_OK;
 }
 
+int dpp_fft_plan_supported(int rank, int64_t n0, int64_t n1) {
+  if (rank == 1) return n0 >= 2 && (n0 & (n0 - 1)) == 0 && n0 <= (1LL << 30);
+  if (rank == 2) return dpp::fft2d_shape_supported(n0, n1) ? 1 : 0;
+  return 0;
+}
+
 int dpp_fft_plan_describe(const dpp_fft_plan* plan, char* buf, size_t len) {
   if (!plan || !buf || len == 0) return dpp::fail(DPP_EINVAL, "bad describe arguments");
   snprintf(buf, len, "%s", plan->impl.desc);
@@ -170,8 +176,12 @@ int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* 
   if (p.rank != 2) return dpp::fail(DPP_EINVAL, "the fused u8 -> 2-D FFT -> spectrum path needs a rank-2 plan");
   if (batch < 0 || batch > p.batch)
     return dpp::fail(DPP_EINVAL, "batch %lld outside the planned 0..%lld", (long long)batch, (long long)p.batch);
-  if (!p.rows || !p.rows->ws4k || !p.col_ring)
-    return dpp::fail(DPP_ENOTSUP, "no fused schedule for %lld x %lld (needs 4096 columns and a ring column pass)",
+  // the spectrum epilogue exists for the 4096- and 16384-row rings only:
+  // reject everything else before the row pass is launched
+  if (!p.rows || !p.rows->ws4k || !p.col_ring || (p.n0 != 4096 && p.n0 != 16384))
+    return dpp::fail(DPP_ENOTSUP,
+                     "no fused schedule for %lld x %lld (needs 4096 or 16384 rows of 4096 columns and a ring "
+                     "column pass)",
                      (long long)p.n0, (long long)p.n1);
   if (batch == 0) return DPP_OK;
   if (!in || !out || !work) return dpp::fail(DPP_EINVAL, "NULL data pointer");

@@ -192,6 +192,20 @@ static int launch_columns(float2* data, int64_t ncols, int64_t batch, const floa
 std::vector<float2> twiddle_table(int64_t n, int64_t count);
 int upload_table(const std::vector<float2>& h, float2** d);
 
+// the shape rules of fft2d_plan_init / fft2d_colring_init, without the device
+bool fft2d_shape_supported(int64_t n0, int64_t n1) {
+  if (n0 < 2 || (n0 & (n0 - 1)) || n1 < 2 || (n1 & (n1 - 1)) || n1 > (1LL << 30)) return false;
+  int width = 0;
+  switch (n0) {
+#define WIDTH(L, A, B, C, W) \
+  case L: width = W; break;
+    DPP_COLUMN_TABLE(WIDTH)
+#undef WIDTH
+    case 32768: width = 16; break;
+  }
+  return width && n1 % width == 0;
+}
+
 int fft2d_plan_init(FftPlan* p) {
   const int64_t n0 = p->n0, n1 = p->n1;
   if (n0 < 2 || (n0 & (n0 - 1)) || n1 < 2 || (n1 & (n1 - 1)))

@@ -642,7 +642,7 @@ int fft2d_colring_execute_peer(const FftPlan* p, const float2* const* slabs, flo
                                int tb, int64_t batch, cudaStream_t s) {
   const int64_t R = p->n0, C = p->n1;
   const int B = (int)(R / 256);
-  if (!p->col_ring) return fail(DPP_ENOTSUP, "row-sharded column pass needs the column ring (n0 = 4096 or 16384)");
+  if (!p->col_ring) return fail(DPP_ENOTSUP, "row-sharded column pass needs the column ring (n0 = 1024 .. 32768, rows a multiple of 16 columns)");
   if (np < 1 || np > 8 || (np & (np - 1)) || B % np)
     return fail(DPP_EINVAL, "rank count %d must be a power of two <= 8 dividing %d", np, B);
   if (rank < 0 || rank >= np) return fail(DPP_EINVAL, "rank %d outside 0..%d", rank, np - 1);

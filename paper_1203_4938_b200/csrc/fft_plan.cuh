@@ -55,6 +55,7 @@ struct FftPlan {
 int fft1d_plan_init(FftPlan* p);
 int fft1d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_plan_init(FftPlan* p);
+bool fft2d_shape_supported(int64_t n0, int64_t n1);
 int fft2d_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft2d_columns_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s);
 void fft_plan_release(FftPlan* p);

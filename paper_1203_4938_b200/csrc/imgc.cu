@@ -215,6 +215,12 @@ struct EncodeArgs {
   float* block_grad;
   float* norm32;
   double* norm64;  // STATS variant only
+  // planar records (graph node outputs mu / sig / idx): when set, the
+  // tensor-core encoder writes the three record bytes to these planes
+  // instead of the interleaved `records` run
+  uint8_t* mu_plane;
+  uint8_t* sig_plane;
+  uint8_t* idx_plane;
 };
 
 template <int CH>
@@ -313,7 +319,7 @@ __device__ __forceinline__ void gray_lut_fill(float4* lut, int tid, int nthreads
 template <int CH, bool STATS>
 __device__ __forceinline__ bool block_front(const EncodeArgs& a, int64_t img, int64_t k, float (&nb)[16],
                                             double& mean, double& sd, const float4* lut = nullptr,
-                                            bool aligned4 = false) {
+                                            bool aligned4 = false, const uint32_t* pre = nullptr) {
   const int64_t bw = a.width / 4, bh = a.height / 4, nblocks = bw * bh;
   {
     const int64_t by = k / bw, bx = k - by * bw;
@@ -325,7 +331,9 @@ __device__ __forceinline__ bool block_front(const EncodeArgs& a, int64_t img, in
       for (int r = 0; r < 4; ++r) {
         const uint8_t* row = base + (4 * by + r) * a.row_stride + 4 * bx;
         uint32_t w;
-        if (aligned4) {
+        if (pre) {
+          w = pre[r];  // loaded one tile ahead by the caller
+        } else if (aligned4) {
           w = __ldg(reinterpret_cast<const unsigned int*>(row));
         } else {
           w = (uint32_t)row[0] | (uint32_t)row[1] << 8 | (uint32_t)row[2] << 16 | (uint32_t)row[3] << 24;
@@ -449,8 +457,14 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
     srec[3 * t + 0] = q8d(mean);
     srec[3 * t + 1] = q8d(__dmul_rn(sd, 4.0));  // sd / 0.25 is exact
     srec[3 * t + 2] = (uint8_t)bj;
+    if (a.idx_plane) {
+      a.mu_plane[img * nblocks + k] = srec[3 * t];
+      a.sig_plane[img * nblocks + k] = srec[3 * t + 1];
+      a.idx_plane[img * nblocks + k] = srec[3 * t + 2];
+    }
   }
   if constexpr (!STATS) {
+    if (a.idx_plane) return;
     __syncthreads();
     // records of this CTA are one contiguous run: write it with coalesced bytes
     const int64_t nrec = (nblocks - k0 < (int64_t)blockDim.x ? nblocks - k0 : (int64_t)blockDim.x) * 3;
@@ -535,43 +549,33 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-// keys: the score bits with centroid index j in the low byte — non-negative
-// fp32 values order like their bit patterns, so an integer min picks the
-// smallest score (to within the low byte) and carries its index along
-__device__ __forceinline__ float key_value(int k) { return __int_as_float(k & (int)0xFFFFFF00u); }
-// best (m1) and runner-up (m2) keys after two more candidates x, y:
-// the second smallest of {m1, m2, x, y} is min(m2, max(m1, min(x, y)), max(x, y))
-__device__ __forceinline__ void top2(int& m1, int& m2, int x, int y) {
-  const int lo = min(x, y), hi = max(x, y);
-  m2 = __vimin3_s32(m2, max(m1, lo), hi);
-  m1 = min(m1, lo);
-}
 }  // namespace tc
 
-// Warp-specialised, double-buffered encoder (round 2).  One CTA per SM, 16
-// warps in two independent pipelines b = 0, 1 (local tiles i = b, b + 2, ...):
-//   front group FG_b (warps 4b..4b+3): pixels -> Y/Cb/Cr (gray: table), chroma
-//     bytes, binary64 statistics, normalised block (one block per thread) ->
-//     A operand A_b (-n as tf32 hi + exact lo), mean/sigma bytes; then one
-//     elected thread issues the 3xTF32 + bias MMAs of the WHOLE codebook
-//     (N = 256) into TMEM columns [256 b, 256 b + 256) and commits mma_done[b];
-//   epilogue group EG_b (warps 8 + 4b..): waits mma_done[b], reads the 256
-//     scores of its row (tcgen05.ld), integer-key best / runner-up, the exact
-//     re-check of the rare ambiguous block, index byte; writes the tile's
-//     records and arrives eg_done[b].
-// FG_b computes the statistics of tile i + 2 while EG_b scores tile i and the
-// tensor core runs the other pipeline's MMA; it waits for eg_done[b] only to
-// overwrite A_b / TMEM_b.  Round 1 ran the same phases back to back inside
-// four 128-thread CTAs per SM with two CTA barriers and two MMA waits per tile.
-// Images are processed one after another with every CTA striding over the
-// image's tiles; the codebook (B operand) is restaged between images after a
-// CTA-wide barrier.
+// Encoder (round 2): one CTA per SM, 16 warps in FOUR identical groups of
+// 128 threads; group g takes local tiles i = g, g + 4, ... (128 blocks each,
+// one block per thread) and runs every phase of its tile itself:
+//   front: pixels -> Y/Cb/Cr (gray: table), chroma bytes, binary64
+//     statistics, normalised block -> the group's A buffer (-n as tf32 hi +
+//     exact lo); the record bytes mu / sigma stay in the thread's registers;
+//   MMA: one elected thread issues the 3xTF32 + bias MMAs of the whole
+//     codebook (N = 256) into TMEM slot i & 1 (256 columns) once the group
+//     two tiles back has read that slot, and commits mma_done[i & 1];
+//   rank: tcgen05.ld of the row's 256 scores (32 per chunk), chunk minimum
+//     and threshold count on the FMA pipe, TMEM slot released, the exact
+//     re-check of the rare ambiguous block, the record written.
+// The front of a tile is a long binary64 latency chain; four groups keep
+// four such chains (and the short rank phases) in flight per SM partition
+// where a front / epilogue split kept two, with the two TMEM slots shared
+// by the groups in tile order.  Images are processed one after another with
+// every CTA striding over the image's tiles; the codebook (B operand) is
+// restaged between images after a CTA-wide barrier.
+
 namespace ws {
 constexpr int THREADS = 512;
 constexpr size_t A_BYTES = tc::M * 32 * 4;                  // 16 KB per buffer
 constexpr size_t B_OFF = 0;                                 // codebook hi|lo, 256 x 32 tf32
-constexpr size_t A_OFF = B_OFF + tc::B_BYTES;               // two A buffers
-constexpr size_t CN_OFF = A_OFF + 2 * A_BYTES;              // |c_j|^2
+constexpr size_t A_OFF = B_OFF + tc::B_BYTES;               // A buffers, one per group
+constexpr size_t CN_OFF = A_OFF + 4 * A_BYTES;              // |c_j|^2
 constexpr size_t ABIAS_OFF = CN_OFF + tc::NCB * 4;          // 8 rows x [1 1 0 0 | 0 0 0 0]
 constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;               // per centroid [hi lo 0 0] of |c|^2/2 + 8
 constexpr size_t LUT_OFF = BBIAS_OFF + tc::NCB * 16;        // gray table, 256 x float4
@@ -597,16 +601,37 @@ __device__ __forceinline__ void ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void top2_chunk(int& m1, int& m2, const uint32_t (&r)[32], int j0) {
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float m;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(m) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+  return m;
+}
+// Rank one 32-column chunk of a row's scores v_j (j = j0 .. j0 + 31) on the
+// FMA pipe.  cm = the chunk minimum; every score below thr = RN(cm + band)
+// gets t_j = 1, every other t_j = 0 — FFMA.SAT(v_j, -2^60, 2^60 thr) is
+// exactly 0 or 1 because the fused product-sum differs from 0 by >= 2^27
+// unless v_j == thr (then 0): thr >= band >= 2^-14 has ulp >= 2^-37.  acc =
+// sum t_j (1024 + j) is exact in binary32 (<= 32 * 1279 < 2^24): acc < 2048
+// means the minimum is the only score of the chunk below thr, and then
+// acc - 1024 is its column.  2 FMA-pipe ops per score (immediate forms) and
+// 1/2 ALU op (3-input min), where a best / runner-up tournament on integer
+// keys costs 3.5 ALU ops per score.
+__device__ __forceinline__ void rank_chunk(const uint32_t (&r)[32], int j0, float band60, float& cm, float& acc) {
+  float m[11];
 #pragma unroll
-  for (int e = 0; e < 32; e += 4) {
-    // four indices packed in one register; PRMT puts byte q of it into the low
-    // byte of the score bits: one instruction per key
-    const uint32_t jq = (uint32_t)(j0 + e) | (uint32_t)(j0 + e + 1) << 8 | (uint32_t)(j0 + e + 2) << 16 |
-                        (uint32_t)(j0 + e + 3) << 24;
-    tc::top2(m1, m2, (int)__byte_perm(r[e], jq, 0x3214), (int)__byte_perm(r[e + 1], jq, 0x3215));
-    tc::top2(m1, m2, (int)__byte_perm(r[e + 2], jq, 0x3216), (int)__byte_perm(r[e + 3], jq, 0x3217));
+  for (int e = 0; e < 10; ++e)
+    m[e] = fmin3(__uint_as_float(r[3 * e]), __uint_as_float(r[3 * e + 1]), __uint_as_float(r[3 * e + 2]));
+  m[10] = fminf(__uint_as_float(r[30]), __uint_as_float(r[31]));
+  cm = fmin3(fmin3(fmin3(m[0], m[1], m[2]), fmin3(m[3], m[4], m[5]), fmin3(m[6], m[7], m[8])), m[9], m[10]);
+  const float beta = fmaf(cm, 0x1p60f, band60);  // 2^60 RN(cm + band): power-of-two scaling is exact
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    float t;
+    asm("fma.rn.sat.f32 %0, %1, 0fDD800000, %2;" : "=f"(t) : "f"(__uint_as_float(r[e])), "f"(beta));  // -2^60
+    a[e & 3] = fmaf(t, (float)(1024 + j0 + e), a[e & 3]);
   }
+  acc = (a[0] + a[1]) + (a[2] + a[3]);
 }
 }  // namespace ws
 
@@ -617,17 +642,17 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
   uint8_t* sB = tsm + ws::B_OFF;
   float* scn = reinterpret_cast<float*>(tsm + ws::CN_OFF);  // |c_j|^2
   float4* lut = reinterpret_cast<float4*>(tsm + ws::LUT_OFF);
-  __shared__ uint8_t srec[2][tc::M * 3];
-  __shared__ uint8_t szero[2][tc::M];
-  __shared__ __align__(8) uint64_t mma_done[2], eg_done[2], fg_done[2];
+  // mma_done per GROUP: a barrier shared by the two groups of a TMEM slot
+  // would let a group's parity wait see the other group's completed phase
+  __shared__ __align__(8) uint64_t mma_done[4], tmem_free[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool front = warp < 8;
-  const int b = (warp >> 2) & 1;  // pipeline
+  const int grp = warp >> 2;      // group: local tiles grp, grp + 4, ...
   const int row = tid & 127;      // tile row (block) = TMEM lane of this thread
   const bool aligned4 = (((uintptr_t)a.px | (uintptr_t)a.row_stride | (uintptr_t)a.image_stride) & 3) == 0;
+  uint8_t* sA = tsm + ws::A_OFF + grp * ws::A_BYTES;
 
   auto stage_codebook = [&](int64_t img) {
     const float* cbk = a.codebook + img * a.codebook_stride;
@@ -680,23 +705,22 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int q = 0; q < 2; ++q) {
-      mbar_init(&mma_done[q], 1);
-      mbar_init(&eg_done[q], 4);
-      mbar_init(&fg_done[q], 1);
-    }
+    for (int q = 0; q < 4; ++q) mbar_init(&mma_done[q], 1);
+    for (int q = 0; q < 2; ++q) mbar_init(&tmem_free[q], 4);
     fence_mbar_init();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = tmem_base_s + 256u * b;                         // this pipeline's 256 columns
-  const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);     // lanes 32 (w % 4) ..
-  uint8_t* sA = tsm + ws::A_OFF + b * ws::A_BYTES;
 
   const int64_t nblocks = (a.width / 4) * (a.height / 4);
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
-  uint32_t uses = 0;  // tiles this thread's pipeline has run (barrier phases)
+  // u counts this CTA's local tiles over all images (every group steps it by
+  // one per tile of every group, so all threads agree on the barrier phases):
+  // tile u belongs to group u & 3 and uses TMEM slot u & 1 for the
+  // (u >> 1)-th time
+  uint32_t u0 = 0;
+  uint32_t gtiles = 0;  // tiles this group has run (mma_done[grp] phases)
   unsigned long long namb = 0;
   for (int64_t img = 0; img < batch; ++img) {
     stage_codebook(img);
@@ -705,155 +729,181 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
     // with the distance magnitude (4 + |c|max)^2 for larger codebook vectors
     const float delta2 = 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
     const int zero_idx = zero_key == ~0ull ? 0 : (int)(zero_key & 0xffffffffu);
-    // local tiles i = 0, 1, ... of this CTA in this image: t = blockIdx.x + gridDim.x * i
-    for (int64_t t = blockIdx.x + (int64_t)gridDim.x * b; t < ntiles; t += 2 * (int64_t)gridDim.x, ++uses) {
+    const int64_t nlocal = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    for (int64_t i = grp; i < nlocal; i += 4) {
+      const uint32_t u = u0 + (uint32_t)i;
+      const int slot = u & 1;
+      const uint32_t use = u >> 1;
+      const uint32_t tmem = tmem_base_s + 256u * slot;
+      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // lanes 32 (w % 4) ..
+      const int64_t t = blockIdx.x + (int64_t)gridDim.x * i;
       const int64_t k = t * tc::M + row;
       const bool active = k < nblocks;
-      if (front) {
-        // ------------------------------------------------------------ front
-        float nb[16];
-        double mean = 0.0, sd = 0.0;
-        if (active) {
-          block_front<CH, false>(a, img, k, nb, mean, sd, CH == 1 ? lut : nullptr, aligned4);
-        } else {
+      // ---------------------------------------------------------------- front
+      float nb[16];
+      double mean = 0.0, sd = 0.0;
+      if (active) {
+        block_front<CH, false>(a, img, k, nb, mean, sd, CH == 1 ? lut : nullptr, aligned4);
+      } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) nb[i] = 0.f;
+        for (int e = 0; e < 16; ++e) nb[e] = 0.f;
+      }
+      bool zero = true;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) zero = zero && nb[e] == 0.f;
+      const uint8_t mu = q8d(mean), sg = q8d(__dmul_rn(sd, 4.0));  // sd / 0.25 is exact
+      // the group's A buffer: its previous reader (the MMA of tile u - 4) was
+      // waited for by this group's own rank phase
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 hi, lo;
+        float* h = &hi.x;
+        float* l = &lo.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v = -nb[4 * q + e];
+          h[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+          l[e] = __fsub_rn(v, h[e]);
         }
-        bool zero = true;
+        *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
+        *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
+      }
+      fence_proxy_async_smem();
+      ws::named_sync(1 + grp, 128);
+      // ------------------------------------------------------------------ MMA
+      if (row == 0) {
+        // TMEM slot: free once tile u - 2 (another group) has read its scores
+        mbar_wait(&tmem_free[slot], (use & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
+        const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
 #pragma unroll
-        for (int e = 0; e < 16; ++e) zero = zero && nb[e] == 0.f;
-        // A_b, TMEM_b and srec[b] are free once EG_b has finished tile i - 2
-        mbar_wait(&eg_done[b], (uses & 1) ^ 1);
+        for (int m = 0; m < 6; ++m)
+          ws::mma(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
+        // + |c_j|^2/2 + 8: A = [1 1 0 0 | 0...] in every row, B = [hi lo . . | same quarter again]
+        ws::mma(tmem, tc::sdesc(smem_u32(tsm + ws::ABIAS_OFF), 128, 0),
+                tc::sdesc(smem_u32(tsm + ws::BBIAS_OFF), 0, 128), 1u);
+        tc::commit(&mma_done[grp]);
+      }
+      // ----------------------------------------------------------------- rank
+      mbar_wait(&mma_done[grp], gtiles & 1);
+      ++gtiles;
+      tc::fence_after();
+      // chunks of 32 columns: chunk minimum + count / column of the scores
+      // within `band` of it; across chunks keep the smallest minimum and its
+      // chunk's count.  A block is ambiguous when the smallest chunk holds a
+      // second score below min + band or another chunk's minimum lies within
+      // band of it (conservative when an earlier pair of chunk minima was
+      // close and a later chunk undercuts both: a re-check, never a miss).
+      const float band = 0.5f * delta2 * (1.f + 0x1p-9f);
+      const float band60 = band * 0x1p60f;
+      float gm = __int_as_float(0x7f800000), gacc = 0.f;
+      bool close = false;
+      // TMEM loads are short (tens of cycles): one 32-column chunk in flight
+#pragma unroll
+      for (int c = 0; c < tc::NCB / 32; ++c) {
+        uint32_t r[32];
+        ws::ld32_nowait(taddr + c * 32, r);
+        ws::ld_wait();
+        if (c == tc::NCB / 32 - 1) {
+          // every score of this tile is in registers: the slot goes to tile u + 2
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_free[slot])) : "memory");
+        }
+        float cm, cacc;
+        ws::rank_chunk(r, c * 32, band60, cm, cacc);
+        close = close || fabsf(cm - gm) <= band;
+        gacc = cm < gm ? cacc : gacc;
+        gm = fminf(gm, cm);
+      }
+      const int i1 = (int)gacc - 1024;
+      const float v1 = gm;
+      const float quant = __int_as_float((__float_as_int(fabsf(v1)) & 0x7F800000)) * 0x1p-15f;  // 2^8 ulps of v1
+      const bool amb = active && !zero && (close || gacc >= 2048.f);
+      int bj = zero ? zero_idx : i1;
+      unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
+      // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block
+      // at a time — each lane rescores 8 centroids on the CUDA cores (fp32,
+      // error << DELTA) and runs the reference's exact distance on those inside
+      // the band; a lexicographic (distance, index) warp minimum reproduces
+      // "strict <, first index wins" over all 256.  The block comes back from
+      // the group's A buffer (-(hi + lo) == n exactly).
+      while (amb_lanes) {
+        const int src = __ffs(amb_lanes) - 1;
+        amb_lanes &= amb_lanes - 1;
+        const int srow = (row & ~31) + src;
+        float nv[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          float4 hi, lo;
-          float* h = &hi.x;
-          float* l = &lo.x;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float v = -nb[4 * q + e];
-            h[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-            l[e] = __fsub_rn(v, h[e]);
-          }
-          *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
-          *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
+          const float4 hi = *reinterpret_cast<const float4*>(sA + tc::off(srow, 4 * q));
+          const float4 lo = *reinterpret_cast<const float4*>(sA + tc::off(srow, 16 + 4 * q));
+          nv[4 * q] = -__fadd_rn(hi.x, lo.x);
+          nv[4 * q + 1] = -__fadd_rn(hi.y, lo.y);
+          nv[4 * q + 2] = -__fadd_rn(hi.z, lo.z);
+          nv[4 * q + 3] = -__fadd_rn(hi.w, lo.w);
         }
-        srec[b][3 * row + 0] = q8d(mean);
-        srec[b][3 * row + 1] = q8d(__dmul_rn(sd, 4.0));  // sd / 0.25 is exact
-        szero[b][row] = active && zero ? 1 : 0;
-        fence_proxy_async_smem();
-        ws::named_sync(1 + b, 128);
-        if ((tid & 127) == 0) {
-          tc::fence_after();
-          const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-          // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
-          const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
-#pragma unroll
-          for (int m = 0; m < 6; ++m)
-            ws::mma(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
-          // + |c_j|^2/2 + 8: A = [1 1 0 0 | 0...] in every row, B = [hi lo . . | same quarter again]
-          ws::mma(tmem, tc::sdesc(smem_u32(tsm + ws::ABIAS_OFF), 128, 0),
-                  tc::sdesc(smem_u32(tsm + ws::BBIAS_OFF), 0, 128), 1u);
-          tc::commit(&mma_done[b]);
-          // srec / szero of this tile (written by all 128 front threads before
-          // the named barrier) are published to the epilogue group
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fg_done[b])) : "memory");
-        }
-      } else {
-        // --------------------------------------------------------- epilogue
-        mbar_wait(&mma_done[b], uses & 1);
-        mbar_wait(&fg_done[b], uses & 1);
-        tc::fence_after();
-        int m1 = 0x7fffffff, m2 = 0x7fffffff;
-#pragma unroll
-        for (int cq = 0; cq < tc::NCB / 32; cq += 2) {
-          uint32_t r0[32], r1[32];
-          ws::ld32_nowait(taddr + cq * 32, r0);
-          ws::ld32_nowait(taddr + cq * 32 + 32, r1);
-          ws::ld_wait();
-          ws::top2_chunk(m1, m2, r0, cq * 32);
-          ws::top2_chunk(m1, m2, r1, cq * 32 + 32);
-        }
-        const int i1 = m1 & 0xFF;
-        const float v1 = tc::key_value(m1), v2 = tc::key_value(m2);
-        // keys drop the low byte: the true best lies in [v1, v1 + quantum)
-        const float quant = __int_as_float((m2 & 0x7F800000) | 0) * 0x1p-15f;  // 2^8 ulps of the runner-up
-        const bool zero = szero[b][row] != 0;
-        const bool amb = active && !zero && !(v2 - v1 > 0.5f * delta2 + quant);
-        int bj = zero ? zero_idx : i1;
-        unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
-        // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block
-        // at a time — each lane rescores 8 centroids on the CUDA cores (fp32,
-        // error << DELTA) and runs the reference's exact distance on those inside
-        // the band; a lexicographic (distance, index) warp minimum reproduces
-        // "strict <, first index wins" over all 256.  The block comes back from
-        // A_b (-(hi + lo) == n exactly).
-        while (amb_lanes) {
-          const int src = __ffs(amb_lanes) - 1;
-          amb_lanes &= amb_lanes - 1;
-          const int srow = (row & ~31) + src;
-          float nv[16];
+        // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8)
+        const float lim = __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
+        float2 bp[8];
+        vq_pack(nv, bp);
+        float best = VQ_BEST_INIT;
+        int bx = 0x7fffffff;
+#pragma unroll 1
+        for (int j = lane; j < a.ncb; j += 32) {
+          float c[16];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 hi = *reinterpret_cast<const float4*>(sA + tc::off(srow, 4 * q));
-            const float4 lo = *reinterpret_cast<const float4*>(sA + tc::off(srow, 16 + 4 * q));
-            nv[4 * q] = -__fadd_rn(hi.x, lo.x);
-            nv[4 * q + 1] = -__fadd_rn(hi.y, lo.y);
-            nv[4 * q + 2] = -__fadd_rn(hi.z, lo.z);
-            nv[4 * q + 3] = -__fadd_rn(hi.w, lo.w);
+            const float4 hi = *reinterpret_cast<const float4*>(sB + tc::off(j, 4 * q));
+            const float4 lo = *reinterpret_cast<const float4*>(sB + tc::off(j, 16 + 4 * q));
+            c[4 * q] = __fadd_rn(hi.x, lo.x);  // hi + lo == c exactly
+            c[4 * q + 1] = __fadd_rn(hi.y, lo.y);
+            c[4 * q + 2] = __fadd_rn(hi.z, lo.z);
+            c[4 * q + 3] = __fadd_rn(hi.w, lo.w);
           }
-          // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8)
-          const float lim = __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
-          float2 bp[8];
-          vq_pack(nv, bp);
-          float best = VQ_BEST_INIT;
-          int bx = 0x7fffffff;
-#pragma unroll 1
-          for (int j = lane; j < a.ncb; j += 32) {
-            float c[16];
+          float dotv = 0.f;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 hi = *reinterpret_cast<const float4*>(sB + tc::off(j, 4 * q));
-              const float4 lo = *reinterpret_cast<const float4*>(sB + tc::off(j, 16 + 4 * q));
-              c[4 * q] = __fadd_rn(hi.x, lo.x);  // hi + lo == c exactly
-              c[4 * q + 1] = __fadd_rn(hi.y, lo.y);
-              c[4 * q + 2] = __fadd_rn(hi.z, lo.z);
-              c[4 * q + 3] = __fadd_rn(hi.w, lo.w);
-            }
-            float dotv = 0.f;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) dotv = fmaf(nv[i], c[i], dotv);
-            if (fmaf(-2.f, dotv, scn[j]) <= lim) {
-              float2 cp[8];
-              vq_pack(c, cp);
-              const float d = vq_dist_pairs(bp, cp);
-              if (d < best) { best = d; bx = j; }
-            }
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const float od = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oj = __shfl_xor_sync(0xffffffffu, bx, o);
-            if (od < best || (od == best && oj < bx)) { best = od; bx = oj; }
-          }
-          if (lane == src) {
-            bj = bx == 0x7fffffff ? 0 : bx;
-            ++namb;
+          for (int e = 0; e < 16; ++e) dotv = fmaf(nv[e], c[e], dotv);
+          if (fmaf(-2.f, dotv, scn[j]) <= lim) {
+            float2 cp[8];
+            vq_pack(c, cp);
+            const float d = vq_dist_pairs(bp, cp);
+            if (d < best) { best = d; bx = j; }
           }
         }
-        if (active) srec[b][3 * row + 2] = (uint8_t)bj;
-        tc::fence_before();
-        ws::named_sync(3 + b, 128);
-        const int64_t k0 = t * tc::M;
-        const int64_t nrec = (nblocks - k0 < tc::M ? nblocks - k0 : tc::M) * 3;
-        uint8_t* rec = a.records + (img * nblocks + k0) * 3;
-        for (int e = row; e < nrec; e += tc::M) rec[e] = srec[b][e];
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&eg_done[b])) : "memory");
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float od = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bx, o);
+          if (od < best || (od == best && oj < bx)) { best = od; bx = oj; }
+        }
+        if (lane == src) {
+          bj = bx == 0x7fffffff ? 0 : bx;
+          ++namb;
+        }
+      }
+      // every thread writes its own block's record: three byte stores per
+      // warp instruction cover 96 contiguous bytes (interleaved) or 32 per
+      // plane
+      if (active) {
+        const int64_t gk = img * nblocks + k;
+        if (a.idx_plane) {
+          a.mu_plane[gk] = mu;
+          a.sig_plane[gk] = sg;
+          a.idx_plane[gk] = (uint8_t)bj;
+        } else {
+          uint8_t* rec = a.records + gk * 3;
+          rec[0] = mu;
+          rec[1] = sg;
+          rec[2] = (uint8_t)bj;
+        }
       }
     }
-    // every MMA of this image has been waited for by its epilogue group and
-    // every epilogue has finished reading A/B: the codebook may be replaced
+    u0 += (uint32_t)nlocal;
+    // every MMA of this image has been waited for by its group and every
+    // group has finished reading A/B: the codebook may be replaced
     __syncthreads();
   }
   if (ambiguous && namb) atomicAdd(ambiguous, namb);
@@ -880,7 +930,7 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
   // one CTA per SM (all 512 TMEM columns); every CTA takes every image's tiles
   // in a stride of the grid, so a grid larger than one image's tiles idles
   const int64_t ntiles = (nblocks + tc::M - 1) / tc::M;
-  const int64_t want = ntiles < 2 ? 1 : (ntiles + 1) / 2;  // both pipelines of a CTA busy
+  const int64_t want = (ntiles + 3) / 4;  // every group of a CTA busy
   dim3 grid((unsigned)(want < sm_count ? want : sm_count));
   const size_t smem = ws::SMEM;
   switch (channels) {
@@ -1002,10 +1052,11 @@ int dpp_imgc_vqnearest(const float* blk, const float* cbk, int32_t* idx, int64_t
   return DPP_OK;
 }
 
-int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
-                    int64_t image_stride, int64_t batch, const float* codebook, int n_cb,
-                    int64_t codebook_stride, double sigma_min, uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
-                    float* block_grad, float* norm32, void* stream) {
+static int encode_common(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
+                         int64_t image_stride, int64_t batch, const float* codebook, int n_cb,
+                         int64_t codebook_stride, double sigma_min, uint8_t* records, uint8_t* mu_plane,
+                         uint8_t* sig_plane, uint8_t* idx_plane, uint8_t* cb_plane, uint8_t* cr_plane,
+                         float* block_grad, float* norm32, void* stream) {
   if (height % 4 || width % 4 || height < 4 || width < 4)
     return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
                      (long long)height);
@@ -1016,8 +1067,11 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
   if (batch < 0 || batch > 65535) return dpp::fail(DPP_EINVAL, "batch must be in 0..65535");
   if (batch == 0) return DPP_OK;
   if (!(sigma_min > 0.0)) return dpp::fail(DPP_EINVAL, "sigma_min must be > 0");
-  dpp::EncodeArgs a{px, height, width, row_stride, image_stride, codebook, n_cb, codebook_stride, sigma_min,
-                    records, cb_plane, cr_plane, block_grad, norm32, nullptr};
+  if (!px || !codebook || !cb_plane || !cr_plane || (!records && !(mu_plane && sig_plane && idx_plane)))
+    return dpp::fail(DPP_EINVAL, "NULL data pointer");
+  dpp::EncodeArgs a{px,      height,   width,      row_stride, image_stride, codebook, n_cb,
+                    codebook_stride, sigma_min, records,  cb_plane,   cr_plane, block_grad, norm32,
+                    nullptr, mu_plane, sig_plane, idx_plane};
   const int64_t nblocks = (height / 4) * (width / 4);
   auto s = (cudaStream_t)stream;
   if (dpp::vq_mode() == 1) {
@@ -1031,6 +1085,24 @@ int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t wid
     return DPP_OK;
   }
   return dpp::launch_encode_tc(a, channels, batch, nblocks, 1.0f, nullptr, s);
+}
+
+int dpp_imgc_encode(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
+                    int64_t image_stride, int64_t batch, const float* codebook, int n_cb,
+                    int64_t codebook_stride, double sigma_min, uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane,
+                    float* block_grad, float* norm32, void* stream) {
+  return encode_common(px, channels, height, width, row_stride, image_stride, batch, codebook, n_cb, codebook_stride,
+                       sigma_min, records, nullptr, nullptr, nullptr, cb_plane, cr_plane, block_grad, norm32, stream);
+}
+
+int dpp_imgc_encode_planar(const uint8_t* px, int channels, int64_t height, int64_t width, int64_t row_stride,
+                           int64_t image_stride, int64_t batch, const float* codebook, int n_cb,
+                           int64_t codebook_stride, double sigma_min, uint8_t* mu_plane, uint8_t* sig_plane,
+                           uint8_t* idx_plane, uint8_t* cb_plane, uint8_t* cr_plane, void* stream) {
+  if (!mu_plane || !sig_plane || !idx_plane) return dpp::fail(DPP_EINVAL, "NULL record plane");
+  return encode_common(px, channels, height, width, row_stride, image_stride, batch, codebook, n_cb, codebook_stride,
+                       sigma_min, nullptr, mu_plane, sig_plane, idx_plane, cb_plane, cr_plane, nullptr, nullptr,
+                       stream);
 }
 
 // Test hook: the tensor-core encoder with a scaled pruning band and a count of

@@ -175,13 +175,10 @@ class EncodeNode(NativeNode):
         if not shared and cbk.numel() != self.ncb * 16 * batch:
             raise KernelRuntimeError(f"codebook stream holds {cbk.numel() // 16} centroids, node expects "
                                      f"{self.ncb} (shared) or {self.ncb} per frame", work_item=0)
-        rec = torch.empty(items * 3, dtype=torch.uint8, device=cbk.device)
-        ops.encode(inputs["px"], 1, self.height, self.width, cbk, rec, outputs["cb"], outputs["cr"],
-                   batch=batch, shared_codebook=shared, stream=stream)
-        r3 = rec.view(-1, 3)
-        outputs["mu"].copy_(r3[:, 0])
-        outputs["sig"].copy_(r3[:, 1])
-        outputs["idx"].copy_(r3[:, 2])
+        # the record bytes land directly in the mu / sig / idx output planes
+        ops.encode_planar(inputs["px"], self.height, self.width, cbk, outputs["mu"], outputs["sig"],
+                          outputs["idx"], outputs["cb"], outputs["cr"], batch=batch,
+                          shared_codebook=shared, stream=stream)
 
 
 class ToComplexNode(NativeNode):
@@ -250,12 +247,7 @@ def match_fft(node):
         # narrower than a column tile) run the node's own naive-DFT body
         # through the JIT: the document's meaning, on the GPU, just O(N^2)
         from . import ops
-        from .errors import PlanError
-        try:
-            ops.fft_plan(2, r, c, 1)
-        except PlanError:
-            return None
-        return Fft2dNode(r, c)
+        return Fft2dNode(r, c) if ops.fft_shape_supported(2, r, c) else None
     return None
 
 

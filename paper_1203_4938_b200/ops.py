@@ -19,7 +19,7 @@ from ._torch import require_cuda, stream_handle
 from .errors import KernelRuntimeError, PlanError
 
 __all__ = ["FftPlanHandle", "fft_plan", "fft_forward", "fft2d_forward", "leaf_dft",
-           "ycbcr", "boxdown", "gradient", "vqnearest", "encode", "decode", "fft2d_u8_spectrum"]
+           "ycbcr", "boxdown", "gradient", "vqnearest", "encode", "encode_planar", "decode", "fft2d_u8_spectrum"]
 
 
 def _check_cuda(t: torch.Tensor, name: str, dtype: torch.dtype | None = None) -> None:
@@ -77,6 +77,12 @@ class FftPlanHandle:
 
 _plans: dict[tuple, FftPlanHandle] = {}
 _plans_lock = threading.Lock()
+
+
+def fft_shape_supported(rank: int, n0: int, n1: int = 1) -> bool:
+    """Would a plan of this shape be accepted?  Pure shape rules (C ABI
+    dpp_fft_plan_supported): no device, no allocation."""
+    return bool(_lib.load().dpp_fft_plan_supported(rank, n0, n1))
 
 
 def fft_plan(rank: int, n0: int, n1: int, batch: int, device=None) -> FftPlanHandle:
@@ -225,6 +231,30 @@ def encode(px: torch.Tensor, channels: int, height: int, width: int, codebook: t
         codebook.data_ptr(), ncb, 0 if shared_codebook else ncb * 16, float(sigma_min),
         records.data_ptr(), cb_plane.data_ptr(), cr_plane.data_ptr(), _lib.ptr(block_grad),
         _lib.ptr(norm32), stream_handle(stream)), "imgc encode")
+
+
+def encode_planar(px: torch.Tensor, height: int, width: int, codebook: torch.Tensor, mu: torch.Tensor,
+                  sig: torch.Tensor, idx: torch.Tensor, cb_plane: torch.Tensor, cr_plane: torch.Tensor,
+                  channels: int = 1, batch: int = 1, shared_codebook: bool = True, sigma_min: float = 0.25,
+                  stream=None) -> None:
+    """:func:`encode` with the record bytes written as three planes (the graph
+    node's mu / sig / idx outputs) instead of the interleaved record run."""
+    _check_cuda(px, "px", torch.uint8)
+    _check_cuda(codebook, "codebook", torch.float32)
+    blocks = (height // 4) * (width // 4) * batch
+    for name, t in (("mu", mu), ("sig", sig), ("idx", idx), ("cb_plane", cb_plane), ("cr_plane", cr_plane)):
+        _check_cuda(t, name, torch.uint8)
+        if t.numel() < blocks:
+            raise PlanError(f"{name} holds {t.numel()} bytes, need {blocks}")
+    ncb = codebook.numel() // 16 if shared_codebook else codebook.numel() // (16 * batch)
+    image_bytes = height * width * channels
+    if px.numel() < batch * image_bytes:
+        raise PlanError(f"pixel buffer holds {px.numel()} bytes, need {batch * image_bytes}")
+    _lib.check(_lib.load().dpp_imgc_encode_planar(
+        px.data_ptr(), channels, height, width, width * channels, image_bytes, batch,
+        codebook.data_ptr(), ncb, 0 if shared_codebook else ncb * 16, float(sigma_min),
+        mu.data_ptr(), sig.data_ptr(), idx.data_ptr(), cb_plane.data_ptr(), cr_plane.data_ptr(),
+        stream_handle(stream)), "imgc encode (planar)")
 
 
 def rounding_ties(px: torch.Tensor, channels: int, height: int, width: int, batch: int = 1,

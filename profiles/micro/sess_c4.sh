@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_imgc_gpu.py tests/test_chain_gpu.py -x -q -p no:cacheprovider 2>&1 | tail -3
+bash profiles/micro/ab_c4.sh alt/head_imgc.so paper_1203_4938_b200/libdpp_b200.so

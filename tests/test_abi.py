@@ -57,6 +57,25 @@ def test_error_path_without_a_gpu():
     assert lib.dpp_fft_leaf(5, None, None, 0, None) == _lib.DPP_EINVAL
 
 
+def test_plan_shape_query_without_a_gpu():
+    """dpp_fft_plan_supported is pure shape rules: it answers on a CPU-only host."""
+    lib = _lib.load()
+    assert lib.dpp_fft_plan_supported(1, 1 << 16, 1) == 1
+    assert lib.dpp_fft_plan_supported(1, 1 << 30, 1) == 1
+    assert lib.dpp_fft_plan_supported(1, 3, 1) == 0
+    assert lib.dpp_fft_plan_supported(1, 1 << 31, 1) == 0
+    assert lib.dpp_fft_plan_supported(2, 16384, 16384) == 1
+    assert lib.dpp_fft_plan_supported(2, 32768, 32) == 1
+    assert lib.dpp_fft_plan_supported(2, 32768, 8) == 0     # 16-column tiles
+    assert lib.dpp_fft_plan_supported(2, 8192, 8) == 1      # 8-column tiles
+    assert lib.dpp_fft_plan_supported(2, 128, 256) == 0     # columns < 256 rows: JIT body
+    assert lib.dpp_fft_plan_supported(3, 16, 16) == 0
+    from paper_1203_4938_b200.nodes import match_fft
+    from paper_1203_4938_b200.apps.fft import fft2d_kernel
+    assert match_fft(fft2d_kernel(4096, 256)) is not None
+    assert match_fft(fft2d_kernel(128, 256)) is None
+
+
 def _sass_by_function() -> dict[str, list[str]]:
     import subprocess
     out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout

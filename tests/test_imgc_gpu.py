@@ -128,6 +128,33 @@ def test_batched_encode_equals_single(cuda):
         assert np.array_equal(crp[b].cpu().numpy(), f["cr"].ravel())
 
 
+@pytest.mark.parametrize("mode", ["tc", "exact"])
+@pytest.mark.parametrize("shape", [(128, 64), (512, 260), (36, 20)])
+def test_planar_records_equal_interleaved(cuda, monkeypatch, mode, shape):
+    """dpp_imgc_encode_planar (the graph node's mu / sig / idx outputs) writes
+    the same bytes as the interleaved record run, batched, both searches,
+    including frames whose tiles straddle block rows."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    if mode == "exact":
+        monkeypatch.setenv("DPP_IMGC_VQ", "exact")
+    w, h = shape
+    imgs = torch.from_numpy(np.stack([io.synthetic_image(w, h, seed=s)[..., 1] for s in (4, 5)])).cuda()
+    cb = torch.from_numpy(io.train_codebook(io.ycbcr(np.repeat(imgs[0].cpu().numpy()[..., None], 3, 2))[0],
+                                            32, 0)).cuda()
+    nb = (w // 4) * (h // 4) * 2
+    rec = torch.empty(nb * 3, dtype=torch.uint8, device="cuda")
+    cbp, crp = (torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(2))
+    ops.encode(imgs, 1, h, w, cb, rec, cbp, crp, batch=2)
+    planes = [torch.full((nb,), 7, dtype=torch.uint8, device="cuda") for _ in range(5)]
+    ops.encode_planar(imgs, h, w, cb, *planes, batch=2)
+    r3 = rec.view(-1, 3)
+    for i in range(3):
+        assert torch.equal(planes[i], r3[:, i])
+    assert torch.equal(planes[3], cbp) and torch.equal(planes[4], crp)
+
+
 def test_c4_full_size_8192_gray(cuda):
     """C4 at full size: 8192^2 gray (R=G=B).  The oracle (too slow for the whole
     frame) checks the first 64 block rows exactly."""

@@ -104,6 +104,13 @@ def test_single_rank_matches_2d_plan(n0, n1, batch, back):
     (2, 4096, 256, 2, False),
     (2, 16384, 128, 1, True),
     (4, 4096, 256, 1, False),
+    # sub-box layouts of the short rings: one row group per rank (nb = 1),
+    # kk = 256 / P output rows per rank, both output modes
+    (2, 1024, 64, 1, True),
+    (4, 1024, 64, 1, False),
+    (4, 1024, 64, 1, True),
+    (2, 2048, 32, 1, True),
+    (2, 2048, 32, 1, False),
 ])
 def test_ranks_share_one_gpu_bit_exact(world, n0, n1, batch, back):
     full = _input(n0, n1, batch)
