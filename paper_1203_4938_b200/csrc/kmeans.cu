@@ -51,76 +51,119 @@ __global__ void kpp_update(const double* __restrict__ pts, int64_t n, const doub
   }
 }
 
-// single CTA: scan block sums, locate u*total, then the point inside the block
-// (first index whose inclusive prefix exceeds the target: searchsorted 'right')
-__global__ void kpp_pick(const double* __restrict__ d2, int64_t n, const double* __restrict__ block_sums,
-                         int nblocks, int block, double u, const double* __restrict__ pts,
-                         double* __restrict__ centroid, int64_t* __restrict__ pick_out) {
-  __shared__ double total_s;
-  __shared__ int64_t pick_s;
-  if (threadIdx.x == 0) {
-    double total = 0.0;
-    for (int b = 0; b < nblocks; ++b) total += block_sums[b];
-    int64_t pick = -1;
-    if (total <= 0.0) {
-      pick = (int64_t)(u * (double)n);  // degenerate: uniform pick
-      if (pick >= n) pick = n - 1;
-    } else {
-      const double target = u * total;
-      double acc = 0.0;
-      int b = 0;
-      for (; b < nblocks - 1; ++b) {
-        if (acc + block_sums[b] > target) break;
-        acc += block_sums[b];
-      }
-      const int64_t lo = (int64_t)b * block, hi = lo + block < n ? lo + block : n;
-      pick = hi - 1;
-      for (int64_t i = lo; i < hi; ++i) {
-        acc += d2[i];
-        if (acc > target) { pick = i; break; }
-      }
+// k-means++ draw, one CTA of PICK_T threads (log-depth; a single thread walking
+// the 16k block sums of a 4M-point frame took milliseconds per draw):
+//   total = sum of the block sums, target = u * total (or the caller's target);
+//   block = the first whose inclusive prefix exceeds target (else the last),
+//   pick  = the first point of that block whose inclusive prefix exceeds target
+//           (else the block's last point) — numpy's searchsorted(cdf, u, 'right')
+//           as imgc.py:241-248 draws it, over d2 in index order.
+constexpr int PICK_T = 1024;
+
+// inclusive CTA-wide scan of one double per thread; *total = the CTA sum
+__device__ double cta_scan_incl(double v, double* ws, double* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) ws[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double s = lane < nw ? ws[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
     }
-    total_s = total;
-    pick_s = pick;
-    *pick_out = pick;
+    ws[lane] = s;
   }
   __syncthreads();
-  if (threadIdx.x < KD) centroid[threadIdx.x] = pts[pick_s * KD + threadIdx.x];
-  (void)total_s;
+  if (w > 0) v += ws[w - 1];
+  *total = ws[nw - 1];
+  __syncthreads();
+  return v;
 }
 
-// shard-local pick: the point whose inclusive prefix of d2 first exceeds
-// `target` (the global target minus the totals of the ranks before this one)
-__global__ void kpp_pick_target(const double* __restrict__ d2, int64_t n, const double* __restrict__ block_sums,
-                                int nblocks, int block, double target, const double* __restrict__ pts,
-                                double* __restrict__ centroid, int64_t* __restrict__ pick_out) {
+// USE_U: target = u * total (degenerate total <= 0: uniform pick u * n);
+// otherwise `val` is the target itself (shard-local draw)
+template <bool USE_U>
+__global__ void __launch_bounds__(PICK_T) kpp_pick(const double* __restrict__ d2, int64_t n,
+                                                   const double* __restrict__ block_sums, int nblocks, int block,
+                                                   double val, const double* __restrict__ pts,
+                                                   double* __restrict__ centroid, int64_t* __restrict__ pick_out) {
+  __shared__ double ws[32];
+  __shared__ int first_t;
+  __shared__ int blk_s;
   __shared__ int64_t pick_s;
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    int b = 0;
-    for (; b < nblocks - 1; ++b) {
+  __shared__ double acc_s;
+  const int tid = threadIdx.x;
+  const int per = (nblocks + PICK_T - 1) / PICK_T;
+  const int b0 = min(nblocks, tid * per), b1 = min(nblocks, b0 + per);
+  double loc = 0.0;
+  for (int b = b0; b < b1; ++b) loc += block_sums[b];
+  double total;
+  const double incl = cta_scan_incl(loc, ws, &total);
+  if (tid == 0) {
+    first_t = PICK_T;
+    pick_s = -1;
+  }
+  __syncthreads();
+  double target = val;
+  if (USE_U) {
+    if (total <= 0.0) {
+      if (tid == 0) {
+        int64_t pk = (int64_t)(val * (double)n);
+        pick_s = pk < n ? pk : n - 1;
+      }
+      __syncthreads();
+      goto copy;
+    }
+    target = val * total;
+  }
+  // the first block whose prefix exceeds target lies in the first such thread's range
+  if (b1 > b0 && (incl > target || b1 == nblocks)) atomicMin(&first_t, tid);
+  __syncthreads();
+  if (tid == first_t) {
+    double acc = incl - loc;
+    int b = b0;
+    for (; b < b1 - 1; ++b) {
       if (acc + block_sums[b] > target) break;
       acc += block_sums[b];
     }
-    const int64_t lo = (int64_t)b * block, hi = lo + block < n ? lo + block : n;
-    int64_t pick = hi - 1;
-    for (int64_t i = lo; i < hi; ++i) {
-      acc += d2[i];
-      if (acc > target) { pick = i; break; }
-    }
-    pick_s = pick;
-    *pick_out = pick;
+    blk_s = b;
+    acc_s = acc;
   }
   __syncthreads();
-  if (threadIdx.x < KD) centroid[threadIdx.x] = pts[pick_s * KD + threadIdx.x];
+  {
+    const int64_t lo = (int64_t)blk_s * block, hi = lo + block < n ? lo + block : n;
+    const double v = tid < hi - lo ? d2[lo + tid] : 0.0;
+    double unused;
+    const double pin = acc_s + cta_scan_incl(v, ws, &unused);
+    if (tid == 0) first_t = PICK_T;
+    __syncthreads();
+    if (tid < hi - lo && pin > target) atomicMin(&first_t, tid);
+    __syncthreads();
+    if (tid == 0) pick_s = first_t < PICK_T ? lo + first_t : hi - 1;
+    __syncthreads();
+  }
+copy:
+  if (tid == 0) *pick_out = pick_s;
+  if (tid < KD) centroid[tid] = pts[pick_s * KD + tid];
 }
 
-// sequential (block-order) total of the block sums, as kpp_pick forms it
-__global__ void kpp_total(const double* __restrict__ block_sums, int nblocks, double* __restrict__ total) {
-  if (threadIdx.x != 0) return;
-  double t = 0.0;
-  for (int b = 0; b < nblocks; ++b) t += block_sums[b];
-  *total = t;
+// total of the block sums (the shard's d2 total for the all-reduce)
+__global__ void __launch_bounds__(PICK_T) kpp_total(const double* __restrict__ block_sums, int nblocks,
+                                                    double* __restrict__ total) {
+  __shared__ double ws[32];
+  const int per = (nblocks + PICK_T - 1) / PICK_T;
+  const int b0 = min(nblocks, (int)threadIdx.x * per), b1 = min(nblocks, b0 + per);
+  double loc = 0.0;
+  for (int b = b0; b < b1; ++b) loc += block_sums[b];
+  double t;
+  cta_scan_incl(loc, ws, &t);
+  if (threadIdx.x == 0) *total = t;
 }
 
 // shard accumulator for the all-reduce: [k*16 sums][k counts][changed][sse] in binary64
@@ -268,7 +311,7 @@ int dpp_kmeans_shard_seed(dpp_kmeans_shard* shard, const double* centroid, int f
     return DPP_OK;
   }
   kpp_update<<<m.nb, 256, 0, m.s>>>(m.pts, m.n, centroid, m.d2, m.bsum, first);
-  kpp_total<<<1, 32, 0, m.s>>>(m.bsum, m.nb, m.total);
+  kpp_total<<<1, PICK_T, 0, m.s>>>(m.bsum, m.nb, m.total);
   DPP_LAUNCH_CHECK("k-means++ shard update");
   DPP_CUDA_CHECK(cudaMemcpyAsync(total, m.total, sizeof(double), cudaMemcpyDeviceToHost, m.s));
   DPP_CUDA_CHECK(cudaStreamSynchronize(m.s));
@@ -291,7 +334,7 @@ int dpp_kmeans_shard_pick(dpp_kmeans_shard* shard, double target, int64_t local_
     *picked = local_index;
     return DPP_OK;
   }
-  kpp_pick_target<<<1, 32, 0, m.s>>>(m.d2, m.n, m.bsum, m.nb, 256, target, m.pts, centroid_out, m.pick);
+  kpp_pick<false><<<1, PICK_T, 0, m.s>>>(m.d2, m.n, m.bsum, m.nb, 256, target, m.pts, centroid_out, m.pick);
   DPP_LAUNCH_CHECK("k-means++ shard pick");
   DPP_CUDA_CHECK(cudaMemcpyAsync(picked, m.pick, sizeof(int64_t), cudaMemcpyDeviceToHost, m.s));
   DPP_CUDA_CHECK(cudaStreamSynchronize(m.s));
@@ -397,7 +440,7 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   DPP_CUDA_CHECK(cudaMemcpyAsync(cents, pts + first_pick * KD, KD * sizeof(double), cudaMemcpyDeviceToDevice, s));
   for (int j = 1; j < k; ++j) {
     kpp_update<<<nb, T, 0, s>>>(pts, n, cents + (j - 1) * KD, d2, bsum, j == 1);
-    kpp_pick<<<1, 32, 0, s>>>(d2, n, bsum, nb, T, uniforms[j - 1], pts, cents + j * KD, pick);
+    kpp_pick<true><<<1, PICK_T, 0, s>>>(d2, n, bsum, nb, T, uniforms[j - 1], pts, cents + j * KD, pick);
   }
   DPP_LAUNCH_CHECK("k-means++ seeding");
 
