@@ -54,3 +54,22 @@ def to_device(values: np.ndarray, device="cuda", pinned: bool = True) -> torch.T
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
+
+
+class nvtx_range:
+    """NVTX range around host-side launch code (SURVEY §5 tracing): visible in
+    nsys / ncu --nvtx timelines as ``dpp:<name>``; a no-op cost when no tool
+    is attached (one C call each way)."""
+
+    __slots__ = ("name",)
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push("dpp:" + self.name)
+        return self
+
+    def __exit__(self, *exc):
+        torch.cuda.nvtx.range_pop()
+        return False

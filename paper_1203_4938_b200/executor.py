@@ -34,7 +34,7 @@ from .errors import EngineRuntimeError, KernelRuntimeError, PlanError
 from .model import FreePoint, Program, as_program, free_points, program_id, topological_order, validate
 from .nodes import NativeNode, resolve
 from .types import Direction
-from ._torch import require_cuda, torch_dtype
+from ._torch import nvtx_range, require_cuda, torch_dtype
 
 __all__ = ["DEFAULT_CHUNK_SIZE", "ExecutionPlan", "Chunk", "RunResult", "plan", "run_chunk",
            "run_stream", "chunk_arrays"]
@@ -252,7 +252,8 @@ def _run_one(p: ExecutionPlan, iid: int, chunk: Chunk, elements: int, produced: 
         if items:
             native.check_items(items)
             _jit().set_site(iid, chunk.index)
-            native.launch(items, inputs, outputs, stream)
+            with nvtx_range(f"{native.kind}[{iid}]"):
+                native.launch(items, inputs, outputs, stream)
     except KernelRuntimeError as exc:
         raise EngineRuntimeError(str(exc), instance=iid, work_item=exc.work_item,
                                  chunk=chunk.index) from exc
@@ -342,7 +343,8 @@ def run_stream(p: ExecutionPlan, chunks: Iterable[Chunk], writer: Callable[[Chun
             start = torch.cuda.Event(enable_timing=True)
             stop = torch.cuda.Event(enable_timing=True)
             start.record(s)
-            out = run_chunk(p, chunk, s)
+            with nvtx_range(f"chunk {chunk.index}"):
+                out = run_chunk(p, chunk, s)
             stop.record(s)
             result.events.append((start, stop))
             result.total_work_items += int(per_element * elements)
