@@ -733,7 +733,8 @@ def run_ours(args) -> None:
 
             def step1d():
                 ops.fft_forward(part, n1d, out=out1)
-            how = "local: transpose + 16384-point rows + twiddled 16384-point column ring (3 HBM passes)"
+            how = ("local, two HBM passes: 16384-point column ring with transposed output, twiddled 16384-point "
+                   "column ring")
         else:
             from paper_1203_4938_b200.distributed import fft1d_row_sharded
 
@@ -752,7 +753,10 @@ def run_ours(args) -> None:
                       "roofline": {"bound": "hbm" if world == 1 else "nvlink",
                                    "compulsory_bytes_per_gpu": 16 * n1d / world,
                                    "frac_of_compulsory": round(16 * n1d / world / (ms1 / 1e3) / 1e9 / pk["hbm_gbs"],
-                                                               4)}})
+                                                               4),
+                                   "two_pass_bytes_per_gpu": 32 * n1d / world,
+                                   "frac_of_two_pass": round(32 * n1d / world / (ms1 / 1e3) / 1e9 / pk["hbm_gbs"],
+                                                             4)}})
         part = out1 = step1d = None
     except Exception as exc:
         fft1d["error"] = f"{type(exc).__name__}: {exc}"[:300]

@@ -74,6 +74,11 @@ void fft_plan_release(FftPlan* p) {
     delete p->rows;
     p->rows = nullptr;
   }
+  if (p->xcols) {
+    fft_plan_release(p->xcols);
+    delete p->xcols;
+    p->xcols = nullptr;
+  }
   if (p->cols) {
     fft_plan_release(p->cols);
     delete p->cols;

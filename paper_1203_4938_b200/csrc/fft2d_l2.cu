@@ -81,8 +81,15 @@ struct MapSet<true> {
 __device__ __forceinline__ const CUtensorMap* map_at(const CUtensorMap& m, int) { return &m; }
 __device__ __forceinline__ const CUtensorMap* map_at(const Maps8& m, int j) { return &m.m[j]; }
 
+// XP (the first pass of the two-pass large 1-D transform, csrc/fft_large.cu):
+// the ring slot is laid out S[column][k1 / 16][a][k1 % 16] instead of
+// S[k1][a][column], so a P2 block is one column's 16 consecutive k1 over all
+// a, and its output (16 k1 x 256 k2 of ONE column) is a 128-byte-row box of
+// the transposed result T[column][k1 + B k2]: (col, a, k1) sits at
+// 4096 (col B/16 + k1/16) + swz(a, k1 % 16) of the slot.
+
 // P1, B = 16: thread = one (column, a) sequence over b; no exchange
-template <bool TW = false>
+template <bool TW = false, bool XP = false>
 __device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
                                        const Args& a, uint64_t keep_pol, int colbase = 0) {
   const int col = lane & 15, alo = 2 * warp + (lane >> 4);
@@ -101,9 +108,21 @@ __device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, in
     v[k1] = cmul(v[k1], w);
     w = cmul(w, wa);
   }
-  float2* dst = slot + swz(ar, col);
+  if constexpr (XP) {
+    // one 128-byte row: k1 = 0..15 of (col, a), four whole 32-byte sectors;
+    // k1 = 4 g .. 4 g + 3 lands in sector g ^ ((a & 7) >> 1), chunk pair
+    // swapped when a is odd (the 128B swizzle)
+    float2* dst = slot + 4096 * col + 16 * ar;
+    const bool odd = ar & 1;
 #pragma unroll
-  for (int k1 = 0; k1 < 16; ++k1) st_l2_hint(dst + 4096 * k1, v[k1], keep_pol);
+    for (int g4 = 0; g4 < 4; ++g4)
+      st_l2_hint4(dst + 4 * (g4 ^ ((ar & 7) >> 1)), odd ? v[4 * g4 + 2] : v[4 * g4], odd ? v[4 * g4 + 3] : v[4 * g4 + 1],
+                  odd ? v[4 * g4] : v[4 * g4 + 2], odd ? v[4 * g4 + 1] : v[4 * g4 + 3], keep_pol);
+  } else {
+    float2* dst = slot + swz(ar, col);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) st_l2_hint(dst + 4096 * k1, v[k1], keep_pol);
+  }
 }
 
 // P1, B = 64: four lanes per (column, a) sequence; b = 4 b1 + b0 with b1 in
@@ -113,7 +132,7 @@ __device__ __forceinline__ void p1_b16(float2 (&v)[16], uint32_t b, int warp, in
 // = 16 distinct bank pairs.
 __device__ __forceinline__ int gbeta(int m0) { return (m0 << 2) | ((m0 >> 2) & 1); }
 
-template <bool TW = false>
+template <bool TW = false, bool XP = false>
 __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
                                        const Args& a, uint64_t keep_pol, int colbase = 0) {
   const int alo = warp >> 1, col = 8 * (warp & 1) + (lane & 7), b0 = lane >> 3;
@@ -149,15 +168,39 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
   const float2 s1 = __ldg(a.twr + ar), s16 = __ldg(a.twr + 16 * ar);
   float2 wi = __ldg(a.twr + 4 * ar * j);
   float2* base = slot + swz(ar, col);
+  if constexpr (XP) {
+    // k1 = 4 j + i + 16 m1: this lane holds k1 % 16 = 4 j .. 4 j + 3 of every
+    // m1 — one whole 32-byte sector of row (col, m1, a): sector j ^ ((a & 7)
+    // >> 1), chunk pair swapped when a is odd
+    float2 wv[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 w = wi;
+    for (int i = 0; i < 4; ++i) {
+      wv[i] = wi;
+      wi = cmul(wi, s1);
+    }
+    const bool odd = ar & 1;
 #pragma unroll
     for (int m1 = 0; m1 < 4; ++m1) {
-      st_l2_hint(base + 4096 * (4 * j + i + 16 * m1), cmul(v[4 * i + m1], w), keep_pol);
-      w = cmul(w, s16);
+      float2 e[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        e[i] = cmul(v[4 * i + m1], wv[i]);
+        wv[i] = cmul(wv[i], s16);
+      }
+      st_l2_hint4(slot + 4096 * (4 * col + m1) + 16 * ar + 4 * (j ^ ((ar & 7) >> 1)), odd ? e[2] : e[0],
+                  odd ? e[3] : e[1], odd ? e[0] : e[2], odd ? e[1] : e[3], keep_pol);
     }
-    wi = cmul(wi, s1);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 w = wi;
+#pragma unroll
+      for (int m1 = 0; m1 < 4; ++m1) {
+        st_l2_hint(base + 4096 * (4 * j + i + 16 * m1), cmul(v[4 * i + m1], w), keep_pol);
+        w = cmul(w, s16);
+      }
+      wi = cmul(wi, s1);
+    }
   }
 }
 
@@ -288,7 +331,7 @@ __device__ __forceinline__ void p1_bL(float2 (&v)[16], uint32_t b, int warp, int
 // the 256 output rows of its k1 as P sub-boxes into the ranks' row slabs
 // (tb: natural row-sharded output, in place is safe because column block q is
 // touched by rank q only) or one box into the local R x (C/P) column slab.
-template <int B, bool DISCARD, bool SPEC = false, bool PEER = false, bool TW = false>
+template <int B, bool DISCARD, bool SPEC = false, bool PEER = false, bool TW = false, bool XP = false>
 __global__ void __launch_bounds__(THREADS, 3)
 fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
              const __grid_constant__ typename MapSet<PEER>::type tout, const Args a) {
@@ -336,6 +379,10 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
           } else {
             tma_store_3d(map_at(tout, 0), 16 * ct, g, img * 256, smem + s * TILE);
           }
+        } else if constexpr (XP) {
+          // P2 block g = (column, k1 / 16): row img C + 16 ct + column of T, viewed [k2][k1]
+          const int C = 16 * a.tiles_per_image;
+          tma_store_3d(&tout, 16 * (g % (B / 16)), 0, img * C + 16 * ct + g / (B / 16), smem + s * TILE);
         } else {
           tma_store_3d(&tout, 16 * ct, g, img * 256,
                        SPEC ? reinterpret_cast<const void*>(reinterpret_cast<const uint8_t*>(smem + S * TILE) +
@@ -428,10 +475,10 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
     if (pass == 1) {
       const int colbase = TW ? 16 * (u - (u / a.tiles_per_image) * a.tiles_per_image) : 0;
       if constexpr (B == 16)
-        p1_b16<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
+        p1_b16<TW, XP>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
       else
         if constexpr (B == 64)
-          p1_b64<TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
+          p1_b64<TW, XP>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
         else if constexpr (B < 16)
           p1_bsmall<B>(v, b, warp, lane, g, slot, a, keep_pol);
         else
@@ -497,6 +544,8 @@ static int colring_prepare(int* ctas) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, false, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   int per_sm = 0, dev = 0, sms = 0;
   DPP_CUDA_CHECK(
@@ -555,7 +604,7 @@ int fft2d_colring_init(FftPlan* p) {
 
 // spec_out != nullptr: fused spectrum_u8 — the column pass writes u8 spectra there
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s, uint8_t* spec_out,
-                          float alpha, float2* dst, const float2* twlo, const float2* twhi) {
+                          float alpha, float2* dst, const float2* twlo, const float2* twhi, bool xp) {
   if (!dst) dst = data;
   const int64_t R = p->n0, C = p->n1;
   const int B = (int)(R / 256);
@@ -568,7 +617,16 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
     const uint32_t box[3] = {16, (uint32_t)(colring::TILE / (16 * B)), (uint32_t)B};
     if (int rc = make_tmap_c64_3d(&tin, data, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
   }
-  if (spec_out) {
+  if (xp) {
+    // transposed output T (C rows of R = 256 B per image), a row viewed [k2][k1]
+    if (spec_out || twlo || (B != 16 && B != 64))
+      return fail(DPP_ENOTSUP, "transposed column pass needs 4096 or 16384 rows, no fused epilogue");
+    if (dst == data) return fail(DPP_EINVAL, "transposed column pass cannot run in place");
+    const uint64_t dims[3] = {(uint64_t)B, 256, (uint64_t)C * batch};
+    const uint64_t strides[2] = {(uint64_t)B * 8, (uint64_t)R * 8};
+    const uint32_t box[3] = {16, 256, 1};
+    if (int rc = make_tmap_c64_3d(&tout, dst, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  } else if (spec_out) {
     const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch)};
     const uint64_t strides[2] = {(uint64_t)C, (uint64_t)C * B};
     const uint32_t box[3] = {16, 1, 256};
@@ -600,7 +658,12 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   const size_t smem = colring_smem(spec_out != nullptr);
   if ((twlo || spec_out) && B != 16 && B != 64)
     return fail(DPP_ENOTSUP, "fused spectrum / twiddled column pass needs 4096 or 16384 rows");
-  if (twlo) {
+  if (xp) {
+    if (B == 16)
+      colring::fft_cols_l2w<16, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    else
+      colring::fft_cols_l2w<64, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+  } else if (twlo) {
     if (B == 16)
       colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
     else

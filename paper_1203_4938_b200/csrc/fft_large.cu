@@ -11,6 +11,13 @@
 //    X[A k2 .. A k2 + A) — natural order, no second transpose.
 // Three HBM passes (48 B per point) against the 16 B compulsory; the two
 // FFT passes are the tuned kernels, the transpose is a 32 x 32 tile copy.
+//
+// Two passes (32 B per point) when A and Bc are both 4096 or 16384 (n = 2^24,
+// 2^26, 2^28): steps 1 + 2 become ONE column ring over the A x Bc view of x
+// (A-point FFTs down its Bc columns) whose ring slot is laid out per column,
+// so each P2 block writes 16 consecutive k1 of one row of T by a TMA box
+// (fft2d_l2.cu, XP) — the transpose rides on the exchange that the column
+// FFT does anyway.
 #include <cmath>
 #include <vector>
 
@@ -81,13 +88,26 @@ int fft_large_init(FftPlan* p) {
   // in-place calls go through a scratch of big_chunk transforms (<= 256 MB, or one transform)
   const int64_t per = (1LL << 25) / n > 1 ? (1LL << 25) / n : 1;
   p->big_chunk = p->batch < per ? (p->batch > 0 ? p->batch : 1) : per;
-  p->rows = new FftPlan();
-  p->rows->rank = 1;
-  p->rows->n0 = a;
-  p->rows->n1 = 1;
-  p->rows->batch = (p->batch > 0 ? p->batch : 1) * bc;
-  p->rows->device = p->device;
-  if (int rc = fft1d_plan_init(p->rows)) return rc;
+  const bool two_pass = (a == 4096 || a == 16384) && (bc == 4096 || bc == 16384);
+  if (two_pass) {
+    p->xcols = new FftPlan();
+    p->xcols->rank = 2;
+    p->xcols->n0 = a;
+    p->xcols->n1 = bc;
+    p->xcols->batch = p->batch > 0 ? p->batch : 1;
+    p->xcols->device = p->device;
+    if (int rc = fft2d_colring_init(p->xcols))
+      return rc == DPP_ENOTSUP ? fail(rc, "no column ring for %lld x %lld", (long long)a, (long long)bc) : rc;
+  }
+  if (!two_pass) {
+    p->rows = new FftPlan();
+    p->rows->rank = 1;
+    p->rows->n0 = a;
+    p->rows->n1 = 1;
+    p->rows->batch = (p->batch > 0 ? p->batch : 1) * bc;
+    p->rows->device = p->device;
+    if (int rc = fft1d_plan_init(p->rows)) return rc;
+  }
   p->cols = new FftPlan();
   p->cols->rank = 2;
   p->cols->n0 = bc;
@@ -108,9 +128,15 @@ int fft_large_init(FftPlan* p) {
   }
   DPP_CUDA_CHECK(cudaMalloc(&p->big_tw, tw.size() * sizeof(float2)));
   DPP_CUDA_CHECK(cudaMemcpy(p->big_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  snprintf(p->desc, sizeof(p->desc),
-           "%lld x %lld four-step: transpose, %lld-point rows (%.120s), twiddled %lld-point column ring",
-           (long long)a, (long long)bc, (long long)a, p->rows->desc, (long long)bc);
+  if (two_pass)
+    snprintf(p->desc, sizeof(p->desc),
+             "%lld x %lld four-step in two passes: %lld-point column ring with transposed output, twiddled "
+             "%lld-point column ring",
+             (long long)a, (long long)bc, (long long)a, (long long)bc);
+  else
+    snprintf(p->desc, sizeof(p->desc),
+             "%lld x %lld four-step: transpose, %lld-point rows (%.120s), twiddled %lld-point column ring",
+             (long long)a, (long long)bc, (long long)a, p->rows->desc, (long long)bc);
   return DPP_OK;
 }
 
@@ -130,6 +156,13 @@ int fft_large_execute(const FftPlan* p, const float2* in, float2* out, int64_t b
     const float2* src = in + b0 * n;
     float2* dst = out + b0 * n;
     float2* t = inplace ? p->big_scratch : dst;
+    if (p->xcols) {
+      if (int rc = fft2d_colring_execute(p->xcols, const_cast<float2*>(src), nb, s, nullptr, 0.f, t, nullptr, nullptr,
+                                         true))
+        return rc;
+      if (int rc = fft2d_colring_execute(p->cols, t, nb, s, nullptr, 0.f, dst, twlo, twhi)) return rc;
+      continue;
+    }
     transpose_c64<<<dim3((unsigned)(bc / 32), (unsigned)(a / 32), (unsigned)nb), dim3(32, 8), 0, s>>>(src, t, a, bc);
     DPP_LAUNCH_CHECK("transpose_c64");
     if (int rc = fft1d_execute(p->rows, t, t, nb * bc, s)) return rc;

@@ -46,6 +46,9 @@ struct FftPlan {
   int ring128k = 0;
   // rank 1, n > 2^17 (fft_large.cu): transpose, row pass (rows), twiddled column ring (cols)
   FftPlan* cols = nullptr;
+  // two-pass schedule (n = A x Bc, both 4096 or 16384): xcols = A-point column
+  // ring with transposed output (replaces transpose + row pass)
+  FftPlan* xcols = nullptr;
   float2* big_tw = nullptr;       // W_N^m, m < 16384, then W_N^(16384 h)
   float2* big_scratch = nullptr;  // in-place calls: big_chunk transforms at a time
   int64_t big_chunk = 0;
@@ -64,7 +67,7 @@ int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_
 int fft2d_colring_init(FftPlan* p);
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s,
                           uint8_t* spec_out = nullptr, float alpha = 0.f, float2* dst = nullptr,
-                          const float2* twlo = nullptr, const float2* twhi = nullptr);
+                          const float2* twlo = nullptr, const float2* twhi = nullptr, bool xp = false);
 int fft_large_init(FftPlan* p);
 int fft_twiddle_slab(float2* data, int64_t rows, int64_t cols, int64_t c0, int64_t n, cudaStream_t s);
 int fft_large_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);

@@ -213,6 +213,13 @@ __device__ __forceinline__ void st_l2_hint(float2* p, float2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
 }
 
+// one 32-byte sector: four complex values (32-byte aligned; STG.256 on sm_100)
+__device__ __forceinline__ void st_l2_hint4(float2* p, float2 a, float2 b, float2 c, float2 d, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "f"(a.x),
+               "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y), "f"(d.x), "f"(d.y), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int x, int y) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(x), "r"(y)
                : "memory");

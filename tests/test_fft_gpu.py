@@ -335,15 +335,49 @@ def test_2d_column_pass_variants(cuda, env):
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-5
 
 
-@pytest.mark.parametrize("m,batch", [(18, 4), (19, 2), (20, 2), (22, 1), (25, 1)])
+@pytest.mark.parametrize("m,batch", [(18, 4), (19, 2), (20, 2), (22, 1), (24, 2), (25, 1)])
 def test_sizes_above_2e17_vs_oracle(cuda, m, batch):
     """n > 2^17: transpose + row pass + twiddled column ring (csrc/fft_large.cu);
-    2^25 takes the 16384-row column ring."""
+    2^25 takes the 16384-row column ring; 2^24 runs in two passes (column
+    ring with transposed output, then the twiddled column ring)."""
     n = 1 << m
     x = complex_signals(300 + m, (batch, n))
     got = _fft(x, n, cuda)
     errs = [rel_l2(g, r) for g, r in zip(got, fo.fft_rows(x))]
     assert max(errs) <= tol(n), (n, max(errs))
+
+
+@pytest.mark.parametrize("m", [26, 28])
+def test_two_pass_large_sizes_vs_numpy_f64(cuda, m):
+    """2^26 (4096 x 16384) and 2^28 (16384 x 16384): the two-pass schedule
+    against numpy's binary64 FFT of the same signal (the oracle port would
+    take minutes here; it is pinned to numpy at smaller sizes)."""
+    import numpy as np
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    n = 1 << m
+    assert "two passes" in ops.fft_plan(1, n, 1, 1, cuda).description
+    gen = torch.Generator(device=cuda).manual_seed(m)
+    x = torch.randn(n, dtype=torch.complex64, device=cuda, generator=gen)
+    y = ops.fft_forward(x, n).cpu().numpy()
+    ref = np.fft.fft(x.cpu().numpy().astype(np.complex128))
+    assert rel_l2(y, ref) <= tol(n)
+
+
+def test_two_pass_in_place_matches_out_of_place(cuda):
+    """In place, pass 1 writes the plan's scratch (two 2^24 transforms per
+    chunk); three transforms cross a chunk boundary."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    n, batch = 1 << 24, 3
+    gen = torch.Generator(device=cuda).manual_seed(7)
+    x = torch.randn((batch, n), dtype=torch.complex64, device=cuda, generator=gen)
+    ref = ops.fft_forward(x, n)
+    y = x.clone()
+    ops.fft_forward(y, n, out=y)
+    assert torch.equal(y, ref)
 
 
 def test_large_in_place_chunks_match_out_of_place(cuda):
