@@ -175,6 +175,7 @@ class _Replay:
     def __init__(self, p, names, sizes):
         import torch
 
+        from . import ops
         from ._torch import torch_dtype
         from .executor import Chunk, run_chunk
 
@@ -194,12 +195,13 @@ class _Replay:
                                                pin_memory=True) for fp in p.free_outputs}
             self.stream.synchronize()
             self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph, stream=self.stream):
+            with torch.cuda.graph(self.graph, stream=self.stream), ops.pin_plans() as pins:
                 for n in names:
                     dbuf[n].copy_(self.stage[n], non_blocking=True)
                 out = run_chunk(p, Chunk(0, dbuf, counts), self.stream)
                 for fp in p.free_outputs:
                     self.out[fp.stream].copy_(out.buffers[fp.stream], non_blocking=True)
+            self.plans = pins  # native plans (tables, scratch) the graph's kernels use
         self.dbuf = dbuf
         self.out_np = {n: t.numpy() for n, t in self.out.items()}
         self.datas = {fp.stream: fp.data for fp in p.free_outputs}

@@ -85,6 +85,25 @@ def fft_shape_supported(rank: int, n0: int, n1: int = 1) -> bool:
     return bool(_lib.load().dpp_fft_plan_supported(rank, n0, n1))
 
 
+_pin = threading.local()
+
+
+class pin_plans:
+    """Collect every plan handed out in this thread while active: a CUDA graph
+    captured meanwhile (client._Replay) bakes the plans' tables and scratch
+    into its kernel nodes, so it keeps them alive even after the cache
+    replaces a plan with a larger one."""
+
+    def __enter__(self) -> list:
+        self.prev = getattr(_pin, "plans", None)
+        _pin.plans = []
+        return _pin.plans
+
+    def __exit__(self, *exc):
+        _pin.plans = self.prev
+        return False
+
+
 def fft_plan(rank: int, n0: int, n1: int, batch: int, device=None) -> FftPlanHandle:
     """Cached plan with capacity >= batch (grown geometrically)."""
     dev = require_cuda(device)
@@ -97,6 +116,9 @@ def fft_plan(rank: int, n0: int, n1: int, batch: int, device=None) -> FftPlanHan
             cap = max(batch, 2 * p.batch if p is not None else batch, 1)
             p = FftPlanHandle(rank, n0, n1 if rank == 2 else 1, cap, dev)
             _plans[key] = p
+    pins = getattr(_pin, "plans", None)
+    if pins is not None:
+        pins.append(p)
     return p
 
 

@@ -65,3 +65,26 @@ def test_jit_graph_takes_the_stream_path(cuda):
     out = run(None, prog, {"0.z": StreamFile(DataType("float", 2), z)})
     assert np.array_equal(out["2.z"].values, z[0::2] + z[1::2] * np.float32(65536.0))
     assert {k: v for k, v in client._replays.items() if k not in before} == {}
+
+
+def test_replay_survives_plan_replacement(cuda, monkeypatch):
+    """A larger batch replaces the cached 1024-point plan; the captured graph
+    keeps the plan it was built with (its twiddle tables) alive."""
+    import gc
+
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    from paper_1203_4938_b200.apps import fft as afft
+    x = complex_signals(21, 1024)
+    first = afft.fft(x)
+    big = torch.from_numpy(complex_signals(22, (4096, 1024))).to(cuda)
+    ops.fft_forward(big, 1024)
+    del big
+    gc.collect()
+    torch.cuda.empty_cache()
+    torch.randn(1 << 24, device=cuda).mul_(3.0)  # reuse freed device memory
+    again = afft.fft(x)
+    assert np.array_equal(first, again)
+    _stream_path(monkeypatch)
+    assert np.array_equal(afft.fft(x), again)
