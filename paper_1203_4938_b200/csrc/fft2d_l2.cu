@@ -271,7 +271,7 @@ __device__ __forceinline__ void dftLc(float2* v) {
     for (int q = 0; q < 8; ++q) v[q] = t[q];
   }
 }
-template <int L>
+template <int L, bool XP = false>
 __device__ __forceinline__ void p1_bL(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
                                       const Args& a, uint64_t keep_pol) {
   constexpr int A = 16 / L, Q = 16 / L;  // a values per item (A * L = 16), m0 values per lane
@@ -307,16 +307,47 @@ __device__ __forceinline__ void p1_bL(float2 (&v)[16], uint32_t b, int warp, int
   const int ar = A * g + alo;
   const float2 s1 = __ldg(a.twr + ar), s16 = __ldg(a.twr + 16 * ar);
   float2 wi = __ldg(a.twr + Q * ar * j);
-  float2* base = slot + swz(ar, col);
+  if constexpr (XP) {
+    // this lane holds k1 % 16 = Q j .. Q j + Q - 1 of every m1: whole 32-byte
+    // sectors (Q = 8: two) or one 16-byte chunk (Q = 2) of row (col, m1, a)
+    float2 wv[Q];
 #pragma unroll
-  for (int ii = 0; ii < Q; ++ii) {
-    float2 w = wi;
+    for (int ii = 0; ii < Q; ++ii) {
+      wv[ii] = wi;
+      wi = cmul(wi, s1);
+    }
+    const bool odd = ar & 1;
 #pragma unroll
     for (int m1 = 0; m1 < L; ++m1) {
-      st_l2_hint(base + 4096 * (Q * j + ii + 16 * m1), cmul(v[L * ii + m1], w), keep_pol);
-      w = cmul(w, s16);
+      float2 e[Q];
+#pragma unroll
+      for (int ii = 0; ii < Q; ++ii) {
+        e[ii] = cmul(v[L * ii + m1], wv[ii]);
+        wv[ii] = cmul(wv[ii], s16);
+      }
+      float2* row = slot + 4096 * (col * L + m1) + 16 * ar;
+      if constexpr (Q >= 4) {
+#pragma unroll
+        for (int h = 0; h < Q / 4; ++h)
+          st_l2_hint4(row + 4 * ((Q * j / 4 + h) ^ ((ar & 7) >> 1)), odd ? e[4 * h + 2] : e[4 * h],
+                      odd ? e[4 * h + 3] : e[4 * h + 1], odd ? e[4 * h] : e[4 * h + 2],
+                      odd ? e[4 * h + 1] : e[4 * h + 3], keep_pol);
+      } else {
+        st_l2_hint2(row + 2 * (j ^ (ar & 7)), e[0], e[1], keep_pol);
+      }
     }
-    wi = cmul(wi, s1);
+  } else {
+    float2* base = slot + swz(ar, col);
+#pragma unroll
+    for (int ii = 0; ii < Q; ++ii) {
+      float2 w = wi;
+#pragma unroll
+      for (int m1 = 0; m1 < L; ++m1) {
+        st_l2_hint(base + 4096 * (Q * j + ii + 16 * m1), cmul(v[L * ii + m1], w), keep_pol);
+        w = cmul(w, s16);
+      }
+      wi = cmul(wi, s1);
+    }
   }
 }
 
@@ -482,7 +513,7 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
         else if constexpr (B < 16)
           p1_bsmall<B>(v, b, warp, lane, g, slot, a, keep_pol);
         else
-          p1_bL<B / 16>(v, b, warp, lane, g, slot, a, keep_pol);
+          p1_bL<B / 16, XP>(v, b, warp, lane, g, slot, a, keep_pol);
     } else {
       if (DISCARD) discard_l2(slot + 4096 * g + 16 * (tid & 255));
       const uint32_t bA = b + offA;
@@ -544,6 +575,8 @@ static int colring_prepare(int* ctas) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  if constexpr (B >= 16) {  // transposed output (first pass of the two-pass large 1-D transform)
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, false, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
@@ -619,8 +652,8 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   }
   if (xp) {
     // transposed output T (C rows of R = 256 B per image), a row viewed [k2][k1]
-    if (spec_out || twlo || (B != 16 && B != 64))
-      return fail(DPP_ENOTSUP, "transposed column pass needs 4096 or 16384 rows, no fused epilogue");
+    if (spec_out || twlo || B < 16)
+      return fail(DPP_ENOTSUP, "transposed column pass needs 4096 .. 32768 rows, no fused epilogue");
     if (dst == data) return fail(DPP_EINVAL, "transposed column pass cannot run in place");
     const uint64_t dims[3] = {(uint64_t)B, 256, (uint64_t)C * batch};
     const uint64_t strides[2] = {(uint64_t)B * 8, (uint64_t)R * 8};
@@ -659,10 +692,12 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   if ((twlo || spec_out) && B != 16 && B != 64)
     return fail(DPP_ENOTSUP, "fused spectrum / twiddled column pass needs 4096 or 16384 rows");
   if (xp) {
-    if (B == 16)
-      colring::fft_cols_l2w<16, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
-    else
-      colring::fft_cols_l2w<64, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    switch (B) {
+      case 16: colring::fft_cols_l2w<16, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      case 32: colring::fft_cols_l2w<32, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      case 64: colring::fft_cols_l2w<64, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      default: colring::fft_cols_l2w<128, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    }
   } else if (twlo) {
     if (B == 16)
       colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);

@@ -12,8 +12,8 @@
 // Three HBM passes (48 B per point) against the 16 B compulsory; the two
 // FFT passes are the tuned kernels, the transpose is a 32 x 32 tile copy.
 //
-// Two passes (32 B per point) when A and Bc are both 4096 or 16384 (n = 2^24,
-// 2^26, 2^28): steps 1 + 2 become ONE column ring over the A x Bc view of x
+// Two passes (32 B per point) when Bc is 4096 or 16384 and A is 4096 ..
+// 32768 (n = 2^24 .. 2^29): steps 1 + 2 become ONE column ring over the A x Bc view of x
 // (A-point FFTs down its Bc columns) whose ring slot is laid out per column,
 // so each P2 block writes 16 consecutive k1 of one row of T by a TMA box
 // (fft2d_l2.cu, XP) — the transpose rides on the exchange that the column
@@ -78,7 +78,11 @@ int fft_twiddle_slab(float2* data, int64_t rows, int64_t cols, int64_t c0, int64
 
 int fft_large_init(FftPlan* p) {
   const int64_t n = p->n0;
-  const int64_t bc = n <= (1LL << 24) ? 4096 : 16384;
+  // two passes need the second factor Bc in {4096, 16384} (the twiddled ring)
+  // and the first A in 4096 .. 32768 (the transposed-output ring)
+  auto xp_ok = [](int64_t a) { return a >= 4096 && a <= 32768; };
+  int64_t bc = n <= (1LL << 24) ? 4096 : 16384;
+  if (!xp_ok(n / bc) && xp_ok(n / (20480 - bc))) bc = 20480 - bc;  // the other column length
   const int64_t a = n / bc;
   if (a < 32 || a > 65536)
     return fail(DPP_ENOTSUP, "1-D transform size %lld is outside 2^18..2^30", (long long)n);
@@ -88,7 +92,7 @@ int fft_large_init(FftPlan* p) {
   // in-place calls go through a scratch of big_chunk transforms (<= 256 MB, or one transform)
   const int64_t per = (1LL << 25) / n > 1 ? (1LL << 25) / n : 1;
   p->big_chunk = p->batch < per ? (p->batch > 0 ? p->batch : 1) : per;
-  const bool two_pass = (a == 4096 || a == 16384) && (bc == 4096 || bc == 16384);
+  const bool two_pass = xp_ok(a);
   if (two_pass) {
     p->xcols = new FftPlan();
     p->xcols->rank = 2;

@@ -213,6 +213,13 @@ __device__ __forceinline__ void st_l2_hint(float2* p, float2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
 }
 
+// two adjacent complex values (one 16-byte chunk, 16-byte aligned)
+__device__ __forceinline__ void st_l2_hint2(float2* p, float2 a, float2 b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(a.x), "f"(a.y), "f"(b.x),
+               "f"(b.y), "l"(pol)
+               : "memory");
+}
+
 // one 32-byte sector: four complex values (32-byte aligned; STG.256 on sm_100)
 __device__ __forceinline__ void st_l2_hint4(float2* p, float2 a, float2 b, float2 c, float2 d, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "f"(a.x),

@@ -347,9 +347,9 @@ def test_sizes_above_2e17_vs_oracle(cuda, m, batch):
     assert max(errs) <= tol(n), (n, max(errs))
 
 
-@pytest.mark.parametrize("m", [26, 28])
+@pytest.mark.parametrize("m", [26, 27, 28])
 def test_two_pass_large_sizes_vs_numpy_f64(cuda, m):
-    """2^26 (4096 x 16384) and 2^28 (16384 x 16384): the two-pass schedule
+    """2^26 (4096 x 16384), 2^27 (8192 x 16384) and 2^28 (16384 x 16384): the two-pass schedule
     against numpy's binary64 FFT of the same signal (the oracle port would
     take minutes here; it is pinned to numpy at smaller sizes)."""
     import numpy as np
@@ -363,6 +363,34 @@ def test_two_pass_large_sizes_vs_numpy_f64(cuda, m):
     y = ops.fft_forward(x, n).cpu().numpy()
     ref = np.fft.fft(x.cpu().numpy().astype(np.complex128))
     assert rel_l2(y, ref) <= tol(n)
+
+
+def test_two_pass_2e29_identities_and_sampled_bins(cuda):
+    """2^29 (32768 x 16384; 4 GiB in + out): sum_k X[k] = N x[0], Parseval,
+    and three bins against their direct binary64 DFT sums (exact integer
+    phases (k n) mod N)."""
+    import torch
+
+    from paper_1203_4938_b200 import ops
+    n = 1 << 29
+    assert "two passes" in ops.fft_plan(1, n, 1, 1, cuda).description
+    gen = torch.Generator(device=cuda).manual_seed(29)
+    x = torch.randn(n, dtype=torch.complex64, device=cuda, generator=gen)
+    y = ops.fft_forward(x, n)
+    s = y.to(torch.complex128).sum()
+    assert abs(s - n * x[0].to(torch.complex128)) / (n ** 0.5 * n ** 0.5) < 1e-5
+    ex = x.abs().to(torch.float64).pow(2).sum()
+    ey = y.abs().to(torch.float64).pow(2).sum() / n
+    assert abs(ey / ex - 1) < 1e-5
+    for k in (1, 12345, n - 7):
+        acc = torch.zeros((), dtype=torch.complex128, device=cuda)
+        for lo in range(0, n, 1 << 26):
+            idx = torch.arange(lo, lo + (1 << 26), dtype=torch.int64, device=cuda)
+            ph = (idx * k) % n
+            w = torch.polar(torch.ones_like(ph, dtype=torch.float64), -2 * torch.pi * ph.to(torch.float64) / n)
+            acc += (x[lo:lo + (1 << 26)].to(torch.complex128) * w).sum()
+        assert abs(y[k].to(torch.complex128) - acc) / (n ** 0.5) < 1e-4
+    del x, y
 
 
 def test_two_pass_in_place_matches_out_of_place(cuda):
