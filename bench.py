@@ -514,16 +514,19 @@ def run_ours(args) -> None:
     del host_in, host_out
     # ... and through the reference-shaped graph API: run() on numpy StreamFiles
     afft.fft_batch(x_host, N)  # warm: page-locked staging slots of the full size
-    barrier(world)
-    g0 = time.perf_counter()
-    y_graph = afft.fft_batch(x_host, N)
-    g_s = max_over_ranks(time.perf_counter() - g0, world)
-    graph_ok = bool(np.array_equal(y_graph[:4], y_host[:4]))
-    del y_graph
+    g_runs = []
+    for _ in range(3):  # median of 3 host-timed calls (one call is ~0.15 s of host copies)
+        barrier(world)
+        g0 = time.perf_counter()
+        y_graph = afft.fft_batch(x_host, N)
+        g_runs.append(max_over_ranks(time.perf_counter() - g0, world))
+        graph_ok = bool(np.array_equal(y_graph[:4], y_host[:4]))
+        del y_graph
+    g_s = sorted(g_runs)[1]
     e2e_graph = {"value": round(world * BATCH * FLOPS_PER_TRANSFORM / g_s / 1e9, 2), "unit": "GFLOP/s",
                  "api": "apps.fft.fft_batch(numpy) -> run(backend, fft65536 program, StreamFile) -> numpy",
                  "h2d_bytes_per_step": BATCH * N * 8, "d2h_bytes_per_step": BATCH * N * 8,
-                 "same_output_as_device_path": graph_ok}
+                 "same_output_as_device_path": graph_ok, "calls_s": [round(t, 4) for t in g_runs]}
     del x, y
 
     # ------------------------------------------------------------------ C4
