@@ -17,11 +17,30 @@ namespace dpp {
 
 constexpr int KD = 16;  // block vectors are 16-dim
 
-__device__ __forceinline__ double dist2(const double* a, const double* c) {
+// The trainer keeps its points as structure of arrays, coordinate m of point
+// i at soa[m n + i]: a warp's loads of one coordinate are 256 contiguous
+// bytes (the caller's (n, 16) rows made every per-thread load a 128-byte
+// stride: the k-means++ pass ran at a third of HBM bandwidth).
+__global__ void __launch_bounds__(256) to_soa(const double* __restrict__ pts, int64_t n, double* __restrict__ soa) {
+  __shared__ double t[16][257];
+  const int64_t i0 = (int64_t)blockIdx.x * 256;
+  for (int e = threadIdx.x; e < 256 * KD; e += 256) {  // coalesced row-major read
+    const int64_t r = i0 + e / KD;
+    t[e % KD][e / KD] = r < n ? pts[i0 * KD + e] : 0.0;
+  }
+  __syncthreads();
+  const int64_t i = i0 + threadIdx.x;
+  if (i < n)
+#pragma unroll
+    for (int m = 0; m < KD; ++m) soa[m * n + i] = t[m][threadIdx.x];
+}
+
+__device__ __forceinline__ double dist2_soa(const double* __restrict__ soa, int64_t n, int64_t i,
+                                            const double* c) {
   double s = 0.0;
 #pragma unroll
   for (int m = 0; m < KD; ++m) {
-    const double d = a[m] - c[m];
+    const double d = soa[m * n + i] - c[m];
     s = fma(d, d, s);
   }
   return s;
@@ -37,7 +56,7 @@ __global__ void kpp_update(const double* __restrict__ pts, int64_t n, const doub
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (i < n) {
-    const double d = dist2(pts + i * KD, cs);
+    const double d = dist2_soa(pts, n, i, cs);
     v = first ? d : fmin(d2[i], d);
     d2[i] = v;
   }
@@ -150,7 +169,7 @@ __global__ void __launch_bounds__(PICK_T) kpp_pick(const double* __restrict__ d2
   }
 copy:
   if (tid == 0) *pick_out = pick_s;
-  if (tid < KD) centroid[tid] = pts[pick_s * KD + tid];
+  if (tid < KD) centroid[tid] = pts[tid * n + pick_s];
 }
 
 // total of the block sums (the shard's d2 total for the all-reduce)
@@ -177,49 +196,133 @@ __global__ void pack_acc(const double* __restrict__ sums, const unsigned long lo
   else if (e == k * KD + k + 1) acc[e] = *sse;
 }
 
-// nearest centroid (first minimum), counts changes vs previous assignment,
-// accumulates per-cluster sums/counts in shared memory then globally
-__global__ void lloyd_assign(const double* __restrict__ pts, int64_t n, const double* __restrict__ cents, int k,
-                             int32_t* __restrict__ assign, double* __restrict__ sums,
-                             unsigned long long* __restrict__ counts, unsigned long long* __restrict__ changed,
-                             double* __restrict__ sse) {
-  extern __shared__ double sh[];
+// nearest centroid, counts changes vs previous assignment, accumulates
+// per-cluster sums / counts in shared memory then globally.  The distance
+// ranking uses the reference's own expansion (imgc.py:276-279: |p|^2 + |c|^2 -
+// 2 p.c, |p|^2 dropped as it is the same for every centroid): one binary64
+// FMA per coordinate instead of a subtract and an FMA, strict <, first index.
+// Each thread takes PPT points, so every centroid read from shared memory (8
+// LDS.128, broadcast) serves PPT dot products.  The SSE adds the direct
+// binary64 distance to the chosen centroid (the reference's trace formula).
+constexpr int PPT = 2;
+__global__ void __launch_bounds__(256) lloyd_assign(const double* __restrict__ pts, int64_t n,
+                                                    const double* __restrict__ cents, int k,
+                                                    int32_t* __restrict__ assign, double* __restrict__ sums,
+                                                    unsigned long long* __restrict__ counts,
+                                                    unsigned long long* __restrict__ changed,
+                                                    double* __restrict__ sse) {
+  extern __shared__ __align__(16) double sh[];
   double* sc = sh;                  // k * KD centroids
   double* ssum = sh + k * KD;       // k * KD partial sums
-  unsigned int* scnt = reinterpret_cast<unsigned int*>(ssum + k * KD);
+  double* scn = ssum + k * KD;      // k: |c_j|^2
+  unsigned int* scnt = reinterpret_cast<unsigned int*>(scn + k);
   for (int e = threadIdx.x; e < k * KD; e += blockDim.x) {
     sc[e] = cents[e];
     ssum[e] = 0.0;
   }
-  for (int e = threadIdx.x; e < k; e += blockDim.x) scnt[e] = 0;
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double local_sse = 0.0;
-  if (i < n) {
-    double p[KD];
-#pragma unroll
-    for (int m = 0; m < KD; ++m) p[m] = pts[i * KD + m];
-    double best = 1.0 / 0.0;
-    int bj = 0;
-    for (int j = 0; j < k; ++j) {
-      const double d = dist2(p, sc + j * KD);
-      if (d < best) { best = d; bj = j; }
-    }
-    local_sse = best;
-    if (assign[i] != bj) atomicAdd(changed, 1ULL);
-    assign[i] = bj;
-#pragma unroll
-    for (int m = 0; m < KD; ++m) atomicAdd(&ssum[bj * KD + m], p[m]);
-    atomicAdd(&scnt[bj], 1u);
+  for (int e = threadIdx.x; e < k; e += blockDim.x) {
+    double c2 = 0.0;
+    for (int m = 0; m < KD; ++m) c2 = fma(cents[e * KD + m], cents[e * KD + m], c2);
+    scn[e] = c2;
+    scnt[e] = 0;
   }
-  for (int o = 16; o > 0; o >>= 1) local_sse += __shfl_xor_sync(0xffffffffu, local_sse, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(sse, local_sse);
+  __syncthreads();
+  double local_sse = 0.0;
+  unsigned nchanged = 0;
+  // persistent blocks: the partial sums reach global memory once per block
+  // (one atomic per block and coordinate, not one per 512 points)
+  for (int64_t i0 = (int64_t)blockIdx.x * (256 * PPT) + threadIdx.x; i0 - threadIdx.x < n;
+       i0 += (int64_t)gridDim.x * (256 * PPT)) {
+    double p[PPT][KD];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int64_t i = i0 + 256 * q;
+#pragma unroll
+      for (int m = 0; m < KD; ++m) p[q][m] = i < n ? pts[m * n + i] : 0.0;
+    }
+    double best[PPT];
+    int bj[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      best[q] = 1.0 / 0.0;
+      bj[q] = 0;
+    }
+    for (int j = 0; j < k; ++j) {
+      const double2* c2 = reinterpret_cast<const double2*>(sc + j * KD);
+      double dot[PPT];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) dot[q] = 0.0;
+#pragma unroll
+      for (int h = 0; h < KD / 2; ++h) {
+        const double2 c = c2[h];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+          dot[q] = fma(p[q][2 * h], c.x, dot[q]);
+          dot[q] = fma(p[q][2 * h + 1], c.y, dot[q]);
+        }
+      }
+      const double cn = scn[j];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const double sc2 = fma(-2.0, dot[q], cn);
+        if (sc2 < best[q]) {
+          best[q] = sc2;
+          bj[q] = j;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int64_t i = i0 + 256 * q;
+      if (i < n) {
+        const double* c = sc + bj[q] * KD;
+        double d = 0.0;
+#pragma unroll
+        for (int m = 0; m < KD; ++m) {
+          const double t = p[q][m] - c[m];
+          d = fma(t, t, d);
+        }
+        local_sse += d;
+        nchanged += assign[i] != bj[q];
+        assign[i] = bj[q];
+#pragma unroll
+        for (int m = 0; m < KD; ++m) atomicAdd(&ssum[bj[q] * KD + m], p[q][m]);
+        atomicAdd(&scnt[bj[q]], 1u);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    local_sse += __shfl_xor_sync(0xffffffffu, local_sse, o);
+    nchanged += __shfl_xor_sync(0xffffffffu, nchanged, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(sse, local_sse);
+    if (nchanged) atomicAdd(changed, (unsigned long long)nchanged);
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < k * KD; e += blockDim.x)
     if (ssum[e] != 0.0) atomicAdd(&sums[e], ssum[e]);
   for (int e = threadIdx.x; e < k; e += blockDim.x)
     if (scnt[e]) atomicAdd(&counts[e], (unsigned long long)scnt[e]);
 }
+
+// launch geometry and shared memory of lloyd_assign: at most the resident blocks
+static inline int lloyd_blocks(int64_t n) {
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lloyd_assign, 256,
+                                                      (size_t)256 * KD * 2 * sizeof(double) + 256 * 12) != cudaSuccess ||
+        per < 1)
+      per = 1;
+    resident = per * sms;
+  }
+  const int64_t need = (n + 256 * PPT - 1) / (256 * PPT);
+  return (int)(need < resident ? need : resident);
+}
+static inline size_t lloyd_smem(int k) { return (size_t)k * KD * 2 * sizeof(double) + k * (sizeof(double) + sizeof(unsigned int)); }
 
 __global__ void lloyd_means(double* __restrict__ cents, const double* __restrict__ sums,
                             const unsigned long long* __restrict__ counts, int k) {
@@ -234,7 +337,7 @@ __global__ void far_point(const double* __restrict__ pts, int64_t n, const doubl
                           int64_t base = 0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double d = dist2(pts + i * KD, cents + (int64_t)assign[i] * KD);
+  const double d = dist2_soa(pts, n, i, cents + (int64_t)assign[i] * KD);
   // pack (distance as f32 bits, inverted index): atomicMax picks the largest
   // distance and, among equal ones, the lowest index (np.argmax)
   atomicMax(best, ((unsigned long long)__float_as_uint((float)d) << 32) | (0xffffffffu - (uint32_t)(base + i)));
@@ -245,7 +348,8 @@ __global__ void far_point(const double* __restrict__ pts, int64_t n, const doubl
 // driver (paper_1203_4938_b200/kmeans.py, kmeans_sharded) combines shards
 // with one all-reduce per seeding step / Lloyd iteration
 struct KmShard {
-  const double* pts = nullptr;
+  const double* pts = nullptr;  // the caller's (n, 16) rows
+  double* soa = nullptr;        // the trainer's copy, coordinate-major
   int64_t n = 0;
   int k = 0, nb = 0;
   cudaStream_t s = nullptr;
@@ -254,8 +358,8 @@ struct KmShard {
   unsigned long long *counts = nullptr, *changed = nullptr, *far = nullptr;
   int64_t* pick = nullptr;
   void release() {
-    for (void* ptr : {(void*)d2, (void*)bsum, (void*)sums, (void*)sse, (void*)total, (void*)assign, (void*)counts,
-                      (void*)changed, (void*)far, (void*)pick})
+    for (void* ptr : {(void*)soa, (void*)d2, (void*)bsum, (void*)sums, (void*)sse, (void*)total, (void*)assign,
+                      (void*)counts, (void*)changed, (void*)far, (void*)pick})
       if (ptr) cudaFree(ptr);
   }
 };
@@ -282,7 +386,8 @@ int dpp_kmeans_shard_create(dpp_kmeans_shard** shard, const double* pts, int64_t
   m.nb = (int)((n + 255) / 256);
   m.s = static_cast<cudaStream_t>(stream);
   const size_t nn = (size_t)(n > 0 ? n : 1), nbb = (size_t)(m.nb > 0 ? m.nb : 1);
-  bool ok = cudaMalloc(&m.d2, nn * sizeof(double)) == cudaSuccess &&
+  bool ok = cudaMalloc(&m.soa, nn * KD * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&m.d2, nn * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&m.bsum, nbb * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&m.sums, (size_t)k * KD * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&m.sse, sizeof(double)) == cudaSuccess && cudaMalloc(&m.total, sizeof(double)) == cudaSuccess &&
@@ -291,6 +396,10 @@ int dpp_kmeans_shard_create(dpp_kmeans_shard** shard, const double* pts, int64_t
             cudaMalloc(&m.changed, sizeof(unsigned long long)) == cudaSuccess &&
             cudaMalloc(&m.far, sizeof(unsigned long long)) == cudaSuccess &&
             cudaMalloc(&m.pick, sizeof(int64_t)) == cudaSuccess;
+  if (ok && n > 0) {
+    to_soa<<<m.nb, 256, 0, m.s>>>(pts, n, m.soa);
+    ok = cudaGetLastError() == cudaSuccess;
+  }
   if (!ok || cudaMemsetAsync(m.assign, 0xff, nn * sizeof(int32_t), m.s) != cudaSuccess) {
     m.release();
     delete h;
@@ -310,7 +419,7 @@ int dpp_kmeans_shard_seed(dpp_kmeans_shard* shard, const double* centroid, int f
     *total = 0.0;
     return DPP_OK;
   }
-  kpp_update<<<m.nb, 256, 0, m.s>>>(m.pts, m.n, centroid, m.d2, m.bsum, first);
+  kpp_update<<<m.nb, 256, 0, m.s>>>(m.soa, m.n, centroid, m.d2, m.bsum, first);
   kpp_total<<<1, PICK_T, 0, m.s>>>(m.bsum, m.nb, m.total);
   DPP_LAUNCH_CHECK("k-means++ shard update");
   DPP_CUDA_CHECK(cudaMemcpyAsync(total, m.total, sizeof(double), cudaMemcpyDeviceToHost, m.s));
@@ -334,7 +443,7 @@ int dpp_kmeans_shard_pick(dpp_kmeans_shard* shard, double target, int64_t local_
     *picked = local_index;
     return DPP_OK;
   }
-  kpp_pick<false><<<1, PICK_T, 0, m.s>>>(m.d2, m.n, m.bsum, m.nb, 256, target, m.pts, centroid_out, m.pick);
+  kpp_pick<false><<<1, PICK_T, 0, m.s>>>(m.d2, m.n, m.bsum, m.nb, 256, target, m.soa, centroid_out, m.pick);
   DPP_LAUNCH_CHECK("k-means++ shard pick");
   DPP_CUDA_CHECK(cudaMemcpyAsync(picked, m.pick, sizeof(int64_t), cudaMemcpyDeviceToHost, m.s));
   DPP_CUDA_CHECK(cudaStreamSynchronize(m.s));
@@ -353,13 +462,14 @@ int dpp_kmeans_shard_assign(dpp_kmeans_shard* shard, const double* cents, double
     DPP_CUDA_CHECK(cudaMemsetAsync(acc, 0, tot * sizeof(double), m.s));
     return DPP_OK;
   }
-  const size_t shm = (size_t)k * KD * 2 * sizeof(double) + k * sizeof(unsigned int);
+  const size_t shm = lloyd_smem(k);
   DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   DPP_CUDA_CHECK(cudaMemsetAsync(m.sums, 0, (size_t)k * KD * sizeof(double), m.s));
   DPP_CUDA_CHECK(cudaMemsetAsync(m.counts, 0, k * sizeof(unsigned long long), m.s));
   DPP_CUDA_CHECK(cudaMemsetAsync(m.changed, 0, sizeof(unsigned long long), m.s));
   DPP_CUDA_CHECK(cudaMemsetAsync(m.sse, 0, sizeof(double), m.s));
-  lloyd_assign<<<m.nb, 256, shm, m.s>>>(m.pts, m.n, cents, k, m.assign, m.sums, m.counts, m.changed, m.sse);
+  lloyd_assign<<<lloyd_blocks(m.n), 256, shm, m.s>>>(m.soa, m.n, cents, k, m.assign, m.sums, m.counts, m.changed,
+                                                      m.sse);
   pack_acc<<<(tot + 255) / 256, 256, 0, m.s>>>(m.sums, m.counts, m.changed, m.sse, k, acc);
   DPP_LAUNCH_CHECK("lloyd shard assign");
   return DPP_OK;
@@ -374,7 +484,7 @@ int dpp_kmeans_shard_far(dpp_kmeans_shard* shard, const double* cents, int64_t b
   KmShard& m = shard->impl;
   DPP_CUDA_CHECK(cudaMemsetAsync(packed, 0, sizeof(int64_t), m.s));
   if (m.n == 0) return DPP_OK;
-  far_point<<<m.nb, 256, 0, m.s>>>(m.pts, m.n, cents, m.assign, reinterpret_cast<unsigned long long*>(packed), base);
+  far_point<<<m.nb, 256, 0, m.s>>>(m.soa, m.n, cents, m.assign, reinterpret_cast<unsigned long long*>(packed), base);
   DPP_LAUNCH_CHECK("far point");
   return DPP_OK;
 }
@@ -407,7 +517,7 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   if (n > 0x7fffffffLL) return fail(DPP_EINVAL, "too many training blocks");
   const int T = 256;
   const int nb = (int)((n + T - 1) / T);
-  double *d2 = nullptr, *bsum = nullptr, *cents = nullptr, *sums = nullptr, *sse = nullptr;
+  double *soa = nullptr, *d2 = nullptr, *bsum = nullptr, *cents = nullptr, *sums = nullptr, *sse = nullptr;
   int32_t* assign = nullptr;
   unsigned long long *counts = nullptr, *changed = nullptr, *far = nullptr;
   int64_t* pick = nullptr;
@@ -425,6 +535,7 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
     release.ptrs.push_back(*ptr);
     return e;
   };
+  DPP_CUDA_CHECK(alloc(&soa, n * KD * sizeof(double)));
   DPP_CUDA_CHECK(alloc(&d2, n * sizeof(double)));
   DPP_CUDA_CHECK(alloc(&bsum, nb * sizeof(double)));
   DPP_CUDA_CHECK(alloc(&cents, (size_t)k * KD * sizeof(double)));
@@ -436,17 +547,18 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   DPP_CUDA_CHECK(alloc(&far, sizeof(unsigned long long)));
   DPP_CUDA_CHECK(alloc(&pick, sizeof(int64_t)));
 
+  to_soa<<<nb, T, 0, s>>>(pts, n, soa);
   // k-means++ seeding
   DPP_CUDA_CHECK(cudaMemcpyAsync(cents, pts + first_pick * KD, KD * sizeof(double), cudaMemcpyDeviceToDevice, s));
   for (int j = 1; j < k; ++j) {
-    kpp_update<<<nb, T, 0, s>>>(pts, n, cents + (j - 1) * KD, d2, bsum, j == 1);
-    kpp_pick<true><<<1, PICK_T, 0, s>>>(d2, n, bsum, nb, T, uniforms[j - 1], pts, cents + j * KD, pick);
+    kpp_update<<<nb, T, 0, s>>>(soa, n, cents + (j - 1) * KD, d2, bsum, j == 1);
+    kpp_pick<true><<<1, PICK_T, 0, s>>>(d2, n, bsum, nb, T, uniforms[j - 1], soa, cents + j * KD, pick);
   }
   DPP_LAUNCH_CHECK("k-means++ seeding");
 
   // Lloyd
   DPP_CUDA_CHECK(cudaMemsetAsync(assign, 0xff, n * sizeof(int32_t), s));  // -1: every point "changes"
-  const size_t shm = (size_t)k * KD * 2 * sizeof(double) + k * sizeof(unsigned int);
+  const size_t shm = lloyd_smem(k);
   DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   std::vector<unsigned long long> hcounts(k);
   int it = 0;
@@ -456,7 +568,7 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
     DPP_CUDA_CHECK(cudaMemsetAsync(counts, 0, k * sizeof(unsigned long long), s));
     DPP_CUDA_CHECK(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), s));
     DPP_CUDA_CHECK(cudaMemsetAsync(sse, 0, sizeof(double), s));
-    lloyd_assign<<<nb, T, shm, s>>>(pts, n, cents, k, assign, sums, counts, changed, sse);
+    lloyd_assign<<<lloyd_blocks(n), T, shm, s>>>(soa, n, cents, k, assign, sums, counts, changed, sse);
     DPP_LAUNCH_CHECK("lloyd_assign");
     DPP_CUDA_CHECK(cudaMemcpyAsync(h_changed, changed, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     DPP_CUDA_CHECK(cudaMemcpyAsync(h_sse, sse, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -473,7 +585,7 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
     for (int j = 0; j < k; ++j) {
       if (hcounts[j]) continue;
       DPP_CUDA_CHECK(cudaMemsetAsync(far, 0, sizeof(unsigned long long), s));
-      far_point<<<nb, T, 0, s>>>(pts, n, cents, assign, far);
+      far_point<<<nb, T, 0, s>>>(soa, n, cents, assign, far);
       unsigned long long hf = 0;
       DPP_CUDA_CHECK(cudaMemcpyAsync(&hf, far, sizeof(hf), cudaMemcpyDeviceToHost, s));
       DPP_CUDA_CHECK(cudaStreamSynchronize(s));
