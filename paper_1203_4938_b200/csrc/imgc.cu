@@ -221,6 +221,10 @@ struct EncodeArgs {
   uint8_t* mu_plane;
   uint8_t* sig_plane;
   uint8_t* idx_plane;
+  // CH = 0 (the k-means trainer's Lloyd assignment, csrc/kmeans.cu): the
+  // blocks are given as normalised binary32 16-vectors, vecs[k][16], and only
+  // idx_plane is written
+  const float* vecs = nullptr;
 };
 
 template <int CH>
@@ -743,7 +747,18 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
       float nb[16];
       double mean = 0.0, sd = 0.0;
       if (active) {
-        block_front<CH, false>(a, img, k, nb, mean, sd, CH == 1 ? lut : nullptr, aligned4);
+        if constexpr (CH == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(a.vecs + k * 16) + q);
+            nb[4 * q] = f.x;
+            nb[4 * q + 1] = f.y;
+            nb[4 * q + 2] = f.z;
+            nb[4 * q + 3] = f.w;
+          }
+        } else {
+          block_front<CH, false>(a, img, k, nb, mean, sd, CH == 1 ? lut : nullptr, aligned4);
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < 16; ++e) nb[e] = 0.f;
@@ -887,7 +902,9 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
       // every thread writes its own block's record: three byte stores per
       // warp instruction cover 96 contiguous bytes (interleaved) or 32 per
       // plane
-      if (active) {
+      if (CH == 0) {
+        if (active) a.idx_plane[k] = (uint8_t)bj;
+      } else if (active) {
         const int64_t gk = img * nblocks + k;
         if (a.idx_plane) {
           a.mu_plane[gk] = mu;
@@ -940,6 +957,7 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
                                         (int)smem));                                                        \
     encode_ws_kernel<CHN><<<grid, ws::THREADS, smem, s>>>(a, batch, delta_scale, ambiguous);              \
     break;
+    TC_CASE(0)
     TC_CASE(1)
     TC_CASE(3)
     TC_CASE(4)
@@ -947,6 +965,21 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
   }
   DPP_LAUNCH_CHECK("encode_ws_kernel");
   return DPP_OK;
+}
+
+// Nearest centroid of n normalised binary32 16-vectors (the encoder's search:
+// 3xTF32 tensor-core scores, exact binary32 re-check of the ambiguous ones,
+// strict <, first index) — the Lloyd assignment of the k-means trainer.
+int vq_assign_tc(const float* vecs, int64_t n, const float* cents, int k, uint8_t* idx, cudaStream_t s) {
+  if (n <= 0) return DPP_OK;
+  EncodeArgs a{};
+  a.vecs = vecs;
+  a.height = 4 * n;  // n "blocks" of one 4-wide column
+  a.width = 4;
+  a.codebook = cents;
+  a.ncb = k;
+  a.idx_plane = idx;
+  return launch_encode_tc(a, 0, 1, n, 1.0f, nullptr, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -21,12 +21,16 @@ constexpr int KD = 16;  // block vectors are 16-dim
 // i at soa[m n + i]: a warp's loads of one coordinate are 256 contiguous
 // bytes (the caller's (n, 16) rows made every per-thread load a 128-byte
 // stride: the k-means++ pass ran at a third of HBM bandwidth).
-__global__ void __launch_bounds__(256) to_soa(const double* __restrict__ pts, int64_t n, double* __restrict__ soa) {
+// (also the binary32 rows the tensor-core Lloyd assignment searches with)
+__global__ void __launch_bounds__(256) to_soa(const double* __restrict__ pts, int64_t n, double* __restrict__ soa,
+                                              float* __restrict__ rows32) {
   __shared__ double t[16][257];
   const int64_t i0 = (int64_t)blockIdx.x * 256;
   for (int e = threadIdx.x; e < 256 * KD; e += 256) {  // coalesced row-major read
     const int64_t r = i0 + e / KD;
-    t[e % KD][e / KD] = r < n ? pts[i0 * KD + e] : 0.0;
+    const double v = r < n ? pts[i0 * KD + e] : 0.0;
+    t[e % KD][e / KD] = v;
+    if (r < n) rows32[i0 * KD + e] = (float)v;
   }
   __syncthreads();
   const int64_t i = i0 + threadIdx.x;
@@ -196,17 +200,25 @@ __global__ void pack_acc(const double* __restrict__ sums, const unsigned long lo
   else if (e == k * KD + k + 1) acc[e] = *sse;
 }
 
-// nearest centroid, counts changes vs previous assignment, accumulates
-// per-cluster sums / counts in shared memory then globally.  The distance
-// ranking uses the reference's own expansion (imgc.py:276-279: |p|^2 + |c|^2 -
-// 2 p.c, |p|^2 dropped as it is the same for every centroid): one binary64
-// FMA per coordinate instead of a subtract and an FMA, strict <, first index.
-// Each thread takes PPT points, so every centroid read from shared memory (8
-// LDS.128, broadcast) serves PPT dot products.  The SSE adds the direct
-// binary64 distance to the chosen centroid (the reference's trace formula).
+int vq_assign_tc(const float* vecs, int64_t n, const float* cents, int k, uint8_t* idx, cudaStream_t s);
+
+// binary64 centroids -> the binary32 codebook of the tensor-core search
+__global__ void cents_to_f32(const double* __restrict__ c, int k, float* __restrict__ c32) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * KD) c32[e] = (float)c[e];
+}
+
+// Lloyd update after the assignment: the nearest centroid of every point
+// comes from the encoder's tensor-core search (vq_assign_tc: 3xTF32 scores
+// on tcgen05, exact binary32 re-check of near ties, strict <, first index —
+// SURVEY §8(f) row 2's "GEMM distances on tensor cores"); this pass counts
+// changed assignments, adds the binary64 distance to the chosen centroid
+// (the reference's trace formula) and accumulates binary64 per-cluster sums
+// and counts in shared memory, flushed once per persistent block.
 constexpr int PPT = 2;
 __global__ void __launch_bounds__(256) lloyd_assign(const double* __restrict__ pts, int64_t n,
                                                     const double* __restrict__ cents, int k,
+                                                    const uint8_t* __restrict__ nearest,
                                                     int32_t* __restrict__ assign, double* __restrict__ sums,
                                                     unsigned long long* __restrict__ counts,
                                                     unsigned long long* __restrict__ changed,
@@ -214,82 +226,30 @@ __global__ void __launch_bounds__(256) lloyd_assign(const double* __restrict__ p
   extern __shared__ __align__(16) double sh[];
   double* sc = sh;                  // k * KD centroids
   double* ssum = sh + k * KD;       // k * KD partial sums
-  double* scn = ssum + k * KD;      // k: |c_j|^2
-  unsigned int* scnt = reinterpret_cast<unsigned int*>(scn + k);
+  unsigned int* scnt = reinterpret_cast<unsigned int*>(ssum + k * KD);
   for (int e = threadIdx.x; e < k * KD; e += blockDim.x) {
     sc[e] = cents[e];
     ssum[e] = 0.0;
   }
-  for (int e = threadIdx.x; e < k; e += blockDim.x) {
-    double c2 = 0.0;
-    for (int m = 0; m < KD; ++m) c2 = fma(cents[e * KD + m], cents[e * KD + m], c2);
-    scn[e] = c2;
-    scnt[e] = 0;
-  }
+  for (int e = threadIdx.x; e < k; e += blockDim.x) scnt[e] = 0;
   __syncthreads();
   double local_sse = 0.0;
   unsigned nchanged = 0;
-  // persistent blocks: the partial sums reach global memory once per block
-  // (one atomic per block and coordinate, not one per 512 points)
-  for (int64_t i0 = (int64_t)blockIdx.x * (256 * PPT) + threadIdx.x; i0 - threadIdx.x < n;
-       i0 += (int64_t)gridDim.x * (256 * PPT)) {
-    double p[PPT][KD];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = nearest[i];
+    const double* c = sc + j * KD;
+    double d = 0.0;
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      const int64_t i = i0 + 256 * q;
-#pragma unroll
-      for (int m = 0; m < KD; ++m) p[q][m] = i < n ? pts[m * n + i] : 0.0;
+    for (int m = 0; m < KD; ++m) {
+      const double p = pts[m * n + i];
+      const double t = p - c[m];
+      d = fma(t, t, d);
+      atomicAdd(&ssum[j * KD + m], p);
     }
-    double best[PPT];
-    int bj[PPT];
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      best[q] = 1.0 / 0.0;
-      bj[q] = 0;
-    }
-    for (int j = 0; j < k; ++j) {
-      const double2* c2 = reinterpret_cast<const double2*>(sc + j * KD);
-      double dot[PPT];
-#pragma unroll
-      for (int q = 0; q < PPT; ++q) dot[q] = 0.0;
-#pragma unroll
-      for (int h = 0; h < KD / 2; ++h) {
-        const double2 c = c2[h];
-#pragma unroll
-        for (int q = 0; q < PPT; ++q) {
-          dot[q] = fma(p[q][2 * h], c.x, dot[q]);
-          dot[q] = fma(p[q][2 * h + 1], c.y, dot[q]);
-        }
-      }
-      const double cn = scn[j];
-#pragma unroll
-      for (int q = 0; q < PPT; ++q) {
-        const double sc2 = fma(-2.0, dot[q], cn);
-        if (sc2 < best[q]) {
-          best[q] = sc2;
-          bj[q] = j;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      const int64_t i = i0 + 256 * q;
-      if (i < n) {
-        const double* c = sc + bj[q] * KD;
-        double d = 0.0;
-#pragma unroll
-        for (int m = 0; m < KD; ++m) {
-          const double t = p[q][m] - c[m];
-          d = fma(t, t, d);
-        }
-        local_sse += d;
-        nchanged += assign[i] != bj[q];
-        assign[i] = bj[q];
-#pragma unroll
-        for (int m = 0; m < KD; ++m) atomicAdd(&ssum[bj[q] * KD + m], p[q][m]);
-        atomicAdd(&scnt[bj[q]], 1u);
-      }
-    }
+    local_sse += d;
+    nchanged += assign[i] != j;
+    assign[i] = j;
+    atomicAdd(&scnt[j], 1u);
   }
   for (int o = 16; o > 0; o >>= 1) {
     local_sse += __shfl_xor_sync(0xffffffffu, local_sse, o);
@@ -306,6 +266,12 @@ __global__ void __launch_bounds__(256) lloyd_assign(const double* __restrict__ p
     if (scnt[e]) atomicAdd(&counts[e], (unsigned long long)scnt[e]);
 }
 
+// one Lloyd assignment: binary32 codebook, tensor-core nearest centroid,
+// binary64 update pass (shared by the single-GPU trainer and the shards)
+static int lloyd_pass(const double* soa, const float* rows32, int64_t n, const double* cents, float* cents32, int k,
+                      uint8_t* nearest, int32_t* assign, double* sums, unsigned long long* counts,
+                      unsigned long long* changed, double* sse, cudaStream_t s);
+
 // launch geometry and shared memory of lloyd_assign: at most the resident blocks
 static inline int lloyd_blocks(int64_t n) {
   static int resident = 0;
@@ -314,15 +280,15 @@ static inline int lloyd_blocks(int64_t n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lloyd_assign, 256,
-                                                      (size_t)256 * KD * 2 * sizeof(double) + 256 * 12) != cudaSuccess ||
+                                                      (size_t)256 * KD * 2 * sizeof(double) + 256 * 4) != cudaSuccess ||
         per < 1)
       per = 1;
     resident = per * sms;
   }
-  const int64_t need = (n + 256 * PPT - 1) / (256 * PPT);
+  const int64_t need = (n + 255) / 256;
   return (int)(need < resident ? need : resident);
 }
-static inline size_t lloyd_smem(int k) { return (size_t)k * KD * 2 * sizeof(double) + k * (sizeof(double) + sizeof(unsigned int)); }
+static inline size_t lloyd_smem(int k) { return (size_t)k * KD * 2 * sizeof(double) + k * sizeof(unsigned int); }
 
 __global__ void lloyd_means(double* __restrict__ cents, const double* __restrict__ sums,
                             const unsigned long long* __restrict__ counts, int k) {
@@ -343,6 +309,27 @@ __global__ void far_point(const double* __restrict__ pts, int64_t n, const doubl
   atomicMax(best, ((unsigned long long)__float_as_uint((float)d) << 32) | (0xffffffffu - (uint32_t)(base + i)));
 }
 
+static int lloyd_pass(const double* soa, const float* rows32, int64_t n, const double* cents, float* cents32, int k,
+                      uint8_t* nearest, int32_t* assign, double* sums, unsigned long long* counts,
+                      unsigned long long* changed, double* sse, cudaStream_t s) {
+  static int attr = 0;
+  if (!attr) {
+    DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lloyd_smem(256)));
+    attr = 1;
+  }
+  DPP_CUDA_CHECK(cudaMemsetAsync(sums, 0, (size_t)k * KD * sizeof(double), s));
+  DPP_CUDA_CHECK(cudaMemsetAsync(counts, 0, k * sizeof(unsigned long long), s));
+  DPP_CUDA_CHECK(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), s));
+  DPP_CUDA_CHECK(cudaMemsetAsync(sse, 0, sizeof(double), s));
+  cents_to_f32<<<(k * KD + 255) / 256, 256, 0, s>>>(cents, k, cents32);
+  if (int rc = vq_assign_tc(rows32, n, cents32, k, nearest, s)) return rc;
+  lloyd_assign<<<lloyd_blocks(n), 256, lloyd_smem(k), s>>>(soa, n, cents, k, nearest, assign, sums, counts, changed,
+                                                           sse);
+  DPP_LAUNCH_CHECK("lloyd_assign");
+  return DPP_OK;
+}
+
 // one shard of a row-sharded k-means (multi-GPU): the
 // device buffers of the single-GPU trainer for this rank's points; the
 // driver (paper_1203_4938_b200/kmeans.py, kmeans_sharded) combines shards
@@ -350,6 +337,9 @@ __global__ void far_point(const double* __restrict__ pts, int64_t n, const doubl
 struct KmShard {
   const double* pts = nullptr;  // the caller's (n, 16) rows
   double* soa = nullptr;        // the trainer's copy, coordinate-major
+  float* rows32 = nullptr;      // binary32 rows for the tensor-core search
+  float* cents32 = nullptr;
+  uint8_t* nearest = nullptr;
   int64_t n = 0;
   int k = 0, nb = 0;
   cudaStream_t s = nullptr;
@@ -358,7 +348,7 @@ struct KmShard {
   unsigned long long *counts = nullptr, *changed = nullptr, *far = nullptr;
   int64_t* pick = nullptr;
   void release() {
-    for (void* ptr : {(void*)soa, (void*)d2, (void*)bsum, (void*)sums, (void*)sse, (void*)total, (void*)assign,
+    for (void* ptr : {(void*)soa, (void*)rows32, (void*)cents32, (void*)nearest, (void*)d2, (void*)bsum, (void*)sums, (void*)sse, (void*)total, (void*)assign,
                       (void*)counts, (void*)changed, (void*)far, (void*)pick})
       if (ptr) cudaFree(ptr);
   }
@@ -387,6 +377,9 @@ int dpp_kmeans_shard_create(dpp_kmeans_shard** shard, const double* pts, int64_t
   m.s = static_cast<cudaStream_t>(stream);
   const size_t nn = (size_t)(n > 0 ? n : 1), nbb = (size_t)(m.nb > 0 ? m.nb : 1);
   bool ok = cudaMalloc(&m.soa, nn * KD * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&m.rows32, nn * KD * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&m.cents32, (size_t)k * KD * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&m.nearest, nn) == cudaSuccess &&
             cudaMalloc(&m.d2, nn * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&m.bsum, nbb * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&m.sums, (size_t)k * KD * sizeof(double)) == cudaSuccess &&
@@ -397,7 +390,7 @@ int dpp_kmeans_shard_create(dpp_kmeans_shard** shard, const double* pts, int64_t
             cudaMalloc(&m.far, sizeof(unsigned long long)) == cudaSuccess &&
             cudaMalloc(&m.pick, sizeof(int64_t)) == cudaSuccess;
   if (ok && n > 0) {
-    to_soa<<<m.nb, 256, 0, m.s>>>(pts, n, m.soa);
+    to_soa<<<m.nb, 256, 0, m.s>>>(pts, n, m.soa, m.rows32);
     ok = cudaGetLastError() == cudaSuccess;
   }
   if (!ok || cudaMemsetAsync(m.assign, 0xff, nn * sizeof(int32_t), m.s) != cudaSuccess) {
@@ -462,14 +455,9 @@ int dpp_kmeans_shard_assign(dpp_kmeans_shard* shard, const double* cents, double
     DPP_CUDA_CHECK(cudaMemsetAsync(acc, 0, tot * sizeof(double), m.s));
     return DPP_OK;
   }
-  const size_t shm = lloyd_smem(k);
-  DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  DPP_CUDA_CHECK(cudaMemsetAsync(m.sums, 0, (size_t)k * KD * sizeof(double), m.s));
-  DPP_CUDA_CHECK(cudaMemsetAsync(m.counts, 0, k * sizeof(unsigned long long), m.s));
-  DPP_CUDA_CHECK(cudaMemsetAsync(m.changed, 0, sizeof(unsigned long long), m.s));
-  DPP_CUDA_CHECK(cudaMemsetAsync(m.sse, 0, sizeof(double), m.s));
-  lloyd_assign<<<lloyd_blocks(m.n), 256, shm, m.s>>>(m.soa, m.n, cents, k, m.assign, m.sums, m.counts, m.changed,
-                                                      m.sse);
+  if (int rc = lloyd_pass(m.soa, m.rows32, m.n, cents, m.cents32, k, m.nearest, m.assign, m.sums, m.counts,
+                          m.changed, m.sse, m.s))
+    return rc;
   pack_acc<<<(tot + 255) / 256, 256, 0, m.s>>>(m.sums, m.counts, m.changed, m.sse, k, acc);
   DPP_LAUNCH_CHECK("lloyd shard assign");
   return DPP_OK;
@@ -518,6 +506,8 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   const int T = 256;
   const int nb = (int)((n + T - 1) / T);
   double *soa = nullptr, *d2 = nullptr, *bsum = nullptr, *cents = nullptr, *sums = nullptr, *sse = nullptr;
+  float *rows32 = nullptr, *cents32 = nullptr;
+  uint8_t* nearest = nullptr;
   int32_t* assign = nullptr;
   unsigned long long *counts = nullptr, *changed = nullptr, *far = nullptr;
   int64_t* pick = nullptr;
@@ -536,6 +526,9 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
     return e;
   };
   DPP_CUDA_CHECK(alloc(&soa, n * KD * sizeof(double)));
+  DPP_CUDA_CHECK(alloc(&rows32, n * KD * sizeof(float)));
+  DPP_CUDA_CHECK(alloc(&cents32, (size_t)k * KD * sizeof(float)));
+  DPP_CUDA_CHECK(alloc(&nearest, (size_t)n));
   DPP_CUDA_CHECK(alloc(&d2, n * sizeof(double)));
   DPP_CUDA_CHECK(alloc(&bsum, nb * sizeof(double)));
   DPP_CUDA_CHECK(alloc(&cents, (size_t)k * KD * sizeof(double)));
@@ -547,7 +540,7 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
   DPP_CUDA_CHECK(alloc(&far, sizeof(unsigned long long)));
   DPP_CUDA_CHECK(alloc(&pick, sizeof(int64_t)));
 
-  to_soa<<<nb, T, 0, s>>>(pts, n, soa);
+  to_soa<<<nb, T, 0, s>>>(pts, n, soa, rows32);
   // k-means++ seeding
   DPP_CUDA_CHECK(cudaMemcpyAsync(cents, pts + first_pick * KD, KD * sizeof(double), cudaMemcpyDeviceToDevice, s));
   for (int j = 1; j < k; ++j) {
@@ -558,18 +551,12 @@ int dpp_kmeans(const double* pts, int64_t n, int k, int64_t first_pick, const do
 
   // Lloyd
   DPP_CUDA_CHECK(cudaMemsetAsync(assign, 0xff, n * sizeof(int32_t), s));  // -1: every point "changes"
-  const size_t shm = lloyd_smem(k);
-  DPP_CUDA_CHECK(cudaFuncSetAttribute(lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   std::vector<unsigned long long> hcounts(k);
   int it = 0;
   // first assignment
   auto assign_pass = [&](unsigned long long* h_changed, double* h_sse) -> int {
-    DPP_CUDA_CHECK(cudaMemsetAsync(sums, 0, (size_t)k * KD * sizeof(double), s));
-    DPP_CUDA_CHECK(cudaMemsetAsync(counts, 0, k * sizeof(unsigned long long), s));
-    DPP_CUDA_CHECK(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), s));
-    DPP_CUDA_CHECK(cudaMemsetAsync(sse, 0, sizeof(double), s));
-    lloyd_assign<<<lloyd_blocks(n), T, shm, s>>>(soa, n, cents, k, assign, sums, counts, changed, sse);
-    DPP_LAUNCH_CHECK("lloyd_assign");
+    if (int rc = lloyd_pass(soa, rows32, n, cents, cents32, k, nearest, assign, sums, counts, changed, sse, s))
+      return rc;
     DPP_CUDA_CHECK(cudaMemcpyAsync(h_changed, changed, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     DPP_CUDA_CHECK(cudaMemcpyAsync(h_sse, sse, sizeof(double), cudaMemcpyDeviceToHost, s));
     DPP_CUDA_CHECK(cudaMemcpyAsync(hcounts.data(), counts, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
