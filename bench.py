@@ -616,7 +616,7 @@ def run_ours(args) -> None:
             secs = []
             for _ in range(3):
                 t0 = time.perf_counter()
-                blob_e2e = aimgc.compress(rgb, 256, 0).to_bytes()
+                blob_e2e = aimgc.compress_to_bytes(rgb, 256, 0)
                 secs.append(time.perf_counter() - t0)
             # codebook quality: SSE over the training blocks, trained vs reference codebook
             norm64, grad = km.block_stats_device(torch.from_numpy(rgb).to(dev), 3, 8192, 8192)
@@ -639,9 +639,9 @@ def run_ours(args) -> None:
             med = sorted(secs)[1]
             compress_e2e.update({
                 "value": round(med, 4), "unit": "s", "mpixel_s": round(8192 * 8192 / med / 1e6, 1),
-                "config": "compress(R=G=B synthetic_image(8192, 8192, seed=7) green, 256, 0): numpy in, H2D, "
-                          "block statistics + gradient filter, k-means++ and Lloyd (binary64, GPU), encode, D2H, "
-                          "container bytes; 1 GPU, median of 3",
+                "config": "compress_to_bytes(R=G=B synthetic_image(8192, 8192, seed=7) green, 256, 0): numpy in, "
+                          "H2D, block statistics + gradient filter, k-means++ and Lloyd (GPU), encode into the "
+                          "device container, D2H, container bytes; 1 GPU, median of 3",
                 "training_blocks": int(train.shape[0]), "bitstream_bytes": len(blob_e2e),
                 "parity": {"codebook_sse_ratio_vs_reference": round(s_ours / s_ref, 5),
                            "sse_trained": s_ours, "sse_reference_codebook": s_ref},

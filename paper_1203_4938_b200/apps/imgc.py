@@ -28,7 +28,8 @@ from ..client import CudaBackend
 from ..model import Instance, Node, Program
 from ..types import DataType, Direction, IOPoint
 
-__all__ = ["read_ppm", "write_ppm", "synthetic_image", "Codebook", "kmeans", "psnr",
+__all__ = ["read_ppm", "write_ppm", "synthetic_image", "Codebook", "kmeans", "psnr", "compress_to_bytes",
+           "decompress_bytes",
            "CompressedImage", "compress", "compress_batch", "decompress", "ycbcr_program",
            "chroma_down_program", "gradient_program", "vq_program", "encode_kernel",
            "encode_program", "SIGMA_STEP", "MAGIC", "NATIVE_TAG"]
@@ -346,6 +347,80 @@ def compress_batch(images, codebooks, *, backend: CudaBackend | None = None, sig
     ops.encode(images, ch, h, w, codebooks.contiguous(), rec, cbp, crp, batch=b,
                shared_codebook=shared, sigma_min=sigma_min)
     return rec, cbp, crp
+
+
+def compress_to_bytes(image, codebook_size: int = 256, seed: int = 0, *, backend: CudaBackend | None = None,
+                      sigma_min: float = 0.25, grad_min: float = 1.0, codebook=None) -> bytes:
+    """``compress(...).to_bytes()`` with the container assembled on the device
+    (SURVEY §8(f) row 4): the encoder writes the record run and both chroma
+    planes at their container offsets in one device buffer, and one D2H
+    brings back the payload — no host-side stacking or re-packing of records.
+    Byte-identical to ``compress(...).to_bytes()``."""
+    import torch
+
+    from .. import ops
+    from .._torch import require_cuda, to_device
+    is_tensor = isinstance(image, torch.Tensor)
+    if not is_tensor:
+        image = np.asarray(image)
+        if image.dtype != np.uint8:
+            raise ValueError("expected an (h, w, 3) uint8 image")
+    elif image.dtype != torch.uint8:
+        raise ValueError("expected an (h, w, 3) uint8 image")
+    h, w, ch = _validate_image(image)
+    if not 1 <= codebook_size <= 256:
+        raise ValueError("codebook size must be in 1..256")
+    dev = require_cuda((backend or CudaBackend()).device)
+    px = image.contiguous().to(dev) if is_tensor else to_device(np.ascontiguousarray(image), dev)
+    if codebook is None:
+        cents = kmeans_codebook(px, ch, h, w, codebook_size, seed, sigma_min, grad_min)
+    else:
+        arr = codebook.centroids if isinstance(codebook, Codebook) else codebook
+        cents = torch.as_tensor(np.ascontiguousarray(arr, np.float32)).to(dev) \
+            if not isinstance(arr, torch.Tensor) else arr.to(dev, torch.float32).contiguous()
+    nb = (h // 4) * (w // 4)
+    payload = torch.empty(5 * nb, dtype=torch.uint8, device=dev)  # records | Cb | Cr, container order
+    ops.encode(px, ch, h, w, cents, payload[:3 * nb], payload[3 * nb:4 * nb], payload[4 * nb:],
+               sigma_min=sigma_min)
+    host = torch.empty(5 * nb, dtype=torch.uint8, pin_memory=True)
+    host.copy_(payload)
+    head = _HEADER.pack(MAGIC, w, h, cents.shape[0], SIGMA_STEP)
+    return head + Codebook(cents.cpu().numpy()).to_bytes() + host.numpy().tobytes()
+
+
+def decompress_bytes(blob, *, backend: CudaBackend | None = None) -> np.ndarray:
+    """``decompress(CompressedImage.from_bytes(blob))`` with the container read
+    on the device: the header is checked on the host, the
+    whole blob goes H2D once and the decoder reads the codebook, records and
+    chroma planes at their container offsets.  Bit-exact with ``decompress``."""
+    import torch
+
+    from .. import ops
+    from .._torch import require_cuda
+    blob = bytes(blob)
+    if len(blob) < _HEADER.size:
+        raise ValueError("truncated container")
+    magic, w, h, ncb, _ = _HEADER.unpack_from(blob)
+    if magic != MAGIC:
+        raise ValueError(f"bad container magic {magic!r}")
+    nb = (w // 4) * (h // 4)
+    off = _HEADER.size
+    need = off + ncb * 64 + 5 * nb
+    if len(blob) < need:
+        raise ValueError(f"truncated container: {len(blob)} bytes, need {need}")
+    dev = require_cuda((backend or CudaBackend()).device)
+    # the codebook floats sit at byte 18: shift the image by 2 bytes so they
+    # land 4-byte aligned on the device
+    pad = (-off) % 4
+    host = torch.empty(need + pad, dtype=torch.uint8, pin_memory=True)
+    host.numpy()[pad:] = np.frombuffer(blob, np.uint8, need)
+    d = host.to(dev, non_blocking=True)
+    cents = d[pad + off:pad + off + ncb * 64].view(torch.float32)
+    base = pad + off + ncb * 64
+    rgb = torch.empty(h * w * 3, dtype=torch.uint8, device=dev)
+    ops.decode(d[base:base + 3 * nb], d[base + 3 * nb:base + 4 * nb], d[base + 4 * nb:base + 5 * nb], cents, h, w,
+               rgb)
+    return rgb.cpu().numpy().reshape(h, w, 3)
 
 
 def decompress(ci: CompressedImage, *, backend: CudaBackend | None = None) -> np.ndarray:

@@ -32,6 +32,22 @@ def test_bitstreams_bit_exact_vs_reference(cuda, imgc_golden):
             pytest.fail(f"{name}: fields differ: {diff}")
 
 
+def test_container_written_and_read_on_the_device(cuda, imgc_golden):
+    """compress_to_bytes / decompress_bytes (the container assembled and
+    parsed on the device) give the reference's own bitstreams and decodes."""
+    from paper_1203_4938_b200.apps import imgc
+    for name in _cases(imgc_golden):
+        blob = imgc_golden[f"{name}_blob"].tobytes()
+        ref = imgc.CompressedImage.from_bytes(blob)
+        assert imgc.compress_to_bytes(imgc_golden[f"{name}_image"], ref.codebook.size,
+                                      codebook=ref.codebook) == blob, name
+        assert np.array_equal(imgc.decompress_bytes(blob), imgc_golden[f"{name}_decoded"]), name
+    with pytest.raises(ValueError, match="truncated container"):
+        imgc.decompress_bytes(blob[:-1])
+    with pytest.raises(ValueError, match="bad container magic"):
+        imgc.decompress_bytes(b"XXXX" + blob[4:])
+
+
 @pytest.mark.parametrize("layout", ["gray", "rgb", "rgba"])
 def test_channel_layouts_agree(cuda, imgc_golden, layout):
     from paper_1203_4938_b200.apps import imgc
