@@ -18,12 +18,17 @@ namespace dpp {
 void set_error(const char* fmt, ...);
 int fail(int code, const char* fmt, ...);
 
+// A failed API call also leaves its code as the runtime's "last error"; it is
+// consumed here so a later launch check does not report it again (e.g. a
+// stream-ordering call refused inside a CUDA-graph capture attempt).
 #define DPP_CUDA_CHECK(expr)                                                         \
   do {                                                                               \
     cudaError_t err__ = (expr);                                                      \
-    if (err__ != cudaSuccess)                                                        \
+    if (err__ != cudaSuccess) {                                                      \
+      (void)cudaGetLastError();                                                      \
       return ::dpp::fail(DPP_ECUDA, "%s failed: %s (%s:%d)", #expr,                  \
                          cudaGetErrorString(err__), __FILE__, __LINE__);             \
+    }                                                                                \
   } while (0)
 
 #define DPP_LAUNCH_CHECK(what)                                                       \

@@ -88,3 +88,20 @@ def test_replay_survives_plan_replacement(cuda, monkeypatch):
     assert np.array_equal(first, again)
     _stream_path(monkeypatch)
     assert np.array_equal(afft.fft(x), again)
+
+
+def test_ring_plans_fall_back_to_the_stream_path(cuda):
+    """A 1024 x 16 2-D node (128 KB: small enough to be a replay candidate)
+    runs the column ring, whose launch orders itself after the plan's previous
+    launch with an event: not capturable, so the call takes the stream path —
+    with the same result as the direct call."""
+    import torch
+
+    from paper_1203_4938_b200 import CudaBackend, DataType, StreamFile, client, ops, run
+    from paper_1203_4938_b200.apps.fft import fft2d_program
+    x = complex_signals(31, (1024, 16))
+    sf = StreamFile(DataType("float", 2), x.reshape(-1).view(np.float32))
+    for _ in range(2):
+        got = run(CudaBackend(), fft2d_program(1024, 16), {"0.x": sf})["0.y"].values.view(np.complex64)
+        ref = ops.fft2d_forward(torch.from_numpy(x).to(cuda), 1024, 16).cpu().numpy().reshape(-1)
+        assert np.array_equal(got, ref)
