@@ -189,6 +189,23 @@ def _pool(threads: int):
     return mp.get_context("spawn").Pool(threads)
 
 
+def timed_flushed(fn, steps: int, stream, flush) -> float:
+    """Average device ms per call of fn() over `steps` calls for inputs smaller
+    than L2: each call is preceded by an untimed write of `flush` (> L2, 126 MB)
+    and timed alone with CUDA events on `stream`."""
+    import torch
+    total = 0.0
+    for _ in range(steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total += e0.elapsed_time(e1)
+    return total / steps
+
+
 def timed(fn, steps: int, stream) -> float:
     """Average device ms per call of fn() over `steps` calls (CUDA events on `stream`)."""
     import torch
@@ -549,7 +566,11 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
         barrier(world)
         csteps = max(3, min(args.steps, 10))
-        c_ms = max_over_ranks(timed(lambda: encode_band(px, 1, h, w, cb, band, bufs), csteps, stream), world)
+        # the 64 MiB frame fits in L2: flush it between timed calls
+        l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        c_ms = max_over_ranks(timed_flushed(lambda: encode_band(px, 1, h, w, cb, band, bufs), csteps, stream,
+                                            l2_flush), world)
+        del l2_flush
         ties = ops.rounding_ties(px[4 * band[0] * w:4 * band[1] * w], 1, 4 * (band[1] - band[0]), w)
         ties = (int(sum_over_ranks(ties[0], world)), int(sum_over_ranks(ties[1], world)))
         # the bitstream: bands concatenated at fixed offsets (imgc.py:295-305)
@@ -580,7 +601,8 @@ def run_ours(args) -> None:
             "scaling": "strong",
             "config": f"synthetic_image(8192, 8192, seed=7) green channel as gray (R=G=B), the 256-entry codebook "
                       f"the reference compress() trained on it (configs[3]; tests/golden/c4_golden.npz), "
-                      f"{world} GPU(s): block-row bands of {bh // world} rows per rank",
+                      f"{world} GPU(s): block-row bands of {bh // world} rows per rank; L2 flushed (256 MB write) "
+                      f"before every timed call",
             "roofline": {"bound": "tensor+fp32 (exact VQ)",
                          "hbm_frac": round(comp_bytes / world / (c_ms / 1e3) / 1e9 / pk["hbm_gbs"], 5),
                          "vq_flop_per_block": 12288,
