@@ -15,6 +15,7 @@ in-process backend runs unchanged — in-process here means the local GPU.
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -157,7 +158,8 @@ def run(backend: CudaBackend | None, program, inputs: dict) -> dict:
 # small host calls: one CUDA graph per (plan, input sizes)
 
 REPLAY_MAX_BYTES = 256 << 10  # host input bytes per call below which run() replays a graph
-_replays: dict = {}
+REPLAY_CACHE = 64             # graphs kept (least recently used evicted with their buffers)
+_replays: OrderedDict = OrderedDict()
 _replays_lock = threading.Lock()
 
 
@@ -268,17 +270,17 @@ def _replay_for(p, free_in: dict, inputs: dict):
     if len(counts) != 1 or not counts.pop() or nbytes > REPLAY_MAX_BYTES:
         return None
     key = (id(p), tuple(sorted(sizes.items())))
-    rp = _replays.get(key)
-    if rp is None:
+    with _replays_lock:
         if key in _replays:
-            return None  # capture failed once for this shape
-        with _replays_lock:
-            if key not in _replays:
-                try:
-                    _replays[key] = _Replay(p, sorted(sizes), sizes)
-                except Exception:  # not capturable (e.g. a node that synchronises): stream path
-                    _replays[key] = None
-            rp = _replays[key]
+            _replays.move_to_end(key)
+            return _replays[key]  # None: capture failed once for this shape
+        try:
+            rp = _Replay(p, sorted(sizes), sizes)
+        except Exception:  # not capturable (e.g. a node that synchronises): stream path
+            rp = None
+        _replays[key] = rp
+        while len(_replays) > REPLAY_CACHE:
+            _replays.popitem(last=False)
     return rp
 
 

@@ -90,3 +90,14 @@ def test_wrong_run_and_faults_reach_the_client(cuda):
     sf = StreamFile(DataType("float", 2), complex_signals(1, 384).view(np.float32))
     with pytest.raises(ClientError, match="run failed"):
         _loopback(fft_program(256), {"0.x": sf}, 384)
+
+
+def test_empty_stream_over_the_data_plane(cuda):
+    """No DATA frames at all: END frames only, empty outputs, zero work-items
+    (the reference's _assemble_chunks accepts END-only runs)."""
+    from paper_1203_4938_b200 import CudaBackend, DataType, StreamFile, run
+    from paper_1203_4938_b200.apps.fft import fft_program
+    sf = StreamFile(DataType("float", 2), np.zeros(0, np.float32))
+    out, items, err = _loopback(fft_program(256), {"0.x": sf}, 1024)
+    assert err is None and items == 0 and out["0.y"].values.size == 0
+    assert run(CudaBackend(), fft_program(256), {"0.x": sf})["0.y"].values.size == 0
