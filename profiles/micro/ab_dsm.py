@@ -1,6 +1,8 @@
 """C2 kernel A/B: the L2-ring kernel vs the DSMEM cluster kernel (DPP_FFT_DSM=2|3
 groups), same input; prints ms per launch (median of 20) and an output digest
-(the two kernels run the same butterflies: digests must match)."""
+(the two kernels run the same butterflies: digests must match).
+The DSMEM kernel is kept unbuilt as fft_dsm_experiment.cu; to rerun, build it
+into an A/B library (build_variant.py) with its DPP_FFT_DSM hook in fft_l2.cu."""
 import hashlib
 import os
 import sys

@@ -1,5 +1,7 @@
 """16384-point FFT A/B: L2-ring kernel vs the register-resident single-CTA
-kernel (DPP_RR16K=1); ms per 2^28 points and the max rel-L2 against numpy."""
+kernel (DPP_RR16K=1); ms per 2^28 points and the max rel-L2 against numpy.
+The register kernel is kept unbuilt as fft16k_rr_experiment.cu; to rerun, build it
+into an A/B library (build_variant.py) with its DPP_RR16K hook in fft.cu."""
 import os
 import sys
 from pathlib import Path
