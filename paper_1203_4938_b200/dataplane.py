@@ -331,11 +331,13 @@ def pump(p, conn, max_in_flight: int = 3) -> int:
                     done.record(s_d2h)
                 outq.put((index, slot, done, frames))
         outq.put(None)
+        thread.join()
     except BaseException:
         outq.put("abort")
+        # a sender blocked on a peer that stopped reading must not hold the
+        # error back: give it a bounded time to drain, then leave it (daemon)
+        thread.join(timeout=30)
         raise
-    finally:
-        thread.join()
     if send_error:
         raise send_error[0]
     return total_items
