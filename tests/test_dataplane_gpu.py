@@ -101,3 +101,20 @@ def test_empty_stream_over_the_data_plane(cuda):
     out, items, err = _loopback(fft_program(256), {"0.x": sf}, 1024)
     assert err is None and items == 0 and out["0.y"].values.size == 0
     assert run(CudaBackend(), fft_program(256), {"0.x": sf})["0.y"].values.size == 0
+
+
+def test_two_input_streams_over_the_data_plane(cuda):
+    """One DATA frame per free input per chunk (the reference's adder node,
+    x and y both free): chunks assemble only when both have arrived."""
+    from paper_1203_4938_b200 import DataType, StreamFile, parse_program, run
+    doc = table2_doc()
+    doc["nodes"] = [[0, {"kernel": "adder"}]]
+    doc["arrows"] = []
+    prog = parse_program(json.dumps(doc))
+    rng = np.random.default_rng(8)
+    xs = StreamFile(DataType("float", 1), rng.standard_normal(3000).astype(np.float32))
+    ys = StreamFile(DataType("float", 1), rng.standard_normal(3000).astype(np.float32))
+    ref = run(None, prog, {"0.x": xs, "0.y": ys})["0.z"].values
+    assert np.array_equal(ref, xs.values + ys.values)
+    out, items, err = _loopback(prog, {"0.x": xs, "0.y": ys}, 512)
+    assert err is None and items == 3000 and np.array_equal(out["0.z"].values, ref)
