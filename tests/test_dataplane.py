@@ -130,3 +130,32 @@ def test_client_helpers_round_trip_through_an_echo_server():
         dp.collect_outputs(a, fout)
     a.close()
     b.close()
+
+
+class _Dribble:
+    """A socket that hands out at most 7 bytes per receive (test_wire.py:14-22
+    of the reference): frames must be reassembled across short reads."""
+
+    def __init__(self, data: bytes):
+        self.data, self.pos = data, 0
+
+    def recv_into(self, view, n):
+        k = min(7, n, len(self.data) - self.pos)
+        view[:k] = self.data[self.pos:self.pos + k]
+        self.pos += k
+        return k
+
+    def recv(self, n):
+        k = min(7, n, len(self.data) - self.pos)
+        out = self.data[self.pos:self.pos + k]
+        self.pos += k
+        return out
+
+
+def test_assemble_across_short_reads():
+    x = np.arange(10, dtype=np.float32)
+    frames = (dp.encode_data_frame("0.x", 0, 5, x.tobytes()) + dp.encode_end_frame("0.x"))
+    got = list(dp.assemble(_Dribble(frames), {"0.x": _fp("0.x")}, lambda n, i, nb: memoryview(bytearray(nb))))
+    assert len(got) == 1 and bytes(got[0][1]["0.x"][0]) == x.tobytes() and got[0][1]["0.x"][1] == 5
+    assert dp.read_handshake(_Dribble(dp.encode_handshake("run-42"))) == "run-42"
+    assert dp.read_reply(_Dribble(dp.encode_reply(False, "busy"))) == (False, "busy")
