@@ -8,6 +8,8 @@
 // and quantisers use round-half-even rint before clipping (imgc.py:375, 400-401).
 #include <cstdint>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace dpp {
@@ -478,63 +480,39 @@ __global__ void __launch_bounds__(256) encode_kernel(const EncodeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core pruned EXACT vector quantisation (tcgen05, kind::tf32).
+// Tensor-core pruned EXACT vector quantisation (tcgen05, kind::f16).
 //
 // The exact search costs 31 binary32 ops per (block, centroid).  Here a
 // 128-block tile is multiplied against the whole 256-entry codebook on the
-// 5th-gen tensor cores (3xTF32 split: n_hi.c_hi + n_hi.c_lo + n_lo.c_hi,
-// fp32 accumulation in TMEM), plus one bias MMA (a constant A column against
-// the per-centroid |c_j|^2/2 + 8), so TMEM holds
+// 5th-gen tensor cores (binary16 hi + lo split of both operands, three MMAs
+// n_hi.c_hi + n_hi.c_lo + n_lo.c_hi, fp32 accumulation in TMEM), plus one bias
+// MMA (a constant A column against the per-centroid |c_j|^2/2 + 8), so TMEM holds
 //   v_j = |c_j|^2/2 + 8 - n.c_j  =  (D_j - |n|^2)/2 + 8  (+- DELTA/2)
-// which is >= D_j/2 >= 0 for every normalised block (|n|^2 <= 16): the fp32
-// bit patterns order like the values, so the epilogue works on integer KEYS
-// — the bits with the centroid index in the low byte — and keeps the best and
-// runner-up with a min/max tournament (2.5 integer min/max per score, 3-input
-// VIMNMX3) instead of compare-and-select chains.
-// When the runner-up is more than 2*DELTA (+ the key quantum) away, the
-// approximate argmin IS the reference's index; otherwise the block is
-// re-checked with the reference's exact binary32 distance over every centroid
-// whose score is within the band, in index order with strict <, so ties
-// resolve to the first index exactly like vq_program (imgc.py:175-178).
-// DELTA bounds |s_j - (D^fp32_j - |n|^2)|: 3xTF32 truncation (3*2^-20 per
-// product), fp32 accumulation of 48 products, the fp32 norm, and the
-// reference's own rounding of D (<= 7u*D); see DESIGN.md.  It is scaled by
-// the codebook's largest norm and checked empirically in tests.
+// which is >= D_j/2 >= 0 for every normalised block (|n|^2 <= 16).  The rank
+// phase (ws::rank_chunk) finds the minimum and counts the scores within the
+// band of it; when the minimum is alone there, the approximate argmin IS the
+// reference's index; otherwise the block is re-checked with the reference's
+// exact binary32 distance over every centroid whose score is within the band,
+// in index order with strict <, so ties resolve to the first index exactly
+// like vq_program (imgc.py:175-178).  DELTA bounds |s_j - (D^fp32_j - |n|^2)|:
+// the split's truncation (2^-22 relative per operand, the same 22 bits as a
+// 3xTF32 split), fp32 accumulation, the fp32 norm, and the reference's own
+// rounding of D (<= 7u*D); see DESIGN.md.  It is scaled by the codebook's
+// largest norm and checked empirically in tests; a codebook outside the
+// binary16 split's range sends every block to the exact path.
 namespace tc {
 constexpr int M = 128;      // blocks per tile (TMEM lanes)
 constexpr int NCB = 256;    // centroids (padded; TMEM columns)
-constexpr int THREADS = 128;
-constexpr int CTAS_PER_SM = 4;
 constexpr float BIAS = 8.f;  // >= |n|^2 / 2 for every normalised block
-// K-major canonical layout, no swizzle: 8-row groups of 8 K-quarters (4 tf32)
-__device__ __forceinline__ uint32_t off(int row, int k) {
-  return (uint32_t)((row >> 3) * 1024 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
-}
-// shared-memory matrix descriptor: lbo = byte offset of the next K-quarter,
-// sbo = byte offset of the next 8-row group (0: every group reads the same rows)
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo = 128, uint32_t sbo = 1024) {
+// shared-memory matrix descriptor, layout SWIZZLE_NONE: lbo = byte offset of
+// the next K core matrix, sbo = byte offset of the next 8-row group (0: every
+// group reads the same rows)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
   return d;                            // base offset 0, layout SWIZZLE_NONE
-}
-// kind::tf32, fp32 accumulate, A/B K-major, N = 128, M = 128
-constexpr int NH = 128;     // centroids per MMA pass = TMEM columns allocated
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) |
-                           ((uint32_t)(M >> 4) << 24);
-constexpr size_t A_BYTES = M * 32 * 4, B_BYTES = NCB * 32 * 4;
-constexpr size_t CN_OFF = A_BYTES + B_BYTES;            // |c_j|^2 (fp32), the re-check filter
-constexpr size_t ABIAS_OFF = CN_OFF + NCB * 4;          // 8 rows x [1 1 0 0 | 0 0 0 0]
-constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;           // per centroid [hi lo 0 0] of |c|^2/2 + 8
-// 53.3 KB -> 4 CTAs per SM, and 4 x 128 TMEM columns = the whole 512
-constexpr size_t SMEM = BBIAS_OFF + NCB * 16;
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
 }
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -542,26 +520,16 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 }  // namespace tc
 
 // Encoder (round 2): one CTA per SM, 16 warps in FOUR identical groups of
 // 128 threads; group g takes local tiles i = g, g + 4, ... (128 blocks each,
 // one block per thread) and runs every phase of its tile itself:
 //   front: pixels -> Y/Cb/Cr (gray: table), chroma bytes, binary64
-//     statistics, normalised block -> the group's A buffer (-n as tf32 hi +
-//     exact lo); the record bytes mu / sigma stay in the thread's registers;
-//   MMA: one elected thread issues the 3xTF32 + bias MMAs of the whole
+//     statistics, normalised block -> the group's A buffer (-n as binary16
+//     hi + lo) and its exact binary32 copy; the record bytes mu / sigma stay
+//     in the thread's registers;
+//   MMA: one elected thread issues the 3 x binary16 + bias MMAs of the whole
 //     codebook (N = 256) into TMEM slot i & 1 (256 columns) once the group
 //     two tiles back has read that slot, and commits mma_done[i & 1];
 //   rank: tcgen05.ld of the row's 256 scores (32 per chunk), chunk minimum
@@ -576,22 +544,38 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 namespace ws {
 constexpr int THREADS = 512;
-constexpr size_t A_BYTES = tc::M * 32 * 4;                  // 16 KB per buffer
-constexpr size_t B_OFF = 0;                                 // codebook hi|lo, 256 x 32 tf32
-constexpr size_t A_OFF = B_OFF + tc::B_BYTES;               // A buffers, one per group
-constexpr size_t CN_OFF = A_OFF + 4 * A_BYTES;              // |c_j|^2
-constexpr size_t ABIAS_OFF = CN_OFF + tc::NCB * 4;          // 8 rows x [1 1 0 0 | 0 0 0 0]
-constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;               // per centroid [hi lo 0 0] of |c|^2/2 + 8
-constexpr size_t LUT_OFF = BBIAS_OFF + tc::NCB * 16;        // gray table, 256 x float4
+// Operands in binary16, split hi + lo (x = hi + lo + e, |e| <= 2^-22 |x|: the
+// same 22 significant bits as the tf32 split, at twice the tensor-core rate;
+// tcgen05 kind::f16 keeps binary16 subnormals, profiles/micro/f16_subnormal.cu).
+// K-major canonical layout without swizzle: 8-row groups of four 16-byte
+// K-chunks (8 halves: hi k 0..7, hi 8..15, lo 0..7, lo 8..15), 512 B per group.
+__device__ __forceinline__ uint32_t off16(int row, int k) {
+  return (uint32_t)((row >> 3) * 512 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
+}
+constexpr size_t A_BYTES = tc::M * 64;                      // 8 KB per buffer (hi | lo halves)
+constexpr size_t B_BYTES = tc::NCB * 64;                    // 16 KB: codebook hi | lo halves
+constexpr size_t B_OFF = 0;
+constexpr size_t A_OFF = B_OFF + B_BYTES;                   // A buffers, one per group
+constexpr size_t AX_OFF = A_OFF + 4 * A_BYTES;              // exact binary32 blocks, 128 x 16 per group
+constexpr size_t CBX_OFF = AX_OFF + 4 * tc::M * 64;         // exact binary32 codebook, 256 x 16
+constexpr size_t CN_OFF = CBX_OFF + tc::NCB * 64;           // |c_j|^2
+constexpr size_t ABIAS_OFF = CN_OFF + tc::NCB * 4;          // 8 rows x [1 1 0 ... 0] (16 halves)
+constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;               // per centroid [hi lo 0 ... 0] of |c|^2/2 + 8
+constexpr size_t LUT_OFF = BBIAS_OFF + tc::NCB * 32;        // gray table, 256 x float4
 constexpr size_t SMEM = LUT_OFF + 256 * 16;
-// kind::tf32, M = 128, N = 256 (the whole codebook in one instruction)
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(tc::NCB >> 3) << 17) |
-                           ((uint32_t)(tc::M >> 4) << 24);
+// kind::f16 (binary16 A and B, fp32 accumulate), M = 128, N = 256 (the whole
+// codebook in one instruction), K = 16 per instruction
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(tc::NCB >> 3) << 17) | ((uint32_t)(tc::M >> 4) << 24);
 __device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+// x -> (hi, lo) binary16 halves; |x - hi - lo| <= 2^-22 |x| (v - hi is exact in binary32)
+__device__ __forceinline__ void split16(float v, __half& hi, __half& lo) {
+  hi = __float2half_rn(v);
+  lo = __float2half_rn(__fsub_rn(v, __half2float(hi)));
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
@@ -652,24 +636,32 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
+  __shared__ int wide_cb;  // codebook outside the binary16 split's range: every block takes the exact path
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = warp >> 2;      // group: local tiles grp, grp + 4, ...
   const int row = tid & 127;      // tile row (block) = TMEM lane of this thread
   const bool aligned4 = (((uintptr_t)a.px | (uintptr_t)a.row_stride | (uintptr_t)a.image_stride) & 3) == 0;
   uint8_t* sA = tsm + ws::A_OFF + grp * ws::A_BYTES;
+  float* sAX = reinterpret_cast<float*>(tsm + ws::AX_OFF) + grp * tc::M * 16;  // exact blocks of this group
+  const float* sCBX = reinterpret_cast<const float*>(tsm + ws::CBX_OFF);
 
   auto stage_codebook = [&](int64_t img) {
     const float* cbk = a.codebook + img * a.codebook_stride;
-    for (int e = tid; e < tc::NCB * 16; e += ws::THREADS) {
-      const int j = e >> 4, k = e & 15;
-      const float c = j < a.ncb ? cbk[j * 16 + k] : 0.f;
-      const float hi = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
-      *reinterpret_cast<float*>(sB + tc::off(j, k)) = hi;
-      *reinterpret_cast<float*>(sB + tc::off(j, 16 + k)) = __fsub_rn(c, hi);  // exact remainder
-    }
     if (tid == 0) {
       cmax_bits = 0;
       zero_key = ~0ull;
+      wide_cb = 0;
+    }
+    __syncthreads();
+    for (int e = tid; e < tc::NCB * 16; e += ws::THREADS) {
+      const int j = e >> 4, k = e & 15;
+      const float c = j < a.ncb ? cbk[j * 16 + k] : 0.f;
+      __half hi, lo;
+      ws::split16(c, hi, lo);
+      *reinterpret_cast<__half*>(sB + ws::off16(j, k)) = hi;
+      *reinterpret_cast<__half*>(sB + ws::off16(j, 16 + k)) = lo;
+      reinterpret_cast<float*>(tsm + ws::CBX_OFF)[e] = c;
+      if (!(fabsf(c) <= 0x1p14f)) wide_cb = 1;  // outside the binary16 split's range (or NaN)
     }
     __syncthreads();
     for (int j = tid; j < tc::NCB; j += ws::THREADS) {
@@ -677,12 +669,16 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
       if (j < a.ncb)
         for (int k = 0; k < 16; ++k) s = fmaf(cbk[j * 16 + k], cbk[j * 16 + k], s);
       scn[j] = j < a.ncb ? s : 1e30f;
-      // bias B operand: |c_j|^2/2 + 8 as tf32 hi + exact remainder (padding
-      // centroids get a huge score so they never win)
-      const float bv = j < a.ncb ? fmaf(0.5f, s, tc::BIAS) : 1e30f;
-      const float bh = __uint_as_float(__float_as_uint(bv) & 0xFFFFE000u);
-      *reinterpret_cast<float4*>(tsm + ws::BBIAS_OFF + (j >> 3) * 128 + (j & 7) * 16) =
-          make_float4(bh, __fsub_rn(bv, bh), 0.f, 0.f);
+      // bias B operand: |c_j|^2/2 + 8 as binary16 hi + lo (padding centroids
+      // get the largest finite score so they never win)
+      const float bv = j < a.ncb ? fmaf(0.5f, s, tc::BIAS) : 60000.f;
+      if (!(bv <= 0x1p15f)) wide_cb = 1;
+      __half bh, bl;
+      ws::split16(bv, bh, bl);
+      uint8_t* brow = tsm + ws::BBIAS_OFF + (j >> 3) * 256 + (j & 7) * 16;  // K-chunks at +0, +128
+      *reinterpret_cast<uint4*>(brow) = make_uint4(__half_as_ushort(bh) | ((uint32_t)__half_as_ushort(bl) << 16), 0u,
+                                                   0u, 0u);
+      *reinterpret_cast<uint4*>(brow + 128) = make_uint4(0u, 0u, 0u, 0u);
       if (j < a.ncb) {
         atomicMax(&cmax_bits, __float_as_uint(s));  // s >= 0: bit order = value order
         // a constant block normalises to exactly 0: its index is the exact
@@ -701,8 +697,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
     __syncthreads();
   };
 
-  if (tid < 64)  // bias A operand: rows [1 1 0 0 | 0 0 0 0] (one 8-row group, sbo = 0)
-    reinterpret_cast<float*>(tsm + ws::ABIAS_OFF)[tid] = (tid < 32 && (tid & 3) < 2) ? 1.f : 0.f;
+  if (tid < 128)  // bias A operand: 8 rows x [1 1 0 ... 0] halves (one 8-row group, sbo = 0)
+    reinterpret_cast<__half*>(tsm + ws::ABIAS_OFF)[tid] = __float2half_rn((tid < 64 && (tid & 7) < 2) ? 1.f : 0.f);
   if (CH == 1) gray_lut_fill(lut, tid, ws::THREADS);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
@@ -770,19 +766,23 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
       // the group's A buffer: its previous reader (the MMA of tile u - 4) was
       // waited for by this group's own rank phase
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float4 hi, lo;
-        float* h = &hi.x;
-        float* l = &lo.x;
+      for (int q = 0; q < 2; ++q) {  // K-chunks of 8: hi at chunk q, lo at chunk 2 + q
+        __half2 hh[4], ll[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float v = -nb[4 * q + e];
-          h[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-          l[e] = __fsub_rn(v, h[e]);
+          __half h0, l0, h1, l1;
+          ws::split16(-nb[8 * q + 2 * e], h0, l0);
+          ws::split16(-nb[8 * q + 2 * e + 1], h1, l1);
+          hh[e] = __halves2half2(h0, h1);
+          ll[e] = __halves2half2(l0, l1);
         }
-        *reinterpret_cast<float4*>(sA + tc::off(row, 4 * q)) = hi;
-        *reinterpret_cast<float4*>(sA + tc::off(row, 16 + 4 * q)) = lo;
+        *reinterpret_cast<uint4*>(sA + ws::off16(row, 8 * q)) = *reinterpret_cast<uint4*>(hh);
+        *reinterpret_cast<uint4*>(sA + ws::off16(row, 16 + 8 * q)) = *reinterpret_cast<uint4*>(ll);
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)  // the exact block for the re-check
+        *reinterpret_cast<float4*>(sAX + row * 16 + 4 * q) =
+            make_float4(nb[4 * q], nb[4 * q + 1], nb[4 * q + 2], nb[4 * q + 3]);
       fence_proxy_async_smem();
       ws::named_sync(1 + grp, 128);
       // ------------------------------------------------------------------ MMA
@@ -791,14 +791,13 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
         mbar_wait(&tmem_free[slot], (use & 1) ^ 1);
         tc::fence_after();
         const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-        // (A quarter, B quarter) pairs: hi.hi, hi.lo, lo.hi over K = 0..7 and 8..15
-        const int aq[6] = {0, 2, 0, 2, 4, 6}, bq[6] = {0, 2, 4, 6, 0, 2};
-#pragma unroll
-        for (int m = 0; m < 6; ++m)
-          ws::mma(tmem, tc::sdesc(a0 + aq[m] * 128), tc::sdesc(b0 + bq[m] * 128), m > 0 ? 1u : 0u);
-        // + |c_j|^2/2 + 8: A = [1 1 0 0 | 0...] in every row, B = [hi lo . . | same quarter again]
+        // hi.hi, hi.lo, lo.hi over K = 0..15 (hi chunks at +0, lo chunks at +256)
+        ws::mma(tmem, tc::sdesc(a0, 128, 512), tc::sdesc(b0, 128, 512), 0u);
+        ws::mma(tmem, tc::sdesc(a0, 128, 512), tc::sdesc(b0 + 256, 128, 512), 1u);
+        ws::mma(tmem, tc::sdesc(a0 + 256, 128, 512), tc::sdesc(b0, 128, 512), 1u);
+        // + |c_j|^2/2 + 8: A = [1 1 0 ... 0] in every row, B = [hi lo 0 ... 0]
         ws::mma(tmem, tc::sdesc(smem_u32(tsm + ws::ABIAS_OFF), 128, 0),
-                tc::sdesc(smem_u32(tsm + ws::BBIAS_OFF), 0, 128), 1u);
+                tc::sdesc(smem_u32(tsm + ws::BBIAS_OFF), 128, 256), 1u);
         tc::commit(&mma_done[grp]);
       }
       // ----------------------------------------------------------------- rank
@@ -837,15 +836,15 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
       const int i1 = (int)gacc - 1024;
       const float v1 = gm;
       const float quant = __int_as_float((__float_as_int(fabsf(v1)) & 0x7F800000)) * 0x1p-15f;  // 2^8 ulps of v1
-      const bool amb = active && !zero && (close || gacc >= 2048.f);
+      const bool amb = active && !zero && (close || gacc >= 2048.f || wide_cb);
       int bj = zero ? zero_idx : i1;
       unsigned amb_lanes = __ballot_sync(0xffffffffu, amb);
       // rare (~0.05 % of blocks): the whole warp re-checks one ambiguous block
       // at a time — each lane rescores 8 centroids on the CUDA cores (fp32,
       // error << DELTA) and runs the reference's exact distance on those inside
       // the band; a lexicographic (distance, index) warp minimum reproduces
-      // "strict <, first index wins" over all 256.  The block comes back from
-      // the group's A buffer (-(hi + lo) == n exactly).
+      // "strict <, first index wins" over all 256.  The block and the codebook
+      // come from their exact binary32 copies.
       while (amb_lanes) {
         const int src = __ffs(amb_lanes) - 1;
         amb_lanes &= amb_lanes - 1;
@@ -853,15 +852,16 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
         float nv[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 hi = *reinterpret_cast<const float4*>(sA + tc::off(srow, 4 * q));
-          const float4 lo = *reinterpret_cast<const float4*>(sA + tc::off(srow, 16 + 4 * q));
-          nv[4 * q] = -__fadd_rn(hi.x, lo.x);
-          nv[4 * q + 1] = -__fadd_rn(hi.y, lo.y);
-          nv[4 * q + 2] = -__fadd_rn(hi.z, lo.z);
-          nv[4 * q + 3] = -__fadd_rn(hi.w, lo.w);
+          const float4 x = *reinterpret_cast<const float4*>(sAX + srow * 16 + 4 * q);
+          nv[4 * q] = x.x;
+          nv[4 * q + 1] = x.y;
+          nv[4 * q + 2] = x.z;
+          nv[4 * q + 3] = x.w;
         }
-        // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8)
-        const float lim = __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
+        // the band in the old score scale s = |c|^2 - 2 n.c = 2 (v - 8); a wide
+        // codebook re-checks every centroid
+        const float lim = wide_cb ? __int_as_float(0x7f800000)
+                                  : __shfl_sync(0xffffffffu, 2.f * (v1 + quant - tc::BIAS) + delta2, src);
         float2 bp[8];
         vq_pack(nv, bp);
         float best = VQ_BEST_INIT;
@@ -871,12 +871,11 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
           float c[16];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 hi = *reinterpret_cast<const float4*>(sB + tc::off(j, 4 * q));
-            const float4 lo = *reinterpret_cast<const float4*>(sB + tc::off(j, 16 + 4 * q));
-            c[4 * q] = __fadd_rn(hi.x, lo.x);  // hi + lo == c exactly
-            c[4 * q + 1] = __fadd_rn(hi.y, lo.y);
-            c[4 * q + 2] = __fadd_rn(hi.z, lo.z);
-            c[4 * q + 3] = __fadd_rn(hi.w, lo.w);
+            const float4 x = *reinterpret_cast<const float4*>(sCBX + j * 16 + 4 * q);
+            c[4 * q] = x.x;
+            c[4 * q + 1] = x.y;
+            c[4 * q + 2] = x.z;
+            c[4 * q + 3] = x.w;
           }
           float dotv = 0.f;
 #pragma unroll
@@ -968,7 +967,7 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
 }
 
 // Nearest centroid of n normalised binary32 16-vectors (the encoder's search:
-// 3xTF32 tensor-core scores, exact binary32 re-check of the ambiguous ones,
+// 3 x binary16 tensor-core scores, exact binary32 re-check of the ambiguous ones,
 // strict <, first index) — the Lloyd assignment of the k-means trainer.
 int vq_assign_tc(const float* vecs, int64_t n, const float* cents, int k, uint8_t* idx, cudaStream_t s) {
   if (n <= 0) return DPP_OK;

@@ -237,18 +237,22 @@ def test_tensor_core_search_equals_exact_search(cuda, seed):
 
 
 def test_tensor_core_search_adversarial_codebooks(cuda):
-    """Duplicated centroids (exact ties -> first index), a tiny codebook, and a
-    codebook with large norms (band scales with |c|max)."""
+    """Duplicated centroids (exact ties -> first index), a tiny codebook, a
+    codebook with large norms (band scales with |c|max) and one beyond the
+    binary16 split's range."""
     rng = np.random.default_rng(4)
     img = io.synthetic_image(256, 128, seed=44)
     y, _, _ = io.ycbcr(img)
     base = io.train_codebook(y, 64, 0)
     dup = np.concatenate([base, base[::-1], base[:5]])       # 133 entries, every vector twice+
     big = (rng.standard_normal((200, 16)) * 6).astype(np.float32)
-    for cents in (dup, base[:3], big):
+    # outside the binary16 split's range (|c| > 2^14): every block takes the exact path
+    wide = np.concatenate([base, np.full((1, 16), 3.0e4, np.float32), -base[:7] * 1.0e5]).astype(np.float32)
+    for cents in (dup, base[:3], big, wide):
         f = io.encode(img, cents)
-        rec, _, _ = _encode_tc(cuda, img, cents)
+        rec, amb, nb = _encode_tc(cuda, img, cents)
         assert np.array_equal(rec[:, 2], f["indices"])
+    assert amb > 0.5 * nb  # the wide codebook re-checked (almost) every block exactly
 
 
 def test_flat_blocks_take_the_zero_block_index(cuda):
