@@ -209,7 +209,7 @@ __global__ void cents_to_f32(const double* __restrict__ c, int k, float* __restr
 }
 
 // Lloyd update after the assignment: the nearest centroid of every point
-// comes from the encoder's tensor-core search (vq_assign_tc: 3xTF32 scores
+// comes from the encoder's tensor-core search (vq_assign_tc: binary16-split scores
 // on tcgen05, exact binary32 re-check of near ties, strict <, first index —
 // SURVEY §8(f) row 2's "GEMM distances on tensor cores"); this pass counts
 // changed assignments, adds the binary64 distance to the chosen centroid
