@@ -39,6 +39,8 @@ def main() -> None:
     res = {}
     res["fft2d_u8_spectrum"] = timed(lambda: ops.fft2d_u8_spectrum(imgs.reshape(-1), side, side, chain.ALPHA,
                                                                    spec.reshape(-1)))
+    one = imgs[:1].reshape(-1)
+    res["  one image x b"] = b * timed(lambda: ops.fft2d_u8_spectrum(one, side, side, chain.ALPHA, spec[0].reshape(-1)))
     res["encode(spectra)"] = timed(lambda: ops.encode(spec, 1, side, side, cbs, rec, cbp, crp, batch=b,
                                                       shared_codebook=False))
     res["encode(noise)"] = timed(lambda: ops.encode(imgs, 1, side, side, cbs, rec, cbp, crp, batch=b,
