@@ -696,14 +696,16 @@ def run_ours(args) -> None:
         barrier(world)
         ms_chain = max_over_ranks(timed(lambda: achain.run_chain(imgs, cbs, backend=be), 2, stream), world)
         per_img = side * side
-        # bytes the two-pass design moves per image: u8 in, complex64 row-pass
-        # result written and read back, u8 spectrum written and read by the
-        # encoder, records + planes out (5 B per 16 px)
-        moved = per_img * (1 + 8 + 8 + 1 + 1) + per_img // 16 * 5
+        # bytes the two-pass design moves per image: u8 in, the row-pass result
+        # written and read back (images go in pairs, one complex transform per
+        # pair: half a complex64 spectrum, 4 B/px, per image), u8 spectrum
+        # written and read by the encoder, records + planes out (5 B per 16 px)
+        moved = per_img * (1 + 4 + 4 + 1 + 1) + per_img // 16 * 5
         compulsory = per_img * 16 + per_img // 16 * 21  # FFT 16 B/px + compression 21 B/block
         chain5.update({
             "config": f"64 x synthetic_image(4096, 4096, seed=1000+i) green channel: to_complex -> fft2d -> "
-                      f"spectrum_u8 -> imgc_encode (reference-trained codebooks of images 0 and 63, alternating), "
+                      f"spectrum_u8 -> imgc_encode (reference-trained codebooks of images 0 and 63, alternating; "
+                      f"the fused FFT pass transforms the images in pairs, z = a + i b), "
                       f"one graph, device-resident edges; {world} GPU(s), {hi - lo} images per rank",
             "value": round(nimg / (ms_chain / 1e3), 2), "unit": "images/s", "ms_per_step": round(ms_chain, 2),
             "scaling": "strong", "mpixel_s": round(nimg * per_img / (ms_chain / 1e3) / 1e6, 1),

@@ -109,7 +109,13 @@ int dpp_fft_twiddle(float* data, int64_t rows, int64_t cols, int64_t col0, int64
  * arithmetic); work: batch * n0 * n1 complex64 (the row-pass result).  Needs
  * n1 = 4096 and n0 in {4096, 16384} (DPP_ENOTSUP otherwise: run the three
  * nodes separately).  The executor uses it when the graph has exactly that
- * chain with no other consumer of the intermediate edges. */
+ * chain with no other consumer of the intermediate edges.  Images go in
+ * pairs, one complex transform of z = a + i b per pair with the two real
+ * spectra separated in the row pass (X[k] = (Z[k] + conj Z[-k]) / 2) and
+ * each written together with its point mirror; the spectra therefore differ
+ * from the three separate nodes by float32 rounding (a count of off-by-one
+ * bytes, within the adapter's tolerance) and are exactly point-symmetric.
+ * An odd last image runs the single-image schedule. */
 int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* out, float alpha, float* work,
                           int64_t batch, void* stream);
 

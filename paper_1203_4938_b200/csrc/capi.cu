@@ -194,8 +194,22 @@ int dpp_fft2d_u8_spectrum(const dpp_fft_plan* plan, const uint8_t* in, uint8_t* 
   auto* w = reinterpret_cast<float2*>(work);
   std::lock_guard<std::mutex> g(const_cast<dpp_fft_plan*>(plan)->mu);
   DeviceScope dev_scope(plan->impl.device);
-  if (int rc = dpp::fft4096_ws_execute_u8(p.rows, in, w, batch * p.n0, s)) return rc;
-  return dpp::fft2d_colring_execute(&p, w, batch, s, out, alpha);
+  // real images in pairs: one complex transform per pair (z = a + i b, the
+  // half spectra separated in the row pass), each spectrum written with its
+  // mirror; an odd last image takes the single-image schedule
+  const int64_t npairs = batch / 2, img = p.n0 * p.n1;
+  if (npairs) {
+    float2* side = w + npairs * img;  // 2 npairs n0 values; work holds batch images
+    if (int rc = dpp::fft4096_ws_execute_u8_pair(p.rows, in, w, npairs, (int)p.n0, s)) return rc;
+    if (int rc = dpp::fft2d_colring_execute(&p, w, npairs, s, out, alpha, nullptr, nullptr, nullptr, false, side))
+      return rc;
+  }
+  if (batch & 1) {
+    const int64_t off = 2 * npairs * img;
+    if (int rc = dpp::fft4096_ws_execute_u8(p.rows, in + off, w, p.n0, s)) return rc;
+    return dpp::fft2d_colring_execute(&p, w, 1, s, out + off, alpha);
+  }
+  return DPP_OK;
 }
 
 int dpp_fft2d_columns_sharded(const dpp_fft_plan* plan, const float* const* slabs, float* const* outs, int nranks,

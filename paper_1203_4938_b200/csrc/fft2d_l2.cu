@@ -45,7 +45,11 @@ struct Args {
   int np, col0, tb;    // PEER: ranks, first column of this rank's block, output to the row slabs
   const float2* twlo;  // TW: W_N^m for m < 16384 ...
   const float2* twhi;  //     ... and W_N^(16384 h): W_N^m = twlo[m & 16383] * twhi[m >> 14]
+  uint8_t* spec = nullptr;  // SPEC on a pair array: the u8 spectra (mirror stores)
+  float2* side = nullptr;  // SPEC on a pair array (non-null): column 0 of each half, raw, for spectrum_pair_fixup
 };
+
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // TW (1-D transforms above 2^17, csrc/fft_large.cu): the four-step twiddle
 // W_N^{r k1} of the column-length (row r) x row-length (column k1) split,
@@ -414,6 +418,11 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
           // P2 block g = (column, k1 / 16): row img C + 16 ct + column of T, viewed [k2][k1]
           const int C = 16 * a.tiles_per_image;
           tma_store_3d(&tout, 16 * (g % (B / 16)), 0, img * C + 16 * ct + g / (B / 16), smem + s * TILE);
+        } else if (SPEC && a.side) {
+          // pair array: column tile ct of half h is image 2 img + h's columns
+          // c0 .. c0 + 15 (the mirror was stored by the compute warps)
+          const int half = a.tiles_per_image / 2, h = ct >= half, c0 = 16 * (ct - h * half);
+          tma_store_3d(&tout, c0, g, (2 * img + h) * 256, smem + s * TILE);
         } else {
           tma_store_3d(&tout, 16 * ct, g, img * 256,
                        SPEC ? reinterpret_cast<const void*>(reinterpret_cast<const uint8_t*>(smem + S * TILE) +
@@ -535,9 +544,49 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
       for (int k = 0; k < 16; ++k) v[k] = lds64((bR ^ (144u * (k & 7))) + 2048 * k);
       dft16c(v);
       if constexpr (SPEC) {
-        uint8_t* o = reinterpret_cast<uint8_t*>(smem + S * TILE) + s * 4096 + 16 * idx + col;
+        if (a.side) {
+          // pair array (fft4096_ws<PAIR> rows): the column is column c of one
+          // image's half spectrum; a real image's |X[-k][C - c]| = |X[k][c]|,
+          // so the tile also lands mirrored.  Column 0 of each half carries
+          // the packed DC / Nyquist columns: raw values to the side buffer.
+          const int half = a.tiles_per_image / 2;
+          const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image, h = ct >= half;
+          if (col == 0 && ct - h * half == 0) {
+            float2* sd = a.side + (size_t)(2 * img + h) * R + g;
 #pragma unroll
-        for (int d1 = 0; d1 < 16; ++d1) o[256 * d1] = spectrum_u8_one(v[d1].x, v[d1].y, a.alpha);  // row k2
+            for (int d1 = 0; d1 < 16; ++d1) sd[B * (idx + 16 * d1)] = v[d1];
+          }
+          bar_compute();  // every warp is done with the stage: the u8 tiles go there
+          uint8_t* o = reinterpret_cast<uint8_t*>(smem + s * TILE);
+#pragma unroll
+          for (int d1 = 0; d1 < 16; ++d1) {
+            const int j = idx + 16 * d1;
+            const int jm = g ? 255 - j : (256 - j) & 255;
+            const uint8_t y = spectrum_u8_one(v[d1].x, v[d1].y, a.alpha);
+            o[16 * j + col] = y;
+            o[4096 + 16 * jm + 15 - col] = y;
+          }
+          bar_compute();
+          // mirror row jm = tid: columns C - c0 - 15 .. C - c0 start one byte
+          // past a 16-byte boundary (TMA cannot store there): 1 + 2 + 4 + 8
+          // (+ 1) byte stores; for c0 = 0 the last byte is the packed column
+          // (written by spectrum_pair_fixup) and is skipped
+          {
+            const int c0 = 16 * (ct - h * half), C = 16 * a.tiles_per_image;  // image width
+            const uint4 w = *reinterpret_cast<const uint4*>(o + 4096 + 16 * tid);
+            const int km = (g ? B - g : 0) + B * tid;
+            uint8_t* dst = a.spec + ((size_t)(2 * img + h) * R + km) * C + (C - c0 - 15);
+            dst[0] = (uint8_t)w.x;
+            *reinterpret_cast<uint16_t*>(dst + 1) = (uint16_t)(w.x >> 8);
+            *reinterpret_cast<uint32_t*>(dst + 3) = __funnelshift_r(w.x, w.y, 24);
+            *reinterpret_cast<uint2*>(dst + 7) = make_uint2(__funnelshift_r(w.y, w.z, 24), __funnelshift_r(w.z, w.w, 24));
+            if (c0) dst[15] = (uint8_t)(w.w >> 24);
+          }
+        } else {
+          uint8_t* o = reinterpret_cast<uint8_t*>(smem + S * TILE) + s * 4096 + 16 * idx + col;
+#pragma unroll
+          for (int d1 = 0; d1 < 16; ++d1) o[256 * d1] = spectrum_u8_one(v[d1].x, v[d1].y, a.alpha);  // row k2
+        }
       } else {
         __syncwarp();
 #pragma unroll
@@ -635,9 +684,28 @@ int fft2d_colring_init(FftPlan* p) {
   return DPP_OK;
 }
 
-// spec_out != nullptr: fused spectrum_u8 — the column pass writes u8 spectra there
+// The DC / Nyquist columns of a pair array's spectra: side holds the column
+// FFT of (A'[r][0]) = (A[r][0], A[r][N/2]) per image, C[k] = P[k] + i Q[k]
+// with P, Q the (Hermitian) spectra of the two real columns; separated as in
+// the row pass and written to columns 0 and C/2.
+__global__ void __launch_bounds__(256) spectrum_pair_fixup(const float2* __restrict__ side, uint8_t* __restrict__ out,
+                                                           int rows, int cols, int64_t n, float alpha) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t img = i / rows;
+  const int k = (int)(i - img * rows);
+  const float2 z = side[i], zm = side[img * rows + ((rows - k) & (rows - 1))];
+  uint8_t* o = out + (size_t)i * cols;
+  o[0] = spectrum_u8_one(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y), alpha);
+  o[cols / 2] = spectrum_u8_one(0.5f * (z.y + zm.y), 0.5f * (zm.x - z.x), alpha);
+}
+
+// spec_out != nullptr: fused spectrum_u8 — the column pass writes u8 spectra there.
+// side != nullptr (with spec_out): `data` is a pair array of `batch` pairs of
+// real images (fft4096_ws<PAIR>); 2 batch spectra are written, side is scratch
+// of 2 batch R complex values.
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s, uint8_t* spec_out,
-                          float alpha, float2* dst, const float2* twlo, const float2* twhi, bool xp) {
+                          float alpha, float2* dst, const float2* twlo, const float2* twhi, bool xp, float2* side) {
   if (!dst) dst = data;
   const int64_t R = p->n0, C = p->n1;
   const int B = (int)(R / 256);
@@ -660,7 +728,8 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
     const uint32_t box[3] = {16, 256, 1};
     if (int rc = make_tmap_c64_3d(&tout, dst, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
   } else if (spec_out) {
-    const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch)};
+    if (side && (C != 4096 || twlo)) return fail(DPP_EINVAL, "pair spectra need 4096-column pair arrays");
+    const uint64_t dims[3] = {(uint64_t)C, (uint64_t)B, (uint64_t)(256 * batch * (side ? 2 : 1))};
     const uint64_t strides[2] = {(uint64_t)C, (uint64_t)C * B};
     const uint32_t box[3] = {16, 1, 256};
     if (int rc = make_tmap_u8_3d(&tout, spec_out, dims, strides, box)) return rc;
@@ -684,6 +753,8 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   a.col0 = a.tb = 0;
   a.twlo = twlo;
   a.twhi = twhi;
+  a.side = spec_out ? side : nullptr;
+  a.spec = spec_out;
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
   const int64_t items = 2 * (int64_t)B * units;
@@ -728,6 +799,11 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   }
   DPP_LAUNCH_CHECK("fft_cols_l2w");
   DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
+  if (spec_out && side) {
+    const int64_t n = 2 * batch * R;
+    spectrum_pair_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(side, spec_out, (int)R, (int)C, n, alpha);
+    DPP_LAUNCH_CHECK("spectrum_pair_fixup");
+  }
   return DPP_OK;
 }
 

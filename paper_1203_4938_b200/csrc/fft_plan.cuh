@@ -67,7 +67,8 @@ int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_
 int fft2d_colring_init(FftPlan* p);
 int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStream_t s,
                           uint8_t* spec_out = nullptr, float alpha = 0.f, float2* dst = nullptr,
-                          const float2* twlo = nullptr, const float2* twhi = nullptr, bool xp = false);
+                          const float2* twlo = nullptr, const float2* twhi = nullptr, bool xp = false,
+                          float2* side = nullptr);
 int fft_large_init(FftPlan* p);
 int fft_twiddle_slab(float2* data, int64_t rows, int64_t cols, int64_t c0, int64_t n, cudaStream_t s);
 int fft_large_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
@@ -80,6 +81,8 @@ int fft128k_l2_execute(const FftPlan* p, const float2* in, float2* out, int64_t 
 int fft4096_ws_init(FftPlan* p);
 int fft4096_ws_execute(const FftPlan* p, const float2* in, float2* out, int64_t batch, cudaStream_t s);
 int fft4096_ws_execute_u8(const FftPlan* p, const uint8_t* in, float2* out, int64_t batch, cudaStream_t s);
+int fft4096_ws_execute_u8_pair(const FftPlan* p, const uint8_t* in, float2* out, int64_t npairs, int rows,
+                               cudaStream_t s);
 int leaf_execute(int k, const float* x, float* y, int64_t items, cudaStream_t s);
 
 }  // namespace dpp
