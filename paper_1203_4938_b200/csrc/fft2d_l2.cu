@@ -45,11 +45,8 @@ struct Args {
   int np, col0, tb;    // PEER: ranks, first column of this rank's block, output to the row slabs
   const float2* twlo;  // TW: W_N^m for m < 16384 ...
   const float2* twhi;  //     ... and W_N^(16384 h): W_N^m = twlo[m & 16383] * twhi[m >> 14]
-  uint8_t* spec = nullptr;  // SPEC on a pair array: the u8 spectra (mirror stores)
   float2* side = nullptr;  // SPEC on a pair array (non-null): column 0 of each half, raw, for spectrum_pair_fixup
 };
-
-__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // TW (1-D transforms above 2^17, csrc/fft_large.cu): the four-step twiddle
 // W_N^{r k1} of the column-length (row r) x row-length (column k1) split,
@@ -420,9 +417,10 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
           tma_store_3d(&tout, 16 * (g % (B / 16)), 0, img * C + 16 * ct + g / (B / 16), smem + s * TILE);
         } else if (SPEC && a.side) {
           // pair array: column tile ct of half h is image 2 img + h's columns
-          // c0 .. c0 + 15 (the mirror was stored by the compute warps)
+          // c0 .. c0 + 15
           const int half = a.tiles_per_image / 2, h = ct >= half, c0 = 16 * (ct - h * half);
-          tma_store_3d(&tout, c0, g, (2 * img + h) * 256, smem + s * TILE);
+          tma_store_3d(&tout, c0, g, (2 * img + h) * 256,
+                       reinterpret_cast<const uint8_t*>(smem + S * TILE) + s * 4096);
         } else {
           tma_store_3d(&tout, 16 * ct, g, img * 256,
                        SPEC ? reinterpret_cast<const void*>(reinterpret_cast<const uint8_t*>(smem + S * TILE) +
@@ -546,9 +544,9 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
       if constexpr (SPEC) {
         if (a.side) {
           // pair array (fft4096_ws<PAIR> rows): the column is column c of one
-          // image's half spectrum; a real image's |X[-k][C - c]| = |X[k][c]|,
-          // so the tile also lands mirrored.  Column 0 of each half carries
-          // the packed DC / Nyquist columns: raw values to the side buffer.
+          // image's half spectrum (the mirrored half is spectrum_pair_mirror's).
+          // Column 0 of each half carries the packed DC / Nyquist columns: raw
+          // values to the side buffer for spectrum_pair_fixup.
           const int half = a.tiles_per_image / 2;
           const int img = u / a.tiles_per_image, ct = u - img * a.tiles_per_image, h = ct >= half;
           if (col == 0 && ct - h * half == 0) {
@@ -556,33 +554,8 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
 #pragma unroll
             for (int d1 = 0; d1 < 16; ++d1) sd[B * (idx + 16 * d1)] = v[d1];
           }
-          bar_compute();  // every warp is done with the stage: the u8 tiles go there
-          uint8_t* o = reinterpret_cast<uint8_t*>(smem + s * TILE);
-#pragma unroll
-          for (int d1 = 0; d1 < 16; ++d1) {
-            const int j = idx + 16 * d1;
-            const int jm = g ? 255 - j : (256 - j) & 255;
-            const uint8_t y = spectrum_u8_one(v[d1].x, v[d1].y, a.alpha);
-            o[16 * j + col] = y;
-            o[4096 + 16 * jm + 15 - col] = y;
-          }
-          bar_compute();
-          // mirror row jm = tid: columns C - c0 - 15 .. C - c0 start one byte
-          // past a 16-byte boundary (TMA cannot store there): 1 + 2 + 4 + 8
-          // (+ 1) byte stores; for c0 = 0 the last byte is the packed column
-          // (written by spectrum_pair_fixup) and is skipped
-          {
-            const int c0 = 16 * (ct - h * half), C = 16 * a.tiles_per_image;  // image width
-            const uint4 w = *reinterpret_cast<const uint4*>(o + 4096 + 16 * tid);
-            const int km = (g ? B - g : 0) + B * tid;
-            uint8_t* dst = a.spec + ((size_t)(2 * img + h) * R + km) * C + (C - c0 - 15);
-            dst[0] = (uint8_t)w.x;
-            *reinterpret_cast<uint16_t*>(dst + 1) = (uint16_t)(w.x >> 8);
-            *reinterpret_cast<uint32_t*>(dst + 3) = __funnelshift_r(w.x, w.y, 24);
-            *reinterpret_cast<uint2*>(dst + 7) = make_uint2(__funnelshift_r(w.y, w.z, 24), __funnelshift_r(w.z, w.w, 24));
-            if (c0) dst[15] = (uint8_t)(w.w >> 24);
-          }
-        } else {
+        }
+        {
           uint8_t* o = reinterpret_cast<uint8_t*>(smem + S * TILE) + s * 4096 + 16 * idx + col;
 #pragma unroll
           for (int d1 = 0; d1 < 16; ++d1) o[256 * d1] = spectrum_u8_one(v[d1].x, v[d1].y, a.alpha);  // row k2
@@ -700,6 +673,34 @@ __global__ void __launch_bounds__(256) spectrum_pair_fixup(const float2* __restr
   o[cols / 2] = spectrum_u8_one(0.5f * (z.y + zm.y), 0.5f * (zm.x - z.x), alpha);
 }
 
+// The mirrored half of pair spectra: out[k][x] = out[(-k) mod R][C - x] for
+// x = C/2 + 1 .. C - 1 (|X[-k][C-x]| = |X[k][x]| for a real image).  One
+// thread per 16-byte output chunk q = C/32 + m of row k: byte i is column
+// c = C - 16q - i of row -k, i.e. byte 16 - i of source chunk a = C/16 - 1 - q
+// (i >= 1) and byte 0 of chunk a + 1 (i = 0).  (Written in the column ring's
+// epilogue instead, the mirror starts one byte past a 16-byte boundary — TMA
+// rejects it — and per-row byte-split stores cost 1 ms per 64 images.)  Byte 0
+// of chunk C/32 is column C/2: spectrum_pair_fixup, which runs after this.
+__global__ void __launch_bounds__(256) spectrum_pair_mirror(uint8_t* __restrict__ out, int rows, int cols,
+                                                            int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cq = cols / 32;
+  const int64_t row = i / cq;
+  const int q = cq + (int)(i - row * cq), a = 2 * cq - 1 - q;
+  const int64_t img = row / rows;
+  const int k = (int)(row - img * rows);
+  const uint8_t* src = out + ((size_t)img * rows + ((rows - k) & (rows - 1))) * cols;
+  const uint4 lo = *reinterpret_cast<const uint4*>(src + 16 * a);
+  const uint32_t b0 = src[16 * (a + 1)];
+  uint4 w;
+  w.x = __byte_perm(b0, lo.w, 0x5670);  // [b0, lo15, lo14, lo13]
+  w.y = __byte_perm(lo.w, lo.z, 0x5670);
+  w.z = __byte_perm(lo.z, lo.y, 0x5670);
+  w.w = __byte_perm(lo.y, lo.x, 0x5670);  // [lo4, lo3, lo2, lo1]
+  *reinterpret_cast<uint4*>(out + ((size_t)img * rows + k) * cols + 16 * q) = w;
+}
+
 // spec_out != nullptr: fused spectrum_u8 — the column pass writes u8 spectra there.
 // side != nullptr (with spec_out): `data` is a pair array of `batch` pairs of
 // real images (fft4096_ws<PAIR>); 2 batch spectra are written, side is scratch
@@ -754,7 +755,6 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   a.twlo = twlo;
   a.twhi = twhi;
   a.side = spec_out ? side : nullptr;
-  a.spec = spec_out;
   DPP_CUDA_CHECK(cudaStreamWaitEvent(s, p->l2_done, 0));
   DPP_CUDA_CHECK(cudaMemsetAsync(p->l2_ctrl, 0, (32 + 2 * (size_t)units) * sizeof(int), s));
   const int64_t items = 2 * (int64_t)B * units;
@@ -800,7 +800,9 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   DPP_LAUNCH_CHECK("fft_cols_l2w");
   DPP_CUDA_CHECK(cudaEventRecord(p->l2_done, s));
   if (spec_out && side) {
-    const int64_t n = 2 * batch * R;
+    const int64_t nm = 2 * batch * R * (C / 32), n = 2 * batch * R;
+    spectrum_pair_mirror<<<(unsigned)((nm + 255) / 256), 256, 0, s>>>(spec_out, (int)R, (int)C, nm);
+    DPP_LAUNCH_CHECK("spectrum_pair_mirror");
     spectrum_pair_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(side, spec_out, (int)R, (int)C, n, alpha);
     DPP_LAUNCH_CHECK("spectrum_pair_fixup");
   }
