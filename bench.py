@@ -720,8 +720,11 @@ def run_ours(args) -> None:
                          "vq_effective_tflops": round(12288 * (hi - lo) * per_img / 16 / (ms_chain / 1e3) / 1e12,
                                                       1)}})
         if rank == 0:
-            spec0 = torch.empty(per_img, dtype=torch.uint8, device=dev)
-            ops.fft2d_u8_spectrum(imgs[0].reshape(-1), side, side, achain.ALPHA, spec0)
+            # image 0's spectrum as the graph computed it: paired with image 1
+            pair0 = min(2, hi - lo)
+            spec0 = torch.empty(pair0 * per_img, dtype=torch.uint8, device=dev)
+            ops.fft2d_u8_spectrum(imgs[:pair0].reshape(-1), side, side, achain.ALPHA, spec0)
+            spec0 = spec0[:per_img]
             nb5 = per_img // 16
             c5_state = (imgs_np[0], cbs_np[0], spec0.view(side, side).cpu().numpy(),
                         {k: v.reshape(-1)[:nb5].cpu().numpy() for k, v in out.items()})
