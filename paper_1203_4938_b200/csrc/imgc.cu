@@ -7,10 +7,12 @@
 // 16-wide reductions (r_m = a_m + a_{m+8}, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))),
 // and quantisers use round-half-even rint before clipping (imgc.py:375, 400-401).
 #include <cstdint>
+#include <cstring>
 
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace dpp {
 
@@ -227,6 +229,9 @@ struct EncodeArgs {
   // blocks are given as normalised binary32 16-vectors, vecs[k][16], and only
   // idx_plane is written
   const float* vecs = nullptr;
+  // CH = 1 on the tensor-core encoder: pixel rows of each tile staged by TMA
+  // (launch_encode_tc sets it when every tile is one 512 x 4 pixel box)
+  int px_tma = 0;
 };
 
 template <int CH>
@@ -282,7 +287,11 @@ __global__ void __launch_bounds__(256) ties_kernel(const EncodeArgs a, unsigned 
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool tm = false, ts = false;
   if (k < nblocks) {
-    const int64_t by = k / bw, bx = k - by * bw;
+    // block row / column in 32 bits (the entry points reject images of
+    // 2^32 blocks or more): a 64-bit division per block was ~3% of the encoder
+    const uint32_t k32 = (uint32_t)k, bw32 = (uint32_t)bw;
+    const uint32_t by32 = k32 / bw32;
+    const int64_t by = by32, bx = k32 - by32 * bw32;
     const uint8_t* base = a.px + img * a.image_stride;
     float yv[16];
 #pragma unroll
@@ -328,7 +337,11 @@ __device__ __forceinline__ bool block_front(const EncodeArgs& a, int64_t img, in
                                             bool aligned4 = false, const uint32_t* pre = nullptr) {
   const int64_t bw = a.width / 4, bh = a.height / 4, nblocks = bw * bh;
   {
-    const int64_t by = k / bw, bx = k - by * bw;
+    // block row / column in 32 bits (the entry points reject images of
+    // 2^32 blocks or more): a 64-bit division per block was ~3% of the encoder
+    const uint32_t k32 = (uint32_t)k, bw32 = (uint32_t)bw;
+    const uint32_t by32 = k32 / bw32;
+    const int64_t by = by32, bx = k32 - by32 * bw32;
     const uint8_t* base = a.px + img * a.image_stride;
     float yv[16];
     float cbs = 0.f, crs = 0.f;
@@ -562,7 +575,9 @@ constexpr size_t CN_OFF = CBX_OFF + tc::NCB * 64;           // |c_j|^2
 constexpr size_t ABIAS_OFF = CN_OFF + tc::NCB * 4;          // 8 rows x [1 1 0 ... 0] (16 halves)
 constexpr size_t BBIAS_OFF = ABIAS_OFF + 256;               // per centroid [hi lo 0 ... 0] of |c|^2/2 + 8
 constexpr size_t LUT_OFF = BBIAS_OFF + tc::NCB * 32;        // gray table, 256 x float4
-constexpr size_t SMEM = LUT_OFF + 256 * 16;
+constexpr size_t PX_OFF = LUT_OFF + 256 * 16;                // gray pixels: 2 boxes of 4 x 512 per group
+constexpr size_t PX_BYTES = 4 * 512;
+constexpr size_t SMEM = PX_OFF + 4 * 2 * PX_BYTES;
 // kind::f16 (binary16 A and B, fp32 accumulate), M = 128, N = 256 (the whole
 // codebook in one instruction), K = 16 per instruction
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(tc::NCB >> 3) << 17) | ((uint32_t)(tc::M >> 4) << 24);
@@ -625,7 +640,8 @@ __device__ __forceinline__ void rank_chunk(const uint32_t (&r)[32], int j0, floa
 
 template <int CH>
 __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeArgs a, int64_t batch,
-                                                                   float delta_scale, unsigned long long* ambiguous) {
+                                                                   float delta_scale, unsigned long long* ambiguous,
+                                                                   const __grid_constant__ CUtensorMap tpx) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   uint8_t* sB = tsm + ws::B_OFF;
   float* scn = reinterpret_cast<float*>(tsm + ws::CN_OFF);  // |c_j|^2
@@ -633,6 +649,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
   // mma_done per GROUP: a barrier shared by the two groups of a TMEM slot
   // would let a group's parity wait see the other group's completed phase
   __shared__ __align__(8) uint64_t mma_done[4], tmem_free[2];
+  __shared__ __align__(8) uint64_t px_full[4][2];  // a.px_tma: pixel box of the group's tile landed
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned int cmax_bits;
   __shared__ unsigned long long zero_key;  // (exact distance of the zero block, index) minimum
@@ -707,6 +724,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
   if (tid == 0) {
     for (int q = 0; q < 4; ++q) mbar_init(&mma_done[q], 1);
     for (int q = 0; q < 2; ++q) mbar_init(&tmem_free[q], 4);
+    for (int q = 0; q < 8; ++q) mbar_init(&px_full[q >> 1][q & 1], 1);
     fence_mbar_init();
   }
   tc::fence_before();
@@ -720,7 +738,18 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
   // tile u belongs to group u & 3 and uses TMEM slot u & 1 for the
   // (u >> 1)-th time
   uint32_t u0 = 0;
-  uint32_t gtiles = 0;  // tiles this group has run (mma_done[grp] phases)
+  uint32_t gtiles = 0;  // tiles this group has run (mma_done[grp] phases, px_full buffer gtiles & 1)
+  const bool px_tma = CH == 1 && a.px_tma;
+  uint32_t* spx = reinterpret_cast<uint32_t*>(tsm + ws::PX_OFF) + grp * (2 * ws::PX_BYTES / 4);
+  // the group's i-th tile of image img: one 512 x 4 pixel box (tiles never
+  // straddle block rows when px_tma is set)
+  auto px_issue = [&](int64_t img, int64_t i, int buf) {
+    const int64_t bw = a.width / 4;
+    const int64_t k0 = (blockIdx.x + (int64_t)gridDim.x * i) * tc::M, by = k0 / bw;
+    mbar_arrive_expect_tx(&px_full[grp][buf], (uint32_t)ws::PX_BYTES);
+    tma_load_3d(spx + buf * (ws::PX_BYTES / 4), &tpx, (int)(k0 - by * bw), (int)(4 * by), (int)img,
+                &px_full[grp][buf]);
+  };
   unsigned long long namb = 0;
   for (int64_t img = 0; img < batch; ++img) {
     stage_codebook(img);
@@ -730,6 +759,10 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
     const float delta2 = 2.f * delta_scale * 1.5e-3f * fmaxf(1.f, (4.f + cmax) * (4.f + cmax) / 64.f);
     const int zero_idx = zero_key == ~0ull ? 0 : (int)(zero_key & 0xffffffffu);
     const int64_t nlocal = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    // the group's first two tiles of this image (every earlier box was consumed)
+    if (px_tma && row == 0)
+      for (int q = 0; q < 2; ++q)
+        if (grp + 4 * q < nlocal) px_issue(img, grp + 4 * q, (gtiles + q) & 1);
     for (int64_t i = grp; i < nlocal; i += 4) {
       const uint32_t u = u0 + (uint32_t)i;
       const int slot = u & 1;
@@ -752,6 +785,13 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
             nb[4 * q + 2] = f.z;
             nb[4 * q + 3] = f.w;
           }
+        } else if (px_tma) {
+          const int buf = gtiles & 1;
+          mbar_wait(&px_full[grp][buf], (gtiles >> 1) & 1);
+          uint32_t w4[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) w4[r] = spx[buf * (ws::PX_BYTES / 4) + r * tc::M + row];
+          block_front<CH, false>(a, img, k, nb, mean, sd, lut, aligned4, w4);
         } else {
           block_front<CH, false>(a, img, k, nb, mean, sd, CH == 1 ? lut : nullptr, aligned4);
         }
@@ -785,6 +825,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) encode_ws_kernel(const EncodeA
             make_float4(nb[4 * q], nb[4 * q + 1], nb[4 * q + 2], nb[4 * q + 3]);
       fence_proxy_async_smem();
       ws::named_sync(1 + grp, 128);
+      // the pixel box is consumed: refill it with the group's tile i + 8
+      if (px_tma && row == 0 && i + 8 < nlocal) px_issue(img, i + 8, gtiles & 1);
       // ------------------------------------------------------------------ MMA
       if (row == 0) {
         // TMEM slot: free once tile u - 2 (another group) has read its scores
@@ -949,12 +991,26 @@ static int launch_encode_tc(const EncodeArgs& a, int channels, int64_t batch, in
   const int64_t want = (ntiles + 3) / 4;  // every group of a CTA busy
   dim3 grid((unsigned)(want < sm_count ? want : sm_count));
   const size_t smem = ws::SMEM;
+  // gray pixels by TMA: every tile one 512 x 4 box (block rows a multiple of
+  // the 128-block tile), 16-byte aligned rows and images
+  EncodeArgs b = a;
+  CUtensorMap tpx;
+  std::memset(&tpx, 0, sizeof(tpx));
+  const int64_t istride = batch > 1 ? a.image_stride : a.row_stride * a.height;
+  b.px_tma = channels == 1 && (a.width / 4) % tc::M == 0 && ((uintptr_t)a.px % 16) == 0 && a.row_stride % 16 == 0 &&
+             istride % 16 == 0 && batch <= 65535;
+  if (b.px_tma) {
+    const uint64_t dims[3] = {(uint64_t)(a.width / 4), (uint64_t)a.height, (uint64_t)(batch > 0 ? batch : 1)};
+    const uint64_t strides[2] = {(uint64_t)a.row_stride, (uint64_t)istride};
+    const uint32_t box[3] = {(uint32_t)tc::M, 4, 1};
+    if (make_tmap_u8_3d(&tpx, a.px, dims, strides, box, true)) b.px_tma = 0;
+  }
   switch (channels) {
 #define TC_CASE(CHN)                                                                                        \
   case CHN:                                                                                                 \
     DPP_CUDA_CHECK(cudaFuncSetAttribute(encode_ws_kernel<CHN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         (int)smem));                                                        \
-    encode_ws_kernel<CHN><<<grid, ws::THREADS, smem, s>>>(a, batch, delta_scale, ambiguous);              \
+    encode_ws_kernel<CHN><<<grid, ws::THREADS, smem, s>>>(b, batch, delta_scale, ambiguous, tpx);         \
     break;
     TC_CASE(0)
     TC_CASE(1)
@@ -1092,6 +1148,8 @@ static int encode_common(const uint8_t* px, int channels, int64_t height, int64_
   if (height % 4 || width % 4 || height < 4 || width < 4)
     return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
                      (long long)height);
+  if ((height / 4) * (width / 4) > 0xffffffffLL)
+    return dpp::fail(DPP_EINVAL, "%lldx%lld has 2^32 or more 4x4 blocks", (long long)width, (long long)height);
   if (n_cb < 1 || n_cb > 256) return dpp::fail(DPP_EINVAL, "codebook size must be in 1..256");
   if (channels != 1 && channels != 3 && channels != 4)
     return dpp::fail(DPP_EINVAL, "channels must be 1, 3 or 4, got %d", channels);
@@ -1143,6 +1201,8 @@ int dpp_imgc_encode_tc_debug(const uint8_t* px, int channels, int64_t height, in
                              int n_cb, uint8_t* records, uint8_t* cb_plane, uint8_t* cr_plane, float delta_scale,
                              unsigned long long* ambiguous, void* stream) {
   if (height % 4 || width % 4 || n_cb < 1 || n_cb > 256) return dpp::fail(DPP_EINVAL, "bad geometry");
+  if ((height / 4) * (width / 4) > 0xffffffffLL)
+    return dpp::fail(DPP_EINVAL, "%lldx%lld has 2^32 or more 4x4 blocks", (long long)width, (long long)height);
   dpp::EncodeArgs a{px, height, width, width * channels, height * width * channels, codebook, n_cb, 0, 0.25,
                     records, cb_plane, cr_plane, nullptr, nullptr, nullptr};
   return dpp::launch_encode_tc(a, channels, 1, (height / 4) * (width / 4), delta_scale, ambiguous,
@@ -1155,6 +1215,8 @@ int dpp_imgc_block_stats(const uint8_t* px, int channels, int64_t height, int64_
   if (height % 4 || width % 4 || height < 4 || width < 4)
     return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
                      (long long)height);
+  if ((height / 4) * (width / 4) > 0xffffffffLL)
+    return dpp::fail(DPP_EINVAL, "%lldx%lld has 2^32 or more 4x4 blocks", (long long)width, (long long)height);
   if (channels != 1 && channels != 3 && channels != 4)
     return dpp::fail(DPP_EINVAL, "channels must be 1, 3 or 4, got %d", channels);
   if (!norm64 || !block_grad) return dpp::fail(DPP_EINVAL, "norm64 and block_grad are required");
@@ -1179,6 +1241,8 @@ int dpp_imgc_rounding_ties(const uint8_t* px, int channels, int64_t height, int6
   if (height % 4 || width % 4 || height < 4 || width < 4)
     return dpp::fail(DPP_EINVAL, "dimensions must be multiples of 4, got %lldx%lld", (long long)width,
                      (long long)height);
+  if ((height / 4) * (width / 4) > 0xffffffffLL)
+    return dpp::fail(DPP_EINVAL, "%lldx%lld has 2^32 or more 4x4 blocks", (long long)width, (long long)height);
   if (channels != 1 && channels != 3 && channels != 4)
     return dpp::fail(DPP_EINVAL, "channels must be 1, 3 or 4, got %d", channels);
   if (!ties) return dpp::fail(DPP_EINVAL, "ties is required");

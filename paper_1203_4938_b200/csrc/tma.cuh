@@ -62,8 +62,9 @@ inline int make_tmap_c64_3d(CUtensorMap* map, const void* base, const uint64_t d
 }
 
 // 3-D view of bytes (u8 planes): dims {d0 (inner), d1, d2}, byte strides {s1, s2}
+// (u32: the same with 4-byte elements, d0 and box[0] counted in words)
 inline int make_tmap_u8_3d(CUtensorMap* map, const void* base, const uint64_t dims[3], const uint64_t strides[2],
-                           const uint32_t box[3]) {
+                           const uint32_t box[3], bool u32 = false) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -77,7 +78,8 @@ inline int make_tmap_u8_3d(CUtensorMap* map, const void* base, const uint64_t di
   const cuuint64_t st[2] = {strides[0], strides[1]};
   const cuuint32_t bx[3] = {box[0], box[1], box[2]};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), d, st, bx, estr,
+  const CUresult r = encode(map, u32 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
+                            const_cast<void*>(base), d, st, bx, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DPP_ECUDA, "cuTensorMapEncodeTiled (u8 3-D) failed (%d)", (int)r);
