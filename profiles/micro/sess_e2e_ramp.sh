@@ -1,3 +1,4 @@
+# (records a session-5 A/B: alt/oldfft/fft.py was the pre-change apps/fft.py; the change was not kept)
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_fft_gpu.py -q -k pinned_host_pipeline > gpurun_out/e2e_test.log 2>&1; tail -2 gpurun_out/e2e_test.log
 for r in 1 2; do
