@@ -208,15 +208,30 @@ __device__ __forceinline__ void p1_b64(float2 (&v)[16], uint32_t b, int warp, in
 // P1 for B = 4 and 8 (1024- and 2048-row images): S = 16 / B whole sequences
 // per thread, in registers (the B = 16 pattern with A = 16 S a-values per
 // item): thread (col, t) owns a = t + 16 s, s < S.
-template <int B>
+// TW: tile row A bb + t + 16 s is row 256 bb + ar of the column (the box
+// takes rows A g .. A g + A of each 256-row block), twiddled by W_N^{row kc}.
+template <int B, bool TW = false>
 __device__ __forceinline__ void p1_bsmall(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
-                                          const Args& a, uint64_t keep_pol) {
+                                          const Args& a, uint64_t keep_pol, int colbase = 0) {
   constexpr int S = 16 / B, A = 16 * S;
   const int col = lane & 15, t = 2 * warp + (lane >> 4);
 #pragma unroll
   for (int s = 0; s < S; ++s)
 #pragma unroll
     for (int bb = 0; bb < B; ++bb) v[s * B + bb] = lds64(b + 8u * swz(A * bb + t + 16 * s, col));
+  if constexpr (TW) {
+    const uint32_t kc = (uint32_t)(colbase + col);
+    const float2 st = tw_big(a, 256u * kc);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      float2 w = tw_big(a, (uint32_t)(A * g + t + 16 * s) * kc);
+#pragma unroll
+      for (int bb = 0; bb < B; ++bb) {
+        v[s * B + bb] = cmul(v[s * B + bb], w);
+        w = cmul(w, st);
+      }
+    }
+  }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     if constexpr (B == 8) {
@@ -518,7 +533,7 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
         if constexpr (B == 64)
           p1_b64<TW, XP>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
         else if constexpr (B < 16)
-          p1_bsmall<B>(v, b, warp, lane, g, slot, a, keep_pol);
+          p1_bsmall<B, TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
         else
           p1_bL<B / 16, XP>(v, b, warp, lane, g, slot, a, keep_pol);
     } else {
@@ -592,12 +607,12 @@ static int colring_prepare(int* ctas) {
                                       (int)smem));
   DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if constexpr (B == 16 || B == 64) {  // the fused spectrum and the four-step twiddle (4096 / 16384 rows)
+  if constexpr (B == 16 || B == 64)  // the fused spectrum (4096 / 16384 rows)
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
+  if constexpr (B <= 16 || B == 64)  // the four-step twiddle (1024, 2048, 4096, 16384 rows)
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  }
   if constexpr (B >= 16) {  // transposed output (first pass of the two-pass large 1-D transform)
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, false, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -760,8 +775,9 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   const int64_t items = 2 * (int64_t)B * units;
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
   const size_t smem = colring_smem(spec_out != nullptr);
-  if ((twlo || spec_out) && B != 16 && B != 64)
-    return fail(DPP_ENOTSUP, "fused spectrum / twiddled column pass needs 4096 or 16384 rows");
+  if (spec_out && B != 16 && B != 64) return fail(DPP_ENOTSUP, "fused spectrum needs 4096 or 16384 rows");
+  if (twlo && B != 4 && B != 8 && B != 16 && B != 64)
+    return fail(DPP_ENOTSUP, "twiddled column pass needs 1024, 2048, 4096 or 16384 rows");
   if (xp) {
     switch (B) {
       case 16: colring::fft_cols_l2w<16, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
@@ -770,10 +786,12 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
       default: colring::fft_cols_l2w<128, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
     }
   } else if (twlo) {
-    if (B == 16)
-      colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
-    else
-      colring::fft_cols_l2w<64, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    switch (B) {
+      case 4: colring::fft_cols_l2w<4, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      case 8: colring::fft_cols_l2w<8, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      case 16: colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      default: colring::fft_cols_l2w<64, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+    }
   } else if (spec_out) {
     if (B == 16)
       colring::fft_cols_l2w<16, true, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
