@@ -2,6 +2,10 @@
 // Each V_* macro selects one measured change; results in profiles/r2_c2_diagnosis.md.
 // Build one:  mkdir -p alt/v && cp profiles/micro/fft_l2_variants.cu alt/v/fft_l2.cu &&
 //   python profiles/micro/build_variant.py NAME alt/v/fft_l2.cu -DV_SW=1   (then profiles/micro/sess_ab_c2.sh alt/NAME.so)
+// Session-5 C2 A/B variants of csrc/fft_l2.cu (NOT built into the library).
+// Each V_* macro selects one measured change; results in profiles/r2_c2_diagnosis.md.
+// Build one:  mkdir -p alt/v && cp profiles/micro/fft_l2_variants.cu alt/v/fft_l2.cu &&
+//   python profiles/micro/build_variant.py NAME alt/v/fft_l2.cu -DV_SW=1   (then profiles/micro/sess_ab_c2.sh alt/NAME.so)
 // FFT node, n = 2^16 (the C2 headline): two-pass four-step with the
 // intermediate kept in L2.
 //
@@ -45,6 +49,9 @@
 #endif
 #ifndef V_RING
 #define V_RING 128
+#endif
+#ifndef V_DIRECT
+#define V_DIRECT 0
 #endif
 #ifndef V_SW
 #define V_SW 0
@@ -110,6 +117,7 @@ struct Args {
   const float2* tw4096;  // W4096^e, e < 256
   const float2* tw65536; // W65536^e, e < 256
   int batch, lag, ring;
+  float2* out;  // V_DIRECT
 };
 
 
@@ -246,8 +254,10 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
         if (!V_CWREL) l2x::red_release_add(cnt1 + t, 1);
       } else {
         if (!V_CWREL && t + a.ring < a.batch) l2x::red_release_add(cnt2 + t, 1);  // lines discarded by the compute warps
-        tma_store_2d_hint(&tout, 16 * g, t * 256, smem + s * TILE, stream_pol);
-        bulk_commit();
+        if (!V_DIRECT) {
+          tma_store_2d_hint(&tout, 16 * g, t * 256, smem + s * TILE, stream_pol);
+          bulk_commit();
+        }
       }
     };
 #if V_DEFER
@@ -433,10 +443,17 @@ fft65536_l2w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CU
 #pragma unroll
       for (int c1 = 0; c1 < 16; ++c1) st_l2_hint(dst + 4096 * c1, v[c1], keep_pol);
     } else {
+      if (V_DIRECT) {
+        // X[16 g + col + 256 d], d = idx + 16 d1, straight from registers
+        float2* o = a.out + (size_t)t * l2x::N + 16 * g + col + 256 * idx;
+#pragma unroll
+        for (int d1 = 0; d1 < 16; ++d1) st_stream(o + 4096 * d1, v[d1]);
+      } else {
       __syncwarp();
       // output tile row d = idx + 16 d1, column col
 #pragma unroll
       for (int d1 = 0; d1 < 16; ++d1) sts64(bA + 2048 * d1, v[d1]);
+      }
     }
     fence_proxy_async_smem();
     __syncwarp();
@@ -524,6 +541,7 @@ int fft65536_l2x_execute(const FftPlan* p, const float2* in, float2* out, int64_
   a.tw4096 = reinterpret_cast<const float2*>(p->l2_tw + 256);
   a.tw65536 = reinterpret_cast<const float2*>(p->l2_tw + 256 + 128);
   a.batch = (int)batch;
+  a.out = out;
   a.lag = (int)(batch < p->l2_lag ? batch : p->l2_lag);
   a.ring = p->l2_ring;
   const int64_t items = 2 * ITEMS * batch;
