@@ -63,8 +63,8 @@ typedef struct dpp_fft_plan dpp_fft_plan;
  *   rank 1: `batch` contiguous transforms of n0 points (n1 ignored).
  *   rank 2: `batch` contiguous n0 x n1 row-major 2-D transforms (n0 256..32768).
  * Sizes must be powers of two >= 2 (same rule as FftPlan, fft.py:133-139);
- * rank 1 up to 2^30 (above 2^20: two HBM passes for 2^22 .. 2^29, three for
- * 2^21 and 2^30; in-place calls stage
+ * rank 1 up to 2^30 (above 2^20: two HBM passes for 2^22 .. 2^30, three for
+ * 2^21; in-place calls stage
  * through a plan-owned scratch of <= 256 MB or one transform, allocated on
  * the first in-place call); in and out must be equal or disjoint.
  * *workspace_bytes receives the scratch the execute call needs (may be 0).

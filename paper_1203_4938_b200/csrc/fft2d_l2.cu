@@ -287,9 +287,10 @@ __device__ __forceinline__ void dftLc(float2* v) {
     for (int q = 0; q < 8; ++q) v[q] = t[q];
   }
 }
-template <int L, bool XP = false>
+// TW: tile row 16 b1 + A b0 + alo is row 256 (L b1 + b0) + ar of the column.
+template <int L, bool TW = false, bool XP = false>
 __device__ __forceinline__ void p1_bL(float2 (&v)[16], uint32_t b, int warp, int lane, int g, float2* slot,
-                                      const Args& a, uint64_t keep_pol) {
+                                      const Args& a, uint64_t keep_pol, int colbase = 0) {
   constexpr int A = 16 / L, Q = 16 / L;  // a values per item (A * L = 16), m0 values per lane
   // 256 threads = 16 columns x A a-values x L lanes
   constexpr int SPW = 32 / L;  // sequences per warp
@@ -298,6 +299,10 @@ __device__ __forceinline__ void p1_bL(float2 (&v)[16], uint32_t b, int warp, int
   const int col = rest & 15, alo = (rest >> 4) & (A - 1);
 #pragma unroll
   for (int b1 = 0; b1 < 16; ++b1) v[b1] = lds64(b + 8u * swz(16 * b1 + A * b0 + alo, col));
+  {
+    const uint32_t kc = (uint32_t)(colbase + col);
+    p1_twiddle<TW>(v, a, (uint32_t)(256 * b0 + A * g + alo) * kc, 256u * L * kc);
+  }
   dft16c(v);  // v[m0]
   {
     const float2 wb = __ldg(a.twr + 256 * b0);  // W_B^b0 = W_R^{256 b0}
@@ -535,7 +540,7 @@ fft_cols_l2w(const __grid_constant__ typename MapSet<PEER>::type tin,
         else if constexpr (B < 16)
           p1_bsmall<B, TW>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
         else
-          p1_bL<B / 16, XP>(v, b, warp, lane, g, slot, a, keep_pol);
+          p1_bL<B / 16, TW, XP>(v, b, warp, lane, g, slot, a, keep_pol, colbase);
     } else {
       if (DISCARD) discard_l2(slot + 4096 * g + 16 * (tid & 255));
       const uint32_t bA = b + offA;
@@ -610,9 +615,9 @@ static int colring_prepare(int* ctas) {
   if constexpr (B == 16 || B == 64)  // the fused spectrum (4096 / 16384 rows)
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colring_smem(true)));
-  if constexpr (B <= 16 || B == 64)  // the four-step twiddle (1024, 2048, 4096, 16384 rows)
-    DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the four-step twiddle (every ring length)
+  DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if constexpr (B >= 16) {  // transposed output (first pass of the two-pass large 1-D transform)
     DPP_CUDA_CHECK(cudaFuncSetAttribute(colring::fft_cols_l2w<B, true, false, false, false, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -776,8 +781,7 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
   const unsigned grid = (unsigned)(items < p->col_ring_ctas ? items : p->col_ring_ctas);
   const size_t smem = colring_smem(spec_out != nullptr);
   if (spec_out && B != 16 && B != 64) return fail(DPP_ENOTSUP, "fused spectrum needs 4096 or 16384 rows");
-  if (twlo && B != 4 && B != 8 && B != 16 && B != 64)
-    return fail(DPP_ENOTSUP, "twiddled column pass needs 1024, 2048, 4096 or 16384 rows");
+
   if (xp) {
     switch (B) {
       case 16: colring::fft_cols_l2w<16, true, false, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
@@ -790,7 +794,9 @@ int fft2d_colring_execute(const FftPlan* p, float2* data, int64_t batch, cudaStr
       case 4: colring::fft_cols_l2w<4, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
       case 8: colring::fft_cols_l2w<8, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
       case 16: colring::fft_cols_l2w<16, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
-      default: colring::fft_cols_l2w<64, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
+      case 32: colring::fft_cols_l2w<32, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      case 64: colring::fft_cols_l2w<64, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a); break;
+      default: colring::fft_cols_l2w<128, true, false, false, true><<<grid, colring::THREADS, smem, s>>>(tin, tout, a);
     }
   } else if (spec_out) {
     if (B == 16)

@@ -13,7 +13,7 @@
 // FFT passes are the tuned kernels, the transpose is a 32 x 32 tile copy.
 //
 // Two passes (32 B per point) when A is 4096 .. 32768 and Bc is 1024, 2048,
-// 4096 or 16384 (n = 2^22 .. 2^29): steps 1 + 2 become ONE column ring over the A x Bc view of x
+// 4096, 16384 or 32768 (n = 2^22 .. 2^30): steps 1 + 2 become ONE column ring over the A x Bc view of x
 // (A-point FFTs down its Bc columns) whose ring slot is laid out per column,
 // so each P2 block writes 16 consecutive k1 of one row of T by a TMA box
 // (fft2d_l2.cu, XP) — the transpose rides on the exchange that the column
@@ -78,12 +78,14 @@ int fft_twiddle_slab(float2* data, int64_t rows, int64_t cols, int64_t c0, int64
 
 int fft_large_init(FftPlan* p) {
   const int64_t n = p->n0;
-  // two passes need the second factor Bc in {1024, 2048, 4096, 16384} (the
-  // twiddled ring) and the first A in 4096 .. 32768 (the transposed-output ring)
+  // two passes need the second factor Bc in {1024, 2048, 4096, 16384, 32768}
+  // (the twiddled ring) and the first A in 4096 .. 32768 (the transposed-output ring)
   auto xp_ok = [](int64_t a) { return a >= 4096 && a <= 32768; };
   int64_t bc = n <= (1LL << 24) ? 4096 : 16384;
-  if (!xp_ok(n / bc))  // another column length that gives two passes (2^22: 4096 x 1024, 2^23: 4096 x 2048)
-    for (const int64_t c : {20480 - bc, (int64_t)2048, (int64_t)1024})
+  // another column length that gives two passes (2^22: 4096 x 1024, 2^23:
+  // 4096 x 2048, 2^30: 32768 x 32768)
+  if (!xp_ok(n / bc))
+    for (const int64_t c : {20480 - bc, (int64_t)2048, (int64_t)1024, (int64_t)32768})
       if (xp_ok(n / c)) {
         bc = c;
         break;

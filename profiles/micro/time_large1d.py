@@ -8,7 +8,7 @@ import torch  # noqa: E402
 from paper_1203_4938_b200 import ops  # noqa: E402
 
 dev = torch.device("cuda:0")
-for m, batch in ((21, 32), (22, 16), (23, 8), (24, 4), (25, 2), (26, 1), (27, 1), (28, 1), (29, 1)):
+for m, batch in ((21, 32), (22, 16), (23, 8), (24, 4), (25, 2), (26, 1), (27, 1), (28, 1), (29, 1), (30, 1)):
     n = 1 << m
     x = torch.randn((batch, n), dtype=torch.complex64, device=dev)
     y = torch.empty_like(x)

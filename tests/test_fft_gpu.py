@@ -366,16 +366,17 @@ def test_two_pass_large_sizes_vs_numpy_f64(cuda, m):
     assert rel_l2(y, ref) <= tol(n)
 
 
-def test_two_pass_2e29_identities_and_sampled_bins(cuda):
-    """2^29 (32768 x 16384; 4 GiB in + out): sum_k X[k] = N x[0], Parseval,
-    and three bins against their direct binary64 DFT sums (exact integer
-    phases (k n) mod N)."""
+@pytest.mark.parametrize("m", [29, 30])
+def test_two_pass_largest_identities_and_sampled_bins(cuda, m):
+    """2^29 (32768 x 16384; 4 GiB in + out) and 2^30 (32768 x 32768; 8 GiB in
+    + out): sum_k X[k] = N x[0], Parseval, and three bins against their
+    direct binary64 DFT sums (exact integer phases (k n) mod N)."""
     import torch
 
     from paper_1203_4938_b200 import ops
-    n = 1 << 29
+    n = 1 << m
     assert "two passes" in ops.fft_plan(1, n, 1, 1, cuda).description
-    gen = torch.Generator(device=cuda).manual_seed(29)
+    gen = torch.Generator(device=cuda).manual_seed(m)
     x = torch.randn(n, dtype=torch.complex64, device=cuda, generator=gen)
     y = ops.fft_forward(x, n)
     s = y.to(torch.complex128).sum()
