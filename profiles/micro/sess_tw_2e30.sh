@@ -1,3 +1,4 @@
+# (session-5 record: alt/old30.so was built from the previous commit's fft_large.cu with build_variant.py)
 # two-pass 2^30 (32768 x 32768: twiddled 32768-row ring): parity tests, then
 # large-size timings with this tree's library and alt/old30.so (pre-change dispatch)
 mkdir -p gpurun_out
