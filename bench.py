@@ -763,8 +763,7 @@ def run_ours(args) -> None:
 
             def step1d():
                 ops.fft_forward(part, n1d, out=out1)
-            how = ("local, two HBM passes: 16384-point column ring with transposed output, twiddled 16384-point "
-                   "column ring")
+            how = "local, two HBM passes: " + ops.fft_plan(1, n1d, 1, 1, dev).description
         else:
             from paper_1203_4938_b200.distributed import fft1d_row_sharded
 

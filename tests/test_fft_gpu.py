@@ -349,8 +349,8 @@ def test_sizes_above_2e17_vs_oracle(cuda, m, batch):
 
 @pytest.mark.parametrize("m", [22, 23, 26, 27, 28])
 def test_two_pass_large_sizes_vs_numpy_f64(cuda, m):
-    """2^22 (4096 x 1024), 2^23 (4096 x 2048), 2^26 (4096 x 16384), 2^27
-    (8192 x 16384) and 2^28 (16384 x 16384): the two-pass schedule
+    """2^22 (4096 x 1024), 2^23 (4096 x 2048), 2^26 (8192 x 8192), 2^27
+    (16384 x 8192) and 2^28 (32768 x 8192): the two-pass schedule
     against numpy's binary64 FFT of the same signal (the oracle port would
     take minutes here; it is pinned to numpy at smaller sizes)."""
     import numpy as np
